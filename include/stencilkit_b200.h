@@ -1,0 +1,168 @@
+/*
+ * stencilkit_b200 -- C ABI of the B200-native loop-of-stencil-reduce engine.
+ *
+ * This is the drop-in boundary for the reference package `stencilkit`
+ * (/root/reference/pkg/src/stencilkit).  The reference's plugin point is the
+ * Executor protocol (loop.py:124-137: begin(plan, grid) -> run; step(run) ->
+ * reduce value; finish(run) -> (Grid, CopyLedger); abort(run)) driven by
+ * _drive (loop.py:198-224).  The Python `DeviceExecutor` in
+ * paper_1609_04567_b200/partition.py implements that protocol on top of the
+ * functions below, loaded with ctypes.
+ *
+ * Conventions: plain C types only; every function returns SK_OK (0) or an
+ * SK_ERR_* code and never throws; sk_last_error() gives the message of the
+ * calling thread's last failure.  Pointers named d_* are CUDA device
+ * pointers (any allocator); `stream` is a cudaStream_t (NULL = legacy
+ * default stream).  One sk_run is single-owner; distinct runs are
+ * independent and may be driven from different host threads.
+ */
+#ifndef STENCILKIT_B200_H
+#define STENCILKIT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SK_ABI_VERSION 1
+
+/* status codes */
+#define SK_OK 0
+#define SK_ERR_ARG 1
+#define SK_ERR_CUDA 2
+#define SK_ERR_STATE 3
+#define SK_ERR_UNSUPPORTED 4
+
+/* element types */
+#define SK_U8 1
+#define SK_F32 3
+#define SK_F64 4
+
+/* device kernels: the reference's block kernels, one per app
+ * (apps/helmholtz.py:85-92, apps/sobel.py:47-66, apps/denoise.py:105-135,
+ *  apps/denoise.py:209-246, apps/life.py:35-43) */
+#define SK_KERNEL_HELMHOLTZ 1 /* params: ax, ay, b, keep, relax           */
+#define SK_KERNEL_SOBEL 2     /* u8 in/out, off-image reads = centre      */
+#define SK_KERNEL_AMF 3       /* params: wmax; u8 in, u8 0/1 out          */
+#define SK_KERNEL_RESTORE 4   /* params: beta, phi_eps; f64 work, u8 mask */
+#define SK_KERNEL_LIFE 5      /* u8 0/1 board                             */
+
+/* Combinator kinds (patterns.py:195-211) and Delta kinds
+ * (apps/helmholtz.py:98-100, apps/denoise.py:252-254) */
+#define SK_REDUCE_SUM 1
+#define SK_REDUCE_MAX 2
+#define SK_DELTA_NONE 0
+#define SK_DELTA_ABS 1
+#define SK_DELTA_SQUARE 2
+
+/* device-evaluable loop conditions (Condition, loop.py:43-57):
+ *   HOST     : never stops on the device; the host evaluates its predicate
+ *   LT       : value < a                      (e.g. max|delta| < 1e-4)
+ *   RMS_LT   : sqrt(value / n) < a            (apps/helmholtz.py:128-131)
+ *   MEAN_LT  : value / n < a                  (apps/denoise.py:282-283)
+ *   ITER_GE  : iteration >= n                 (stop_after, loop.py:70-74)
+ * all evaluated in fp64 exactly as the Python predicate. */
+#define SK_COND_HOST 0
+#define SK_COND_LT 1
+#define SK_COND_RMS_LT 2
+#define SK_COND_MEAN_LT 3
+#define SK_COND_ITER_GE 4
+
+/* One loop plan = the reference's LoopPlan (loop.py:101-110) reduced to
+ * device terms.  Grids are row-major with a row pitch in elements. */
+typedef struct sk_plan {
+  int32_t kernel;      /* SK_KERNEL_* */
+  int32_t dtype;       /* element type of the iterated grid */
+  int64_t rows, cols;  /* owned rows x columns */
+  int32_t partitions;  /* row partitions for the reduce fold (partition.py:187-195) */
+  int32_t reduce_op;   /* SK_REDUCE_* */
+  int32_t delta_op;    /* SK_DELTA_* */
+  int32_t halo_top;    /* 1 if buffers carry a neighbour-owned row above row 0 */
+  int32_t halo_bottom; /* 1 if buffers carry a neighbour-owned row below row rows-1 */
+  int32_t flags;       /* SK_FLAG_* */
+  double identity;     /* combinator identity */
+  double params[8];    /* kernel parameters, see SK_KERNEL_* */
+} sk_plan;
+
+#define SK_FLAG_TIMING 1 /* record CUDA events around every sweep launch */
+
+typedef struct sk_cond {
+  int32_t kind; /* SK_COND_* */
+  int32_t pad;
+  double a;
+  double n;
+  int64_t max_iterations;
+} sk_cond;
+
+typedef struct sk_run sk_run;
+
+const char* sk_last_error(void);
+int sk_abi_version(void);
+
+/* Executor.begin (loop.py:124-137; ParallelExecutor.begin partition.py:607-625).
+ * d_src   : the input grid (read, never written: loop.py:157-161), layout
+ *           (halo_top + rows + halo_bottom) x src_pitch.  Iteration 1 reads it.
+ * d_env   : read-only environment grid (same row layout; env_pitch), or NULL.
+ *           Helmholtz: f (same dtype).  Restore: the 0/1 noise map (u8).
+ * d_buf0/1: the executor's two iteration buffers (PartitionSet.buffer_allocations,
+ *           partition.py:160), layout (halo_top + rows + halo_bottom) x pitch.
+ * pitch / src_pitch / env_pitch must be multiples of 16 bytes / sizeof(elem)
+ * and the pointers 16-byte aligned (the Python layer stages otherwise). */
+int sk_run_begin(const sk_plan* plan, const void* d_src, int64_t src_pitch,
+                 const void* d_env, int64_t env_pitch, void* d_buf0, void* d_buf1,
+                 int64_t pitch, void* stream, sk_run** out);
+
+/* Executor.step (loop.py:209-213): enqueue `n` iterations (async).  Iterations
+ * past a device-decided stop are no-ops. */
+int sk_run_launch(sk_run* run, int32_t n);
+
+/* Wait for iteration `it` (1-based, already launched) and return its
+ * combined reduce value. */
+int sk_run_value(sk_run* run, int64_t it, double* value);
+
+/* Whole _drive loop on the device (loop.py:198-224) for a device-evaluable
+ * condition: one CUDA-graph launch with a conditional WHILE node (or batched
+ * launches when timing).  Outputs: completed iterations, the final reduce
+ * value, and whether the cap was hit without the condition holding. */
+int sk_run_loop(sk_run* run, const sk_cond* cond, int64_t* iterations, double* final_value,
+                int32_t* exhausted);
+
+/* Executor.finish (partition.py:658-661): which iteration buffer holds the
+ * result of iteration `it`: 0 or 1 (-1 means the input itself, it == 0). */
+int sk_run_result(sk_run* run, int64_t it, int32_t* which);
+
+/* Device address of the run's status value (double) for the most recent
+ * iteration -- the per-rank partial a multi-GPU driver all-gathers. */
+int sk_run_value_ptr(sk_run* run, void** d_value);
+
+/* Sum of CUDA-event durations of all timed sweep launches (SK_FLAG_TIMING). */
+int sk_run_kernel_time(sk_run* run, double* total_ms, int64_t* launches);
+
+/* Number of sweep kernels this run has launched (including no-op launches
+ * past a device-decided stop). */
+int sk_run_launches(sk_run* run, int64_t* launches);
+
+/* Executor.abort / end of finish: release device state. */
+int sk_run_destroy(sk_run* run);
+
+/* ---- batched map-only stencils for frame streams (config C2) -----------
+ * Sobel edge magnitude (apps/sobel.py:47-66) over `frames` frames of
+ * rows x cols u8 pixels, frame f at d_in + f*frame_stride (pitch bytes per
+ * row), output likewise; d_sums[f] receives the frame's pixel sum (the
+ * reference's _pixel_sum reduce, apps/sobel.py:73-74). */
+int sk_sobel_frames(const uint8_t* d_in, int64_t in_pitch, int64_t in_frame_stride, uint8_t* d_out,
+                    int64_t out_pitch, int64_t out_frame_stride, int32_t frames, int64_t rows,
+                    int64_t cols, int64_t* d_sums, void* stream);
+
+/* Adaptive-median noise detection (apps/denoise.py:105-135) over frames;
+ * d_counts[f] receives the number of flagged pixels. */
+int sk_amf_frames(const uint8_t* d_in, int64_t in_pitch, int64_t in_frame_stride, uint8_t* d_mask,
+                  int64_t mask_pitch, int64_t mask_frame_stride, int32_t frames, int64_t rows,
+                  int64_t cols, int32_t wmax, int64_t* d_counts, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* STENCILKIT_B200_H */

@@ -1,0 +1,23 @@
+"""B200-native loop-of-stencil-reduce (arxiv 1609.04567), drop-in for `stencilkit`.
+
+Same pattern vocabulary as the reference package (stencilkit/__init__.py):
+grids, elemental functions, combinators, the four loop variants,
+partitioned loops and stream composition.  Underneath, every stencil sweep
+is a hand-written sm_100a kernel fused with its reduce and loop test; the
+loop runs on the GPU.
+"""
+
+from .grid import (ABSENT, Grid, GridError, IndexedNeighborhood, Neighborhood, grid_get_padded,
+                   grid_new, indexed_neighborhood_at, is_absent, neighborhood_at)
+from .ledger import CopyLedger
+from .loop import (Condition, DeviceCond, LoopReport, LoopState, loop_stencil_reduce,
+                   loop_stencil_reduce_d, loop_stencil_reduce_i, loop_stencil_reduce_s,
+                   stop_after)
+from .partition import (DeploymentMode, DeviceExecutor, WorkerGroup, model_ledger,
+                        parallel_loop)
+from .patterns import (Combinator, Delta, DeviceKernel, DeviceUnsupported, ElementalFn,
+                       StencilError, abs_change, apply_to_all, map_pattern, max_combinator,
+                       reduce_all, reduce_pattern, sq_change, stencil_apply,
+                       stencil_apply_indexed, sum_combinator)
+
+__version__ = "0.1.0"

@@ -1,0 +1,195 @@
+// Shared device-side pieces of the stencil-reduce engine (sm_100a).
+//
+// Every sweep kernel in this library has the same epilogue: per-thread
+// delta/reduce accumulation -> warp shuffle -> CTA partial -> a
+// last-CTA-done "finalize" that folds the CTA partials per partition, folds
+// the partitions in ascending order from the combinator identity (the
+// reference's host combine, partition.py:642-646), evaluates the loop
+// condition on the device (loop.py:209-218) and publishes the value.  That is
+// what lets the whole repeat-until loop stay on the GPU (one kernel launch
+// per iteration, or one CUDA-graph launch for the whole loop).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <math.h>
+
+#include "../../include/stencilkit_b200.h"
+
+namespace sk {
+
+constexpr int kRing = 64;  // host-visible per-iteration value ring
+
+// Device-resident loop status.  Written only by the finalizing CTA of each
+// iteration; read by every CTA of the next launch (kernel boundary orders it).
+struct Status {
+  long long iter;       // completed iterations
+  int stop;             // 1 once the loop is over (cond true or cap hit)
+  int exhausted;        // cap hit without cond
+  int cond_true;        // the device condition said stop
+  int pad;
+  double value;         // combined reduce value of iteration `iter`
+  unsigned int ticket;  // last-CTA-done counter
+  unsigned int work;    // dynamic work-chunk counter
+};
+
+constexpr int kMaxParts = 64;
+
+struct CondDev {
+  int kind;             // SK_COND_*
+  double a;             // threshold
+  double n;             // divisor (RMS/MEAN) or iteration count (ITER_GE)
+  long long max_it;
+};
+
+// Everything the shared epilogue needs; embedded in each kernel's params.
+struct LoopCtl {
+  Status* st;
+  double* partials;         // one slot per work chunk
+  int nparts;
+  int part_chunk[kMaxParts + 1];  // chunk ranges per partition (ascending rows)
+  int reduce;               // SK_REDUCE_SUM / SK_REDUCE_MAX
+  double identity;
+  volatile double* ring;    // host-mapped per-iteration values (may be null)
+  CondDev cond;
+  cudaGraphConditionalHandle gh;
+  int use_graph;
+};
+
+// ---------------------------------------------------------------- exact math
+// The reference evaluates numpy/Python expressions op by op: no fused
+// multiply-add, IEEE division and sqrt.  These wrappers pin that down
+// regardless of -fmad (the library is also built with -fmad=false).
+__device__ __forceinline__ float xmul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float xadd(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float xsub(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float xdiv(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ double xmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double xadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double xsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double xdiv(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ double xsqrt(double a) { return __dsqrt_rn(a); }
+
+// ---------------------------------------------------------------- reduce ops
+// MAX follows np.max: NaN propagates.
+__device__ __forceinline__ double rmax(double a, double b) {
+  if (a != a) return a;
+  if (b != b) return b;
+  return b > a ? b : a;
+}
+__device__ __forceinline__ double rcombine(int op, double a, double b) {
+  return op == SK_REDUCE_MAX ? rmax(a, b) : a + b;
+}
+__device__ __forceinline__ double rneutral(int op) {
+  return op == SK_REDUCE_MAX ? -INFINITY : 0.0;
+}
+
+template <int BLOCK>
+__device__ __forceinline__ double block_reduce(int op, double v, double* sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = rcombine(op, v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  double r = rneutral(op);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int w = 0; w < BLOCK / 32; ++w) r = rcombine(op, r, sh[w]);
+  }
+  __syncthreads();
+  return r;  // valid in thread 0
+}
+
+// Device-side loop condition (the recognised threshold forms of the
+// reference's conditions; loop.py:43-57, apps/helmholtz.py:128-131,
+// apps/denoise.py:282-283, loop.py:70-74).  Same fp64 expression as the
+// Python predicate, so the decision is bit-identical.
+__device__ __forceinline__ int eval_cond(const CondDev& c, double v, long long it) {
+  switch (c.kind) {
+    case SK_COND_LT: return v < c.a;
+    case SK_COND_RMS_LT: return xsqrt(xdiv(v, c.n)) < c.a;
+    case SK_COND_MEAN_LT: return xdiv(v, c.n) < c.a;
+    case SK_COND_ITER_GE: return (double)it >= c.n;
+    default: return 0;  // SK_COND_HOST: the host decides
+  }
+}
+
+// Loop-entry check shared by all sweep kernels.  Returns the iteration
+// number this launch computes, or 0 if the loop is already over (an
+// over-launched iteration: every CTA returns without touching memory).
+__device__ __forceinline__ long long loop_enter(const LoopCtl& L) {
+  volatile Status* st = L.st;
+  if (st->stop) {
+    // a graph WHILE body entered after the loop ended must still clear the
+    // condition, or the graph would spin
+    if (L.use_graph && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(L.gh, 0u);
+    return 0;
+  }
+  return st->iter + 1;
+}
+
+// Dynamic work distribution: CTAs pull chunk ids until exhausted.  Every
+// chunk writes its own partial (partials[chunk]), so the reduce tree depends
+// only on the chunk geometry -- never on which CTA ran which chunk.
+__device__ __forceinline__ int next_chunk(const LoopCtl& L, int* s_chunk) {
+  __syncthreads();
+  if (threadIdx.x == 0) *s_chunk = (int)atomicAdd(&L.st->work, 1u);
+  __syncthreads();
+  return *s_chunk;
+}
+
+// Last-CTA-done finalize, called by every CTA once it runs out of chunks.
+// Folds chunk partials per partition (fixed strided split + fixed tree),
+// then partitions in ascending order from the identity, evaluates the
+// condition and publishes the iteration.
+template <int BLOCK>
+__device__ void loop_finalize(const LoopCtl& L, long long it, double* sh) {
+  __shared__ int s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    unsigned prev = atomicAdd(&L.st->ticket, 1u);
+    s_last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int op = L.reduce;
+  double acc = L.identity;  // host combine from the identity, ascending partitions
+  for (int p = 0; p < L.nparts; ++p) {
+    const int c0 = L.part_chunk[p], c1 = L.part_chunk[p + 1];
+    double v;
+    if (op == SK_REDUCE_SUM) {
+      // the partition's CTA partials: fixed strided split over the block,
+      // then a fixed shuffle/warp tree -- same order on every run
+      double t = 0.0;
+      for (int c = c0 + (int)threadIdx.x; c < c1; c += BLOCK) t += __ldcg(&L.partials[c]);
+      v = block_reduce<BLOCK>(op, t, sh);
+    } else {
+      double t = -INFINITY;
+      for (int c = c0 + (int)threadIdx.x; c < c1; c += BLOCK) t = rmax(t, __ldcg(&L.partials[c]));
+      v = block_reduce<BLOCK>(op, t, sh);
+    }
+    if (threadIdx.x == 0) {
+      if (op == SK_REDUCE_SUM) acc = acc + v;
+      else acc = (v < acc) ? acc : v;  // max_combinator fold (patterns.py:205-211)
+    }
+  }
+  if (threadIdx.x == 0) {
+    Status* st = L.st;
+    int c = eval_cond(L.cond, acc, it);
+    int capped = (it >= L.cond.max_it);
+    st->value = acc;
+    st->cond_true = c;
+    st->exhausted = (!c && capped);
+    st->stop = c || capped;
+    st->iter = it;
+    st->ticket = 0;
+    st->work = 0;
+    if (L.ring) L.ring[it % kRing] = acc;
+    __threadfence_system();
+    if (L.use_graph) cudaGraphSetConditional(L.gh, (c || capped) ? 0u : 1u);
+  }
+}
+
+}  // namespace sk

@@ -1,0 +1,259 @@
+// Fused Helmholtz/Jacobi sweep: 5-point relaxed stencil + per-element delta
+// + reduce + loop control, one launch per iteration.
+//
+// Reference: the block kernel apps/helmholtz.py:85-92 (point form :72-83),
+// constants :55-65, delta/sum :98-105; the per-partition reduce in
+// _step_block (partition.py:302-316); the host combine partition.py:642-646.
+//
+// HBM-bound: 12 B/cell (fp32: read u 4 + read f 4 + write u' 4), 24 B/cell
+// fp64.  Each thread owns 16 contiguous bytes of a row (float4 / double2)
+// and marches down a chunk of rows keeping the up/centre/down rows in
+// registers, so every u row is read from DRAM once per chunk (+2 halo rows
+// per chunk); horizontal neighbours come from warp shuffles plus one scalar
+// load at each warp edge.  Loads for U rows are issued before any of them
+// is consumed (memory-level parallelism).  Work is pulled in chunks from an
+// atomic counter (balanced tail); each chunk writes its own reduce partial so
+// the reduce tree is independent of scheduling.
+//
+// Exactness: the update is evaluated op by op in the reference's expression
+// order with round-to-nearest intrinsics (no FMA contraction, IEEE
+// division): keep*c + ((relax*((f + ax*(l+r)) + ay*(u+d))) / b), constants
+// rounded to the grid dtype first (numpy NEP 50).  Results are bit-identical
+// to the reference block route in fp32 and fp64.
+#include "sk_internal.h"
+#include "sk_sweep.cuh"
+
+namespace sk {
+
+template <typename T>
+struct HelmArgs {
+  Sweep2D g;
+  LoopCtl L;
+  T ax, ay, b, keep, relax;
+};
+
+template <typename T>
+__device__ __forceinline__ T tabs(T x);
+template <>
+__device__ __forceinline__ float tabs<float>(float x) { return fabsf(x); }
+template <>
+__device__ __forceinline__ double tabs<double>(double x) { return fabs(x); }
+
+template <typename T, int BLOCK, int U, int DELTA, int REDUCE>
+__global__ void __launch_bounds__(BLOCK)
+    helmholtz_sweep(const __grid_constant__ HelmArgs<T> a) {
+  constexpr int VEC = 16 / sizeof(T);
+  constexpr unsigned FULL = 0xffffffffu;
+  __shared__ double sh[BLOCK / 32];
+  __shared__ int s_chunk;
+
+  const long long it = loop_enter(a.L);
+  if (it == 0) return;
+  const Sweep2D& g = a.g;
+  const T* front;
+  long long fp;
+  if (it == 1) {
+    front = static_cast<const T*>(g.src);
+    fp = g.src_pitch;
+  } else {
+    front = static_cast<const T*>(g.buf[(it - 1) & 1]);
+    fp = g.pitch;
+  }
+  T* back = static_cast<T*>(g.buf[it & 1]) + (long long)g.halo_top * g.pitch;
+  front += (long long)g.halo_top * fp;
+  const T* env = static_cast<const T*>(g.env) + (long long)g.halo_top * g.env_pitch;
+  const int lane = threadIdx.x & 31;
+  const int cols = g.cols, rows = g.rows;
+  const T ax = a.ax, ay = a.ay, b = a.b, keep = a.keep, relax = a.relax;
+  const int total = a.L.part_chunk[a.L.nparts];
+
+  for (int c = next_chunk(a.L, &s_chunk); c < total; c = next_chunk(a.L, &s_chunk)) {
+    int cb, r0, r1;
+    chunk_geom(a.L, g, c, &cb, &r0, &r1);
+    const int col = cb * (BLOCK * VEC) + (int)threadIdx.x * VEC;
+    const bool active = col < cols;
+    const bool has_l = (lane == 0) && col > 0 && col - 1 < cols;
+    const bool has_r = (lane == 31) && col + VEC < cols;
+
+    auto ldrow = [&](int r) -> V16<T> {
+      if (!active || (r < 0 && !g.halo_top) || (r >= rows && !g.halo_bottom)) return zero16<T>();
+      return ldg16(front + (long long)r * fp + col);
+    };
+
+    double acc = REDUCE == SK_REDUCE_MAX ? -INFINITY : 0.0;
+    V16<T> up = ldrow(r0 - 1);
+    V16<T> cen = ldrow(r0);
+    for (int r = r0; r < r1; r += U) {
+      V16<T> dn[U], fv[U];
+      T ls[U], rs[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int rr = r + u;
+        if (rr < r1) {
+          dn[u] = ldrow(rr + 1);
+          fv[u] = active ? ldg16(env + (long long)rr * g.env_pitch + col) : zero16<T>();
+          ls[u] = has_l ? __ldg(front + (long long)rr * fp + col - 1) : T(0);
+          rs[u] = has_r ? __ldg(front + (long long)rr * fp + col + VEC) : T(0);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int rr = r + u;
+        if (rr < r1) {
+          T lv = __shfl_up_sync(FULL, cen.v[VEC - 1], 1);
+          T rv = __shfl_down_sync(FULL, cen.v[0], 1);
+          if (lane == 0) lv = ls[u];
+          if (lane == 31) rv = rs[u];
+          V16<T> o;
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) {
+            const T l = e == 0 ? lv : cen.v[e - 1];
+            T rt = e == VEC - 1 ? rv : cen.v[e + 1];
+            if (col + e + 1 >= cols) rt = T(0);  // Dirichlet-0 right border
+            const T cc = cen.v[e];
+            const T t3 = xadd(fv[u].v[e], xmul(ax, xadd(l, rt)));
+            const T t6 = xadd(t3, xmul(ay, xadd(up.v[e], dn[u].v[e])));
+            const T out = xadd(xmul(keep, cc), xdiv(xmul(relax, t6), b));
+            if (col + e < cols) {
+              o.v[e] = out;
+              T dd;
+              if (DELTA == SK_DELTA_ABS) {
+                dd = tabs(xsub(out, cc));
+              } else if (DELTA == SK_DELTA_SQUARE) {
+                const T d = xsub(out, cc);
+                dd = xmul(d, d);
+              } else {
+                dd = out;
+              }
+              if (REDUCE == SK_REDUCE_MAX) acc = rmax(acc, (double)dd);
+              else acc = acc + (double)dd;
+            } else {
+              o.v[e] = T(0);  // keep row padding zero
+            }
+          }
+          if (active) *reinterpret_cast<float4*>(back + (long long)rr * g.pitch + col) = o.raw;
+          up = cen;
+          cen = dn[u];
+        }
+      }
+    }
+    const double v = block_reduce<BLOCK>(REDUCE, acc, sh);
+    if (threadIdx.x == 0) a.L.partials[c] = v;
+  }
+  loop_finalize<BLOCK>(a.L, it, sh);
+}
+
+// ---------------------------------------------------------------- host side
+
+namespace {
+
+constexpr int kBlock = 128;
+constexpr int kUnroll = 4;
+
+template <typename T>
+using KernelFn = void (*)(const HelmArgs<T>);
+
+template <typename T>
+KernelFn<T> pick(int delta, int reduce) {
+#define SK_H(D, R) \
+  if (delta == D && reduce == R) return helmholtz_sweep<T, kBlock, kUnroll, D, R>;
+  SK_H(SK_DELTA_NONE, SK_REDUCE_SUM)
+  SK_H(SK_DELTA_NONE, SK_REDUCE_MAX)
+  SK_H(SK_DELTA_ABS, SK_REDUCE_SUM)
+  SK_H(SK_DELTA_ABS, SK_REDUCE_MAX)
+  SK_H(SK_DELTA_SQUARE, SK_REDUCE_SUM)
+  SK_H(SK_DELTA_SQUARE, SK_REDUCE_MAX)
+#undef SK_H
+  return nullptr;
+}
+
+template <typename T>
+int setup_t(sk_run* r) {
+  const sk_plan& p = r->plan;
+  constexpr int VEC = 16 / sizeof(T);
+  KernelFn<T> fn = pick<T>(p.delta_op, p.reduce_op);
+  if (!fn) {
+    set_error("helmholtz: unsupported delta/reduce combination");
+    return SK_ERR_UNSUPPORTED;
+  }
+  int per_sm = 0;
+  SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kBlock, 0));
+  const int sms = device_sms(r->device);
+  const long long cells = (long long)p.rows * p.cols;
+  r->block = kBlock;
+  r->colblocks = (int)((p.cols + kBlock * VEC - 1) / (kBlock * VEC));
+  // Chunk height: tall enough that the 2 extra halo-row reads per chunk are
+  // noise (>= 64 rows when the grid is large), short enough that every SM
+  // gets several chunks (dynamic balance) on small grids.
+  const long long slots = (long long)sms * per_sm;
+  long long want_chunks = slots * 4;
+  long long ch = (p.rows * (long long)r->colblocks + want_chunks - 1) / want_chunks;
+  if (cells >= (1ll << 24)) ch = ch < 64 ? 64 : ch;
+  ch = ch < 4 ? 4 : (ch > 256 ? 256 : ch);
+  r->chunk_rows = (int)ch;
+  int nchunks = 0;
+  r->part_chunk[0] = 0;
+  for (int i = 0; i < r->nparts; ++i) {
+    const int pr = r->part_row[i + 1] - r->part_row[i];
+    nchunks += ((pr + r->chunk_rows - 1) / r->chunk_rows) * r->colblocks;
+    r->part_chunk[i + 1] = nchunks;
+  }
+  r->nchunks = nchunks;
+  r->grid = (int)(slots < nchunks ? slots : nchunks);
+  if (r->grid < 1) r->grid = 1;
+  return SK_OK;
+}
+
+template <typename T>
+int launch_t(sk_run* r, const LoopCtl& L, cudaStream_t s) {
+  const sk_plan& p = r->plan;
+  HelmArgs<T> a;
+  Sweep2D& g = a.g;
+  g.src = r->src;
+  g.src_pitch = r->src_pitch;
+  g.buf[0] = r->buf[0];
+  g.buf[1] = r->buf[1];
+  g.pitch = r->pitch;
+  g.env = r->env;
+  g.env_pitch = r->env_pitch;
+  g.rows = (int)p.rows;
+  g.cols = (int)p.cols;
+  g.halo_top = p.halo_top;
+  g.halo_bottom = p.halo_bottom;
+  g.colblocks = r->colblocks;
+  g.chunk_rows = r->chunk_rows;
+  for (int i = 0; i <= r->nparts; ++i) g.part_row[i] = r->part_row[i];
+  a.L = L;
+  // Python-float constants meet the grid dtype: rounded once (NEP 50).
+  a.ax = (T)p.params[0];
+  a.ay = (T)p.params[1];
+  a.b = (T)p.params[2];
+  a.keep = (T)p.params[3];
+  a.relax = (T)p.params[4];
+  KernelFn<T> fn = pick<T>(p.delta_op, p.reduce_op);
+  fn<<<r->grid, r->block, 0, s>>>(a);
+  SK_CUDA(cudaGetLastError());
+  return SK_OK;
+}
+
+int setup(sk_run* r) {
+  if (r->plan.dtype == SK_F32) return setup_t<float>(r);
+  if (r->plan.dtype == SK_F64) return setup_t<double>(r);
+  set_error("helmholtz: dtype must be f32 or f64");
+  return SK_ERR_UNSUPPORTED;
+}
+
+int launch(sk_run* r, const LoopCtl& L, cudaStream_t s) {
+  if (r->plan.dtype == SK_F32) return launch_t<float>(r, L, s);
+  return launch_t<double>(r, L, s);
+}
+
+void teardown(sk_run*) {}
+
+const KernelOps kOps = {setup, launch, teardown};
+
+}  // namespace
+
+const KernelOps* helmholtz_ops() { return &kOps; }
+
+}  // namespace sk

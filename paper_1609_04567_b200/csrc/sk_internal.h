@@ -1,0 +1,85 @@
+// Host-side internals shared by the runtime and the per-kernel launchers.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <string>
+#include <vector>
+
+#include "sk_common.cuh"
+
+struct sk_run;
+
+namespace sk {
+
+void set_error(const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+
+#define SK_CUDA(call)                                 \
+  do {                                                \
+    cudaError_t _e = (call);                          \
+    if (_e != cudaSuccess) return ::sk::cuda_fail(_e, #call); \
+  } while (0)
+
+// Per-kernel hooks.  `setup` sizes the launch (grid, work chunks) and any
+// extra device state; `launch` enqueues one sweep with the given loop
+// control on stream `s` (plain launch or into a graph capture).
+struct KernelOps {
+  int (*setup)(sk_run*);
+  int (*launch)(sk_run*, const LoopCtl&, cudaStream_t);
+  void (*teardown)(sk_run*);
+};
+
+const KernelOps* helmholtz_ops();
+const KernelOps* life_ops();
+const KernelOps* restore_ops();
+const KernelOps* map_ops();  // single-pass map kernels (Sobel, AMF) behind the run API
+
+int device_sms(int device);
+
+}  // namespace sk
+
+struct sk_run {
+  sk_plan plan{};
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  const sk::KernelOps* ops = nullptr;
+
+  const void* src = nullptr;
+  long long src_pitch = 0;
+  const void* env = nullptr;
+  long long env_pitch = 0;
+  void* buf[2] = {nullptr, nullptr};
+  long long pitch = 0;
+
+  // launch geometry (filled by ops->setup)
+  int grid = 0;
+  int block = 0;
+  int nparts = 1;
+  int part_row[sk::kMaxParts + 1] = {};
+  int part_chunk[sk::kMaxParts + 1] = {};
+  int colblocks = 1;
+  int chunk_rows = 1;
+  int nchunks = 0;
+
+  // device loop state
+  sk::Status* d_status = nullptr;
+  double* d_partials = nullptr;
+  double* h_ring = nullptr;  // pinned, mapped
+  double* d_ring = nullptr;  // device alias of h_ring
+  long long launched = 0;
+  long long total_launches = 0;
+  cudaEvent_t ev_done[sk::kRing] = {};
+
+  // optional per-sweep timing
+  bool timing = false;
+  std::vector<cudaEvent_t> t_start, t_stop;
+  std::vector<long long> t_iter;
+
+  // device-loop graph
+  cudaGraphExec_t gexec = nullptr;
+  cudaStream_t cap_stream = nullptr;
+
+  // kernel-specific device state (restore: flagged list, change flags)
+  void* aux[8] = {};
+  long long aux_n[8] = {};
+};

@@ -1,0 +1,401 @@
+// C-ABI runtime: run lifecycle, device-resident loop (CUDA graph WHILE),
+// host-driven steps with asynchronous value readback, per-sweep timing.
+//
+// Maps the reference's Executor protocol (loop.py:124-137) and _drive
+// (loop.py:198-224) onto device state.  See include/stencilkit_b200.h.
+#include <mutex>
+#include <string>
+
+#include "sk_internal.h"
+
+namespace sk {
+
+static thread_local std::string g_err;
+
+void set_error(const std::string& msg) { g_err = msg; }
+
+int cuda_fail(cudaError_t e, const char* what) {
+  g_err = std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+  return SK_ERR_CUDA;
+}
+
+int device_sms(int device) {
+  static std::mutex mu;
+  static int cache[64] = {};
+  std::lock_guard<std::mutex> lk(mu);
+  if (device < 0 || device >= 64) return 148;
+  if (!cache[device]) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || n <= 0)
+      n = 148;
+    cache[device] = n;
+  }
+  return cache[device];
+}
+
+// Pinned, device-mapped arena for the per-run value rings (cudaHostAlloc is
+// far too slow to call per run in a frame stream).
+namespace {
+struct RingArena {
+  std::mutex mu;
+  double* host = nullptr;
+  double* dev = nullptr;
+  std::vector<int> free_slots;
+  static constexpr int kSlots = 1024;
+  int init() {
+    if (host) return SK_OK;
+    SK_CUDA(cudaHostAlloc(&host, sizeof(double) * kRing * kSlots, cudaHostAllocMapped | cudaHostAllocPortable));
+    SK_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dev), host, 0));
+    for (int i = kSlots - 1; i >= 0; --i) free_slots.push_back(i);
+    return SK_OK;
+  }
+  int take(double** h, double** d) {
+    std::lock_guard<std::mutex> lk(mu);
+    int rc = init();
+    if (rc) return rc;
+    if (free_slots.empty()) {
+      set_error("too many concurrent runs (value-ring arena exhausted)");
+      return SK_ERR_STATE;
+    }
+    int s = free_slots.back();
+    free_slots.pop_back();
+    *h = host + (size_t)s * kRing;
+    *d = dev + (size_t)s * kRing;
+    return SK_OK;
+  }
+  void give(double* h) {
+    if (!h) return;
+    std::lock_guard<std::mutex> lk(mu);
+    free_slots.push_back((int)((h - host) / kRing));
+  }
+};
+RingArena g_ring;
+}  // namespace
+
+static LoopCtl make_ctl(sk_run* r, const sk_cond* c, bool graph, cudaGraphConditionalHandle gh) {
+  LoopCtl L;
+  L.st = r->d_status;
+  L.partials = r->d_partials;
+  L.nparts = r->nparts;
+  for (int i = 0; i <= r->nparts; ++i) L.part_chunk[i] = r->part_chunk[i];
+  L.reduce = r->plan.reduce_op;
+  L.identity = r->plan.identity;
+  L.ring = r->d_ring;
+  if (c) {
+    L.cond.kind = c->kind;
+    L.cond.a = c->a;
+    L.cond.n = c->n;
+    L.cond.max_it = c->max_iterations;
+  } else {
+    L.cond.kind = SK_COND_HOST;
+    L.cond.a = 0;
+    L.cond.n = 0;
+    L.cond.max_it = (long long)1 << 62;
+  }
+  L.gh = gh;
+  L.use_graph = graph ? 1 : 0;
+  return L;
+}
+
+static int launch_timed(sk_run* r, const LoopCtl& L) {
+  cudaEvent_t a = nullptr, b = nullptr;
+  if (r->timing) {
+    SK_CUDA(cudaEventCreate(&a));
+    SK_CUDA(cudaEventCreate(&b));
+    SK_CUDA(cudaEventRecord(a, r->stream));
+  }
+  int rc = r->ops->launch(r, L, r->stream);
+  if (rc) return rc;
+  r->launched += 1;
+  r->total_launches += 1;
+  if (r->timing) {
+    SK_CUDA(cudaEventRecord(b, r->stream));
+    r->t_start.push_back(a);
+    r->t_stop.push_back(b);
+    r->t_iter.push_back(r->launched);
+  }
+  cudaEvent_t& ev = r->ev_done[r->launched % kRing];
+  if (!ev) SK_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  SK_CUDA(cudaEventRecord(ev, r->stream));
+  return SK_OK;
+}
+
+}  // namespace sk
+
+using namespace sk;
+
+extern "C" {
+
+const char* sk_last_error(void) { return g_err.c_str(); }
+
+int sk_abi_version(void) { return SK_ABI_VERSION; }
+
+int sk_run_begin(const sk_plan* plan, const void* d_src, int64_t src_pitch, const void* d_env,
+                 int64_t env_pitch, void* d_buf0, void* d_buf1, int64_t pitch, void* stream,
+                 sk_run** out) {
+  if (!plan || !out || !d_buf0 || !d_buf1 || !d_src) {
+    set_error("sk_run_begin: null argument");
+    return SK_ERR_ARG;
+  }
+  *out = nullptr;
+  if (plan->rows < 1 || plan->cols < 1 || plan->rows > (1ll << 31) - 2 || plan->cols > (1ll << 31) - 64) {
+    set_error("sk_run_begin: bad grid dims");
+    return SK_ERR_ARG;
+  }
+  if (plan->partitions < 1 || plan->partitions > kMaxParts || plan->partitions > plan->rows) {
+    set_error("sk_run_begin: partitions must be in [1, min(rows, 64)]");
+    return SK_ERR_ARG;
+  }
+  if (plan->reduce_op != SK_REDUCE_SUM && plan->reduce_op != SK_REDUCE_MAX) {
+    set_error("sk_run_begin: unknown reduce op");
+    return SK_ERR_ARG;
+  }
+  const KernelOps* ops = nullptr;
+  switch (plan->kernel) {
+    case SK_KERNEL_HELMHOLTZ: ops = helmholtz_ops(); break;
+    case SK_KERNEL_LIFE: ops = life_ops(); break;
+    case SK_KERNEL_RESTORE: ops = restore_ops(); break;
+    case SK_KERNEL_SOBEL:
+    case SK_KERNEL_AMF: ops = map_ops(); break;
+    default:
+      set_error("sk_run_begin: unknown kernel id");
+      return SK_ERR_ARG;
+  }
+  sk_run* r = new sk_run();
+  r->plan = *plan;
+  r->ops = ops;
+  r->stream = static_cast<cudaStream_t>(stream);
+  r->src = d_src;
+  r->src_pitch = src_pitch;
+  r->env = d_env;
+  r->env_pitch = env_pitch;
+  r->buf[0] = d_buf0;
+  r->buf[1] = d_buf1;
+  r->pitch = pitch;
+  r->timing = (plan->flags & SK_FLAG_TIMING) != 0;
+  int rc = SK_OK;
+  cudaError_t ce = cudaGetDevice(&r->device);
+  if (ce != cudaSuccess) {
+    delete r;
+    return cuda_fail(ce, "cudaGetDevice");
+  }
+  // partition row boundaries: remainder to the lowest partitions
+  // (_split_ranges, partition.py:187-195)
+  r->nparts = plan->partitions;
+  {
+    const long long base = plan->rows / r->nparts, rem = plan->rows % r->nparts;
+    long long b = 0;
+    r->part_row[0] = 0;
+    for (int i = 0; i < r->nparts; ++i) {
+      b += base + (i < rem ? 1 : 0);
+      r->part_row[i + 1] = (int)b;
+    }
+  }
+  rc = r->ops->setup(r);
+  if (rc) {
+    delete r;
+    return rc;
+  }
+  auto fail = [&](cudaError_t e, const char* what) {
+    int code = cuda_fail(e, what);
+    sk_run_destroy(r);
+    return code;
+  };
+  if ((ce = cudaMallocAsync(reinterpret_cast<void**>(&r->d_status), sizeof(Status), r->stream)))
+    return fail(ce, "cudaMallocAsync(status)");
+  if ((ce = cudaMemsetAsync(r->d_status, 0, sizeof(Status), r->stream)))
+    return fail(ce, "cudaMemsetAsync(status)");
+  const size_t np = (size_t)(r->nchunks > r->grid ? r->nchunks : r->grid) + 1;
+  if ((ce = cudaMallocAsync(reinterpret_cast<void**>(&r->d_partials), np * sizeof(double), r->stream)))
+    return fail(ce, "cudaMallocAsync(partials)");
+  if ((rc = g_ring.take(&r->h_ring, &r->d_ring))) {
+    sk_run_destroy(r);
+    return rc;
+  }
+  *out = r;
+  return SK_OK;
+}
+
+int sk_run_launch(sk_run* r, int32_t n) {
+  if (!r || n < 0) {
+    set_error("sk_run_launch: bad argument");
+    return SK_ERR_ARG;
+  }
+  LoopCtl L = make_ctl(r, nullptr, false, 0);
+  for (int i = 0; i < n; ++i) {
+    int rc = launch_timed(r, L);
+    if (rc) return rc;
+  }
+  return SK_OK;
+}
+
+int sk_run_value(sk_run* r, int64_t it, double* value) {
+  if (!r || !value || it < 1 || it > r->launched || it <= r->launched - kRing) {
+    set_error("sk_run_value: iteration not in the launched window");
+    return SK_ERR_ARG;
+  }
+  SK_CUDA(cudaEventSynchronize(r->ev_done[it % kRing]));
+  *value = static_cast<volatile double*>(r->h_ring)[it % kRing];
+  return SK_OK;
+}
+
+int sk_run_loop(sk_run* r, const sk_cond* c, int64_t* iterations, double* final_value,
+                int32_t* exhausted) {
+  if (!r || !c || c->max_iterations < 1) {
+    set_error("sk_run_loop: bad argument");
+    return SK_ERR_ARG;
+  }
+  if (r->launched != 0) {
+    set_error("sk_run_loop: the run already has host-driven iterations");
+    return SK_ERR_STATE;
+  }
+  int rc = SK_OK;
+  bool use_graph = !r->timing;
+  if (use_graph) {
+    // One graph: conditional WHILE node whose body is one sweep; the sweep's
+    // finalizing CTA clears the condition when the loop is over.
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t ex = nullptr;
+    cudaGraphConditionalHandle h;
+    cudaError_t ce = cudaGraphCreate(&g, 0);
+    if (ce == cudaSuccess) ce = cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault);
+    cudaGraphNodeParams cp = {};
+    cudaGraphNode_t node;
+    if (ce == cudaSuccess) {
+      cp.type = cudaGraphNodeTypeConditional;
+      cp.conditional.handle = h;
+      cp.conditional.type = cudaGraphCondTypeWhile;
+      cp.conditional.size = 1;
+      ce = cudaGraphAddNode(&node, g, nullptr, 0, &cp);
+    }
+    if (ce == cudaSuccess && !r->cap_stream) ce = cudaStreamCreateWithFlags(&r->cap_stream, cudaStreamNonBlocking);
+    if (ce == cudaSuccess) {
+      cudaGraph_t body = cp.conditional.phGraph_out[0];
+      ce = cudaStreamBeginCaptureToGraph(r->cap_stream, body, nullptr, nullptr, 0,
+                                         cudaStreamCaptureModeRelaxed);
+      if (ce == cudaSuccess) {
+        LoopCtl L = make_ctl(r, c, true, h);
+        rc = r->ops->launch(r, L, r->cap_stream);
+        cudaGraph_t body2 = body;
+        cudaError_t ce2 = cudaStreamEndCapture(r->cap_stream, &body2);
+        if (rc) {
+          cudaGraphDestroy(g);
+          return rc;
+        }
+        ce = ce2;
+      }
+    }
+    if (ce == cudaSuccess) ce = cudaGraphInstantiate(&ex, g, 0);
+    if (g) cudaGraphDestroy(g);
+    if (ce == cudaSuccess) {
+      ce = cudaGraphLaunch(ex, r->stream);
+      if (ce == cudaSuccess) r->gexec = ex;
+      else cudaGraphExecDestroy(ex);
+    }
+    if (ce != cudaSuccess) {
+      cudaGetLastError();  // clear; fall back to batched launches
+      use_graph = false;
+    }
+  }
+  if (!use_graph) {
+    // Batched launches: iterations after the device-decided stop are no-ops.
+    LoopCtl L = make_ctl(r, c, false, 0);
+    const int batch = 8;
+    for (;;) {
+      for (int i = 0; i < batch; ++i)
+        if ((rc = launch_timed(r, L))) return rc;
+      Status st;
+      SK_CUDA(cudaMemcpyAsync(&st, r->d_status, sizeof(Status), cudaMemcpyDeviceToHost, r->stream));
+      SK_CUDA(cudaStreamSynchronize(r->stream));
+      if (st.stop) break;
+    }
+  }
+  Status st;
+  SK_CUDA(cudaMemcpyAsync(&st, r->d_status, sizeof(Status), cudaMemcpyDeviceToHost, r->stream));
+  SK_CUDA(cudaStreamSynchronize(r->stream));
+  if (!st.stop) {
+    set_error("sk_run_loop: device loop ended without a decision");
+    return SK_ERR_STATE;
+  }
+  if (use_graph) r->total_launches += st.iter;  // one sweep per WHILE-body execution
+  r->launched = st.iter;  // committed iterations
+  if (iterations) *iterations = st.iter;
+  if (final_value) *final_value = st.value;
+  if (exhausted) *exhausted = st.exhausted;
+  return SK_OK;
+}
+
+int sk_run_result(sk_run* r, int64_t it, int32_t* which) {
+  if (!r || !which || it < 0 || it > r->launched) {
+    set_error("sk_run_result: iteration out of range");
+    return SK_ERR_ARG;
+  }
+  *which = it == 0 ? -1 : (int32_t)(it & 1);
+  return SK_OK;
+}
+
+int sk_run_value_ptr(sk_run* r, void** d_value) {
+  if (!r || !d_value) {
+    set_error("sk_run_value_ptr: null argument");
+    return SK_ERR_ARG;
+  }
+  *d_value = reinterpret_cast<char*>(r->d_status) + offsetof(Status, value);
+  return SK_OK;
+}
+
+int sk_run_kernel_time(sk_run* r, double* total_ms, int64_t* launches) {
+  if (!r || !total_ms || !launches) {
+    set_error("sk_run_kernel_time: null argument");
+    return SK_ERR_ARG;
+  }
+  // Only sweeps that computed an iteration count (over-launched no-ops after
+  // the device-decided stop are excluded).
+  Status st;
+  SK_CUDA(cudaMemcpyAsync(&st, r->d_status, sizeof(Status), cudaMemcpyDeviceToHost, r->stream));
+  SK_CUDA(cudaStreamSynchronize(r->stream));
+  double tot = 0;
+  long long n = 0;
+  for (size_t i = 0; i < r->t_start.size(); ++i) {
+    if (r->t_iter[i] > st.iter) continue;
+    float ms = 0;
+    SK_CUDA(cudaEventElapsedTime(&ms, r->t_start[i], r->t_stop[i]));
+    tot += ms;
+    ++n;
+  }
+  *total_ms = tot;
+  *launches = n;
+  return SK_OK;
+}
+
+int sk_run_launches(sk_run* r, int64_t* launches) {
+  if (!r || !launches) {
+    set_error("sk_run_launches: null argument");
+    return SK_ERR_ARG;
+  }
+  *launches = r->total_launches;
+  return SK_OK;
+}
+
+int sk_run_destroy(sk_run* r) {
+  if (!r) return SK_OK;
+  int rc = SK_OK;
+  // the run's stream may still be executing: wait before freeing
+  if (r->stream || true) {
+    cudaError_t e = cudaStreamSynchronize(r->stream);
+    if (e != cudaSuccess) rc = cuda_fail(e, "cudaStreamSynchronize(destroy)");
+  }
+  if (r->ops && r->ops->teardown) r->ops->teardown(r);
+  if (r->gexec) cudaGraphExecDestroy(r->gexec);
+  if (r->cap_stream) cudaStreamDestroy(r->cap_stream);
+  for (auto& e : r->ev_done)
+    if (e) cudaEventDestroy(e);
+  for (auto e : r->t_start) cudaEventDestroy(e);
+  for (auto e : r->t_stop) cudaEventDestroy(e);
+  if (r->d_status) cudaFreeAsync(r->d_status, r->stream);
+  if (r->d_partials) cudaFreeAsync(r->d_partials, r->stream);
+  g_ring.give(r->h_ring);
+  delete r;
+  return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,434 @@
+"""Partitioned loop runtime on the GPU (reference: partition.py:1-692).
+
+Public surface mirrors the reference: DeploymentMode, WorkerGroup,
+parallel_loop, partition/_split_ranges geometry, PartitionSet, halo_exchange,
+parallel_step -- plus `DeviceExecutor`, the Executor-protocol implementation
+(loop.py:124-137) over the native engine (include/stencilkit_b200.h).
+
+Mapping of the reference's model onto one GPU:
+  * partitions  -> contiguous row blocks exactly as _split_ranges
+                   (partition.py:187-195).  On one device the blocks share one
+                   pair of iteration buffers, so a "halo exchange" is a read of
+                   the neighbour's rows in place; the engine keeps the
+                   per-partition reduce structure (CTA work chunks never span
+                   a partition; partials are folded per partition, then in
+                   ascending partition order from the identity,
+                   partition.py:642-646).  The CopyLedger reports the
+                   reference's traffic model from the committed iteration
+                   count (fill/readback per partition, 2*k*d2 per boundary per
+                   exchanged iteration, none after the last).
+  * WorkerGroup -> a reusable device context: one CUDA stream, one active run
+                   at a time, size = partitions it serves (partition.py:451-532).
+  * multi-GPU   -> one process per GPU (see distributed.py): each rank owns one
+                   row block with real halo rows moved over NCCL/NVLink.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from dataclasses import dataclass
+from enum import Enum
+from typing import Any, Optional
+
+import numpy as np
+
+from . import _native as N
+from .grid import Grid, GridError
+from .ledger import CopyLedger
+from .loop import Executor, LoopPlan, LoopState, _as_plan, _drive
+from .patterns import (Combinator, DeviceUnsupported, _check_env, combinator_kind, delta_kind)
+
+
+class DeploymentMode(Enum):
+    """ONE_TO_ONE: each loop on one partition; ONE_TO_N: split across P >= 2
+    partitions (partition.py:39-57)."""
+
+    ONE_TO_ONE = "1:1"
+    ONE_TO_N = "1:n"
+
+    @classmethod
+    def parse(cls, text) -> "DeploymentMode":
+        if isinstance(text, cls):
+            return text
+        for m in cls:
+            if m.value == text:
+                return m
+        raise GridError(f"unknown deployment mode {text!r} (expected 1:1 or 1:n)")
+
+
+def _split_ranges(d1: int, P: int) -> list:
+    """Row ranges, remainder to the lowest partitions (partition.py:187-195)."""
+    base, rem = divmod(d1, P)
+    out, b = [], 0
+    for i in range(P):
+        s = base + (1 if i < rem else 0)
+        out.append((b, b + s))
+        b += s
+    return out
+
+
+def _check_partitioning(d1: int, P: int, k: int) -> None:
+    """Preconditions of partition() (partition.py:205-215)."""
+    if P < 1:
+        raise GridError(f"partition count must be >= 1, got {P}")
+    if k < 0:
+        raise GridError(f"halo depth must be >= 0, got {k}")
+    if d1 < P:
+        raise GridError(f"cannot split {d1} rows across {P} partitions")
+    if P > 1 and d1 // P < k:
+        raise GridError(f"partitions of {d1} rows across {P} are shallower than halo depth {k}")
+
+
+def model_ledger(dims, P: int, k: int, iterations: int) -> CopyLedger:
+    """The reference's copy-traffic model for a committed run (partition.py:
+    225-262, 170-184; halo skipped after the final iteration, :629-635)."""
+    led = CopyLedger()
+    width = dims[1] if len(dims) == 2 else 1
+    for lo, hi in _split_ranges(dims[0], P):
+        led.record_fill((hi - lo) * width)
+    if k > 0 and P > 1:
+        for _ in range(max(iterations - 1, 0)):
+            for _b in range(P - 1):
+                led.record_halo(2 * k * width, 2)
+    for lo, hi in _split_ranges(dims[0], P):
+        led.record_readback((hi - lo) * width)
+    return led
+
+
+# ---------------------------------------------------------------- worker group
+
+
+class WorkerGroup:
+    """Reusable device context for loop runs (partition.py:451-532).
+
+    Owns one CUDA stream; serves one run at a time; `size` is the partition
+    count of the runs it serves.  Stream-farm replicas keep one each so their
+    runs overlap on the GPU.
+    """
+
+    def __init__(self, size: int, device: Optional[int] = None):
+        if size < 1:
+            raise ValueError(f"worker group size must be >= 1, got {size}")
+        self.size = size
+        self.device = device
+        self._stream = None
+        self._busy = False
+        self._closed = False
+        self._lock = threading.Lock()
+
+    @property
+    def stream(self):
+        if self._stream is None:
+            import torch
+
+            dev = self.device if self.device is not None else torch.cuda.current_device()
+            self._stream = torch.cuda.Stream(device=dev)
+        return self._stream
+
+    def start_run(self) -> None:
+        with self._lock:
+            if self._closed:
+                raise RuntimeError("worker group is closed")
+            if self._busy:
+                raise RuntimeError("worker group already has an active run")
+            self._busy = True
+
+    def end_run(self) -> None:
+        with self._lock:
+            self._busy = False
+
+    def close(self) -> None:
+        with self._lock:
+            if self._closed:
+                return
+            if self._busy:
+                raise RuntimeError("cannot close a worker group with an active run")
+            self._closed = True
+            if self._stream is not None:
+                self._stream.synchronize()
+
+    def __enter__(self) -> "WorkerGroup":
+        return self
+
+    def __exit__(self, *exc) -> None:
+        self.close()
+
+
+# ---------------------------------------------------------------- executor
+
+_KERNEL_IDS = {"helmholtz": N.SK_KERNEL_HELMHOLTZ, "sobel": N.SK_KERNEL_SOBEL,
+               "amf": N.SK_KERNEL_AMF, "restore": N.SK_KERNEL_RESTORE,
+               "life": N.SK_KERNEL_LIFE}
+_REDUCE = {"sum": N.SK_REDUCE_SUM, "max": N.SK_REDUCE_MAX}
+_DELTA = {"none": N.SK_DELTA_NONE, "abs": N.SK_DELTA_ABS, "square": N.SK_DELTA_SQUARE}
+_COND = {"lt": N.SK_COND_LT, "rms_lt": N.SK_COND_RMS_LT, "mean_lt": N.SK_COND_MEAN_LT,
+         "iter_ge": N.SK_COND_ITER_GE}
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+@dataclass
+class _DevRun:
+    plan: LoopPlan
+    dims: tuple
+    P: int
+    handle: Any
+    bufs: list
+    src: Any
+    env: Any
+    pitch: int
+    cols: int
+    out_dtype: Any        # numpy logical dtype of the result grid
+    int_value: bool       # reduce value reported as int
+    stream: Any
+    group: Optional[WorkerGroup]
+    owns_group: bool
+    steps: int = 0        # committed (host-observed) iterations
+    launched: int = 0     # iterations enqueued on the device
+    committed: Optional[int] = None
+    released: bool = False
+
+
+def _u8_from(grid: Grid, what: str, lo: int, hi: int, dev):
+    """Integer image -> device uint8 tensor, values checked in [lo, hi]."""
+    torch = _torch()
+    sd = grid.storage_dtype()
+    if sd.kind not in "iub":
+        raise GridError(f"{what} expects integer pixels, got dtype {sd}")
+    t = grid.tensor(device=dev)
+    if t.dtype != torch.uint8:
+        mn, mx = int(t.min().item()), int(t.max().item())
+        if mn < lo or mx > hi:
+            raise GridError(f"{what}: pixel values must lie in [{lo}, {hi}], found [{mn}, {mx}]")
+        t = t.to(torch.uint8)
+    return t
+
+
+class DeviceExecutor(Executor):
+    """Executor over the native engine: `partitions` row partitions on one GPU."""
+
+    device_loop = True
+
+    def __init__(self, partitions: int = 1, group: Optional[WorkerGroup] = None,
+                 timing: bool = False):
+        if group is not None and group.size != partitions:
+            raise ValueError(
+                f"worker group size {group.size} does not match partitions {partitions}")
+        self.partitions = partitions
+        self._group = group
+        self.timing = timing
+        self.last_kernel_time = None
+        self.launches = 0  # native sweep launches over this executor's runs
+
+    # -- begin -----------------------------------------------------------
+    def begin(self, plan: LoopPlan, grid: Grid) -> _DevRun:
+        lib = N.require_cuda()
+        torch = _torch()
+        _check_env(plan.env, grid.dims)
+        dk = plan.fn.device if hasattr(plan.fn, "device") else None
+        if dk is None:
+            raise DeviceUnsupported(
+                "elemental function has no device kernel; the engine runs only its "
+                "sm_100a kernels (helmholtz, sobel, amf, restore, life)")
+        if grid.ndim != 2:
+            raise DeviceUnsupported("device kernels run on 2D grids")
+        rows, cols = grid.dims
+        P = self.partitions
+        _check_partitioning(rows, P, plan.k)
+        reduce = combinator_kind(plan.op)
+        delta = delta_kind(plan.delta)
+        group = self._group
+        owns = group is None
+        stream = group.stream if group is not None else torch.cuda.current_stream()
+        if group is not None:
+            group.start_run()
+        try:
+            with torch.cuda.stream(stream):
+                return self._begin_on(lib, plan, grid, dk, rows, cols, P, reduce, delta,
+                                      stream, group, owns)
+        except BaseException:
+            if group is not None:
+                group.end_run()
+            raise
+
+    def _begin_on(self, lib, plan, grid, dk, rows, cols, P, reduce, delta, stream, group, owns):
+        torch = _torch()
+        dev = torch.device("cuda", torch.cuda.current_device())
+        name = dk.name
+        env_t = None
+        int_value = False
+        if name == "helmholtz":
+            sd = grid.storage_dtype()
+            if sd not in (np.float32, np.float64):
+                raise DeviceUnsupported(f"helmholtz runs on float32/float64 grids, got {sd}")
+            dtype = N.SK_F32 if sd == np.float32 else N.SK_F64
+            tdt = torch.float32 if sd == np.float32 else torch.float64
+            src = grid.tensor(device=dev)
+            if src.dtype != tdt:
+                src = src.to(tdt)
+            if plan.env is None or not isinstance(plan.env, Grid):
+                raise GridError("helmholtz needs the right-hand side grid as env")
+            ed = plan.env.storage_dtype()
+            if ed != sd:
+                raise DeviceUnsupported(
+                    f"env dtype {ed} differs from grid dtype {sd}: the reference would mix "
+                    "precisions; pass both grids in the same dtype")
+            env_t = plan.env.tensor(device=dev)
+            out_dtype = sd
+        elif name in ("sobel", "amf", "life"):
+            hi = 1 if name == "life" else 255
+            src = _u8_from(grid, name, 0, hi, dev)
+            dtype = N.SK_U8
+            out_dtype = np.dtype(np.int64)
+            int_value = True
+            if delta != "none":
+                raise DeviceUnsupported(f"{name}: delta reduces are not supported")
+        elif name == "restore":
+            sd = grid.storage_dtype()
+            if sd.kind not in "fiu":
+                raise DeviceUnsupported(f"restore needs a numeric grid, got {sd}")
+            src = grid.tensor(device=dev)
+            if src.dtype != torch.float64:
+                src = src.to(torch.float64)
+            if plan.env is None or not isinstance(plan.env, Grid):
+                raise GridError("restore needs the noise map grid as env")
+            env_t = _u8_from(plan.env, "noise map", 0, 1, dev)
+            dtype = N.SK_F64
+            out_dtype = np.dtype(np.float64)
+        else:
+            raise DeviceUnsupported(f"unknown device kernel {name!r}")
+
+        esize = src.element_size()
+        vec = 16 // esize
+        pitch = -(-cols // vec) * vec
+        staged = pitch != cols or src.data_ptr() % 16 != 0
+        if staged:
+            s2 = torch.zeros((rows, pitch), dtype=src.dtype, device=dev)
+            s2[:, :cols] = src.reshape(rows, cols)
+            src = s2
+            bufs = [torch.zeros((rows, pitch), dtype=src.dtype, device=dev) for _ in range(2)]
+        else:
+            src = src.reshape(rows, cols)
+            bufs = [torch.empty((rows, pitch), dtype=src.dtype, device=dev) for _ in range(2)]
+        env_pitch = 0
+        env_ptr = None
+        if env_t is not None:
+            ev = 16 // env_t.element_size()
+            ep = -(-cols // ev) * ev
+            if ep != cols or env_t.data_ptr() % 16 != 0:
+                e2 = torch.zeros((rows, ep), dtype=env_t.dtype, device=dev)
+                e2[:, :cols] = env_t.reshape(rows, cols)
+                env_t = e2
+            env_pitch = ep
+            env_ptr = env_t.data_ptr()
+
+        p = N.sk_plan()
+        p.kernel = _KERNEL_IDS[name]
+        p.dtype = dtype
+        p.rows, p.cols = rows, cols
+        p.partitions = P
+        p.reduce_op = _REDUCE[reduce]
+        p.delta_op = _DELTA[delta]
+        p.halo_top = p.halo_bottom = 0
+        p.flags = N.SK_FLAG_TIMING if self.timing else 0
+        ident = plan.op.identity
+        p.identity = float(ident) if ident is not None else 0.0
+        for i, v in enumerate(dk.params[:8]):
+            p.params[i] = float(v)
+        h = C.c_void_p()
+        N.check(lib.sk_run_begin(C.byref(p), C.c_void_p(src.data_ptr()), pitch if staged else cols,
+                                 C.c_void_p(env_ptr), env_pitch,
+                                 C.c_void_p(bufs[0].data_ptr()), C.c_void_p(bufs[1].data_ptr()),
+                                 pitch, N.stream_handle(stream), C.byref(h)))
+        return _DevRun(plan=plan, dims=(rows, cols), P=P, handle=h, bufs=bufs, src=src, env=env_t,
+                       pitch=pitch, cols=cols, out_dtype=out_dtype, int_value=int_value,
+                       stream=stream, group=group, owns_group=owns)
+
+    # -- host-driven steps (generic Python condition / LoopState) ----------
+    def step(self, run: _DevRun) -> Any:
+        lib = N.load()
+        t = run.steps + 1
+        while run.launched < t + 1:  # keep one speculative iteration in flight (lag-1)
+            N.check(lib.sk_run_launch(run.handle, 1))
+            run.launched += 1
+        v = C.c_double()
+        N.check(lib.sk_run_value(run.handle, t, C.byref(v)))
+        run.steps = t
+        return self._value(run, v.value)
+
+    def _value(self, run: _DevRun, v: float):
+        if run.int_value:
+            return int(v)
+        return v
+
+    # -- whole loop on the device --------------------------------------------
+    def run_loop(self, run: _DevRun, cond):
+        lib = N.load()
+        dc = cond.device
+        c = N.sk_cond()
+        c.kind = _COND[dc.kind]
+        c.a = dc.a
+        c.n = dc.n
+        c.max_iterations = cond.max_iterations
+        it, val, ex = C.c_int64(), C.c_double(), C.c_int32()
+        N.check(lib.sk_run_loop(run.handle, C.byref(c), C.byref(it), C.byref(val), C.byref(ex)))
+        run.steps = run.launched = it.value
+        return it.value, self._value(run, val.value), bool(ex.value)
+
+    # -- finish / abort ------------------------------------------------------
+    def finish(self, run: _DevRun):
+        lib = N.load()
+        torch = _torch()
+        it = run.steps
+        which = C.c_int32()
+        N.check(lib.sk_run_result(run.handle, it, C.byref(which)))
+        nl = C.c_int64()
+        N.check(lib.sk_run_launches(run.handle, C.byref(nl)))
+        self.launches += nl.value
+        if self.timing:
+            ms, n = C.c_double(), C.c_int64()
+            N.check(lib.sk_run_kernel_time(run.handle, C.byref(ms), C.byref(n)))
+            self.last_kernel_time = (ms.value, n.value)
+        buf = run.bufs[which.value] if which.value >= 0 else run.src
+        self._release(run)
+        out = buf[:, :run.cols]
+        if run.pitch != run.cols:
+            out = out.contiguous()
+        led = model_ledger(run.dims, run.P, run.plan.k, it)
+        return Grid.from_tensor(out, logical_dtype=run.out_dtype), led
+
+    def abort(self, run: _DevRun) -> None:
+        self._release(run)
+
+    def _release(self, run: _DevRun) -> None:
+        if run.released:
+            return
+        run.released = True
+        lib = N.load()
+        rc = lib.sk_run_destroy(run.handle)
+        if run.group is not None:
+            run.group.end_run()
+        N.check(rc)
+
+
+def parallel_loop(mode, partitions: int, k, f, op: Combinator, cond, a: Grid,
+                  env: Any = None, *, delta=None, indexed: bool = False,
+                  state: Optional[LoopState] = None,
+                  group: Optional[WorkerGroup] = None,
+                  max_iterations: Optional[int] = None):
+    """Partitioned stencil-reduce loop (partition.py:667-692) on the GPU."""
+    mode = DeploymentMode.parse(mode)
+    if partitions < 1:
+        raise GridError(f"partition count must be >= 1, got {partitions}")
+    if mode is DeploymentMode.ONE_TO_N and partitions < 2:
+        raise GridError("1:n deployment needs at least 2 partitions")
+    eff = partitions if mode is DeploymentMode.ONE_TO_N else 1
+    if group is not None and group.size != eff:
+        raise GridError(f"worker group size {group.size} does not match {eff} partitions")
+    plan = _as_plan(f, k, op, env, indexed=indexed, delta=delta)
+    return _drive(plan, cond, state, a, DeviceExecutor(eff, group), max_iterations)

@@ -1,0 +1,115 @@
+"""Helmholtz device path vs the reference's own outputs (golden fixtures).
+
+Bit-exact grids (fp32 and fp64), identical iteration counts, MAX reduce
+values bit-equal; SUM reduce values within rel 1e-5 (fp32: the reference
+sums in fp32 pairwise order, the engine accumulates in fp64) and rel 1e-12
+(fp64; different but deterministic summation order).
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+import paper_1609_04567_b200 as sk
+from paper_1609_04567_b200.apps import HelmholtzConfig, helmholtz_kernel, helmholtz_solve
+
+pytestmark = pytest.mark.gpu
+
+SUM_RTOL = {"f32": 1e-5, "f64": 1e-12}
+
+
+def _f32_case(golden, name, *, host_cond=False, P=None):
+    m = golden.meta[name]
+    n, c = m["rows"], m["cols"]
+    cfg = HelmholtzConfig(rows=n, cols=c, alpha=m["alpha"], dx=m["dx"], dy=m["dy"],
+                          relax=m["relax"], tol=m["tol"])
+    u0 = sk.Grid((n, c), np.zeros((n, c), np.float32))
+    f = sk.Grid((n, c), golden[name + "/rhs"])
+    tol = m["tol"]
+    if m["reduce"] == "max":
+        op, delta = sk.max_combinator(0.0), sk.abs_change()
+        cond = (lambda v, it, s: v < tol) if host_cond else sk.Condition.below(tol)
+    else:
+        op, delta = sk.sum_combinator(0.0), sk.sq_change()
+        nm = n * c
+        cond = (lambda v, it, s: math.sqrt(v / nm) < tol) if host_cond else \
+            sk.Condition.rms_below(tol, nm)
+    P = m["P"] if P is None else P
+    out, rep = sk.parallel_loop("1:n" if P > 1 else "1:1", P, 1, helmholtz_kernel(cfg), op, cond,
+                                u0, env=f, delta=delta)
+    return m, out, rep
+
+
+@pytest.mark.parametrize("host_cond", [False, True])
+def test_f32_cases_bit_exact(golden, host_cond):
+    for name in golden.cases("helmholtz"):
+        m, out, rep = _f32_case(golden, name, host_cond=host_cond)
+        a = out.to_array()
+        assert a.dtype == np.float32
+        want = golden[name + "/out"]
+        assert rep.iterations == m["iterations"], name
+        assert np.array_equal(a.view(np.uint32), want.view(np.uint32)), name
+        if m["reduce"] == "max":
+            assert rep.final_reduce == m["final_reduce"], name
+        else:
+            assert rep.final_reduce == pytest.approx(m["final_reduce"], rel=SUM_RTOL["f32"]), name
+        assert rep.exhausted == m["exhausted"]
+        assert vars(rep.copies) == m["ledger"], name
+
+
+def test_f64_solve_bit_exact(golden):
+    for name in golden.cases("helmholtz_solve"):
+        m = golden.meta[name]
+        n, c = m["rows"], m["cols"]
+        cfg = HelmholtzConfig(rows=n, cols=c, alpha=m["alpha"], dx=m["dx"], dy=m["dy"],
+                              relax=m["relax"], tol=m["tol"])
+        u0 = sk.Grid.from_array(golden[name + "/u0"]) if golden.has(name + "/u0") else None
+        u, rep = helmholtz_solve(cfg, sk.Grid.from_array(golden[name + "/rhs"]), u0,
+                                 partitions=m["P"])
+        assert rep.iterations == m["iterations"], name
+        assert np.array_equal(u.to_array(), golden[name + "/out"]), name
+        assert rep.final_reduce == pytest.approx(m["final_reduce"], rel=SUM_RTOL["f64"]), name
+        assert vars(rep.copies) == m["ledger"], name
+
+
+def test_partition_invariant_grid_and_deterministic_sum(golden):
+    name = "helm_f32_sum_rand_50x70"
+    vals = {}
+    for P in (1, 2, 3, 7):
+        _, out1, rep1 = _f32_case(golden, name, P=P)
+        _, out2, rep2 = _f32_case(golden, name, P=P)
+        assert rep1.final_reduce == rep2.final_reduce  # bit-identical re-run
+        assert out1 == out2
+        vals[P] = (out1.to_array(), rep1.iterations, rep1.final_reduce)
+    for P in (2, 3, 7):
+        assert np.array_equal(vals[P][0], vals[1][0])
+        assert vals[P][1] == vals[1][1]
+        assert vals[P][2] == pytest.approx(vals[1][2], rel=1e-12)
+
+
+def test_device_input_stays_untouched_and_output_on_device():
+    import torch
+
+    n = 256
+    u0 = torch.zeros((n, n), dtype=torch.float32, device="cuda")
+    f = torch.ones((n, n), dtype=torch.float32, device="cuda")
+    cfg = HelmholtzConfig(rows=n, cols=n)
+    out, rep = sk.parallel_loop("1:1", 1, 1, helmholtz_kernel(cfg), sk.max_combinator(0.0),
+                                sk.Condition.below(1e-4), sk.Grid.from_tensor(u0),
+                                env=sk.Grid.from_tensor(f), delta=sk.abs_change())
+    assert rep.iterations == 36
+    assert out.is_device
+    assert float(u0.abs().max()) == 0.0
+
+
+def test_exhaustion_flag_and_cap():
+    n = 64
+    cfg = HelmholtzConfig(rows=n, cols=n)
+    u0 = sk.Grid((n, n), np.zeros((n, n), np.float32))
+    f = sk.Grid((n, n), np.ones((n, n), np.float32))
+    for cond in (sk.Condition.below(1e-30, max_iterations=7),
+                 sk.Condition(lambda v, it, s: v < 1e-30, max_iterations=7)):
+        out, rep = sk.parallel_loop("1:1", 1, 1, helmholtz_kernel(cfg), sk.max_combinator(0.0),
+                                    cond, u0, env=f, delta=sk.abs_change())
+        assert rep.iterations == 7 and rep.exhausted
