@@ -146,6 +146,11 @@ int sk_run_launches(sk_run* run, int64_t* launches);
 /* Executor.abort / end of finish: release device state. */
 int sk_run_destroy(sk_run* run);
 
+/* Self-check of the engine's exact division by a run constant (see
+ * sk_common.cuh div_const): number of fp32 numerators in the fast range whose
+ * result differs from IEEE division x / b (0 expected; -1 = check failed). */
+long long sk_verify_div_f32(float b, void* stream);
+
 /* ---- batched map-only stencils for frame streams (config C2) -----------
  * Sobel edge magnitude (apps/sobel.py:47-66) over `frames` frames of
  * rows x cols u8 pixels, frame f at d_in + f*frame_stride (pitch bytes per

@@ -23,6 +23,7 @@ LIBNAME = "libstencilkit_b200.so"
 SOURCES = [
     "sk_runtime.cu",
     "sk_helmholtz.cu",
+    "sk_verify.cu",
     "sk_stubs.cu",
 ]
 

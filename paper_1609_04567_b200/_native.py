@@ -24,7 +24,8 @@ SK_FLAG_TIMING = 1
 EXPORTS = (
     "sk_last_error", "sk_abi_version", "sk_run_begin", "sk_run_launch", "sk_run_value",
     "sk_run_loop", "sk_run_result", "sk_run_value_ptr", "sk_run_kernel_time",
-    "sk_run_launches", "sk_run_destroy", "sk_sobel_frames", "sk_amf_frames",
+    "sk_run_launches", "sk_run_destroy", "sk_verify_div_f32", "sk_sobel_frames",
+    "sk_amf_frames",
 )
 
 
@@ -99,6 +100,8 @@ def _declare(lib):
         "sk_sobel_frames": [P, I64, I64, P, I64, I64, I32, I64, I64, P, P],
         "sk_amf_frames": [P, I64, I64, P, I64, I64, I32, I64, I64, I32, P, P],
     }
+    lib.sk_verify_div_f32.argtypes = [C.c_float, P]
+    lib.sk_verify_div_f32.restype = C.c_longlong
     for name, args in sig.items():
         fn = getattr(lib, name)
         fn.argtypes = args

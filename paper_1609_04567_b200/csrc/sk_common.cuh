@@ -70,6 +70,51 @@ __device__ __forceinline__ double xsub(double a, double b) { return __dsub_rn(a,
 __device__ __forceinline__ double xdiv(double a, double b) { return __ddiv_rn(a, b); }
 __device__ __forceinline__ double xsqrt(double a) { return __dsqrt_rn(a); }
 
+// Correctly rounded x / b for a run-constant b, in 3 ops instead of the
+// ~10-op IEEE division sequence: q0 = RN(x*r) with r = RN(1/b) is within one
+// ulp of x/b, and one FMA residual step then yields RN(x/b) (Markstein's
+// theorem; the residual fma(-q0, b, x) is exact).  Valid while nothing
+// over/underflows: callers take this path only for 2^-100 <= |x| < 2^100 and
+// 2^-60 <= |b| <= 2^60 (checked on the host) and use the IEEE division
+// otherwise.  The fp32 form is verified exhaustively on the GPU
+// (tests/test_gpu_division.py).
+__device__ __forceinline__ float div_const(float x, float b, float r) {
+  const float q0 = __fmul_rn(x, r);
+  const float e = __fmaf_rn(-q0, b, x);
+  return __fmaf_rn(e, r, q0);
+}
+__device__ __forceinline__ double div_const(double x, double b, double r) {
+  const double q0 = __dmul_rn(x, r);
+  const double e = __fma_rn(-q0, b, x);
+  return __fma_rn(e, r, q0);
+}
+__device__ __forceinline__ bool div_safe(float x) {
+  const float a = fabsf(x);
+  return a >= 0x1p-60f && a < 0x1p60f;
+}
+__device__ __forceinline__ bool div_safe(double x) {
+  const double a = fabs(x);
+  return a >= 0x1p-500 && a < 0x1p500;
+}
+// host: is b inside the range where div_const is valid for div_safe(x)?
+inline bool div_b_ok(double b, bool f32) {
+  const double a = b < 0 ? -b : b;
+  return f32 ? (a >= 0x1p-30 && a <= 0x1p30) : (a >= 0x1p-200 && a <= 0x1p200);
+}
+
+__device__ __forceinline__ float tabs(float x) { return fabsf(x); }
+__device__ __forceinline__ double tabs(double x) { return fabs(x); }
+
+// NaN-propagating max (np.max semantics) in the element type.
+__device__ __forceinline__ float max_nan(float a, float b) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ double max_nan(double a, double b) {
+  return (a != a || b != b) ? __longlong_as_double(0x7ff8000000000000ll) : fmax(a, b);
+}
+
 // ---------------------------------------------------------------- reduce ops
 // MAX follows np.max: NaN propagates.
 __device__ __forceinline__ double rmax(double a, double b) {

@@ -36,6 +36,10 @@ const KernelOps* map_ops();  // single-pass map kernels (Sobel, AMF) behind the 
 
 int device_sms(int device);
 
+// mismatches of div_const vs IEEE division over all safe fp32 numerators
+// (cached per divisor; -1 if the check could not run)
+long long verify_div_f32(float b, cudaStream_t s);
+
 }  // namespace sk
 
 struct sk_run {
