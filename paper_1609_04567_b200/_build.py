@@ -24,7 +24,10 @@ SOURCES = [
     "sk_runtime.cu",
     "sk_helmholtz.cu",
     "sk_verify.cu",
-    "sk_stubs.cu",
+    "sk_u8stencil.cu",
+    "sk_amf.cu",
+    "sk_restore.cu",
+    "sk_dispatch.cu",
 ]
 
 NVCC_FLAGS = [

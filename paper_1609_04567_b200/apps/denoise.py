@@ -1,0 +1,221 @@
+"""Two-phase impulse-noise removal for 8-bit images (reference: apps/denoise.py).
+
+Phase one flags suspect pixels with the adaptive median test (sm_100a
+kernel csrc/sk_amf.cu); phase two restores only the flagged pixels by
+minimising a local edge-preserving functional with an 18-step ternary
+search in fp64, iterated until the mean change per flagged pixel drops
+below tolerance (csrc/sk_restore.cu; the loop and its stopping test run on
+the device).  The video entry point is the reference's
+
+    pipeline(read, detect, ordered_farm(restore, W), write)
+
+where every restore replica owns a WorkerGroup -- its own CUDA stream -- so
+W restoration loops are in flight on the GPU at once.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+from typing import Callable, Iterable, Optional
+
+import numpy as np
+
+from .. import _native as N
+from ..grid import Grid, GridError
+from ..loop import Condition, stop_after
+from ..partition import DeploymentMode, WorkerGroup, parallel_loop
+from ..patterns import Combinator, DeviceKernel, DeviceUnsupported, ElementalFn, abs_change
+from ..streams import Stage, StreamReport, ordered_farm, pipeline, run_stream
+
+_SEARCH_STEPS = math.ceil(math.log((255.0 - 0.0) / 0.25) / math.log(1.5))  # 18, as the reference
+
+
+@dataclass(frozen=True)
+class RestoreConfig:
+    """Knobs for both phases (apps/denoise.py:48-72)."""
+
+    amf_wmax: int = 7
+    phi_eps: float = 1e-2
+    beta: float = 2.0
+    tol: float = 0.02
+    max_iterations: int = 100
+
+    def __post_init__(self):
+        if self.amf_wmax < 3 or self.amf_wmax % 2 == 0:
+            raise GridError(f"amf_wmax must be odd and >= 3, got {self.amf_wmax}")
+        if self.phi_eps <= 0 or self.beta <= 0 or self.tol <= 0:
+            raise GridError("phi_eps, beta and tol must all be positive")
+
+
+def _device_only(nb, env):
+    raise DeviceUnsupported("denoise kernels run only on the device")
+
+
+# ---------------------------------------------------------------- phase one
+
+
+def detect_kernel(wmax: int = 7) -> ElementalFn:
+    """Adaptive-median classifier of radius wmax//2 (apps/denoise.py:79-138)."""
+    if wmax < 3 or wmax % 2 == 0:
+        raise GridError(f"wmax must be odd and >= 3, got {wmax}")
+    if wmax > 15:
+        raise DeviceUnsupported("the device detector supports windows up to 15x15")
+    return ElementalFn(point=_device_only, k=wmax // 2, block=None, pad_mode="constant",
+                       pad_value=0, device=DeviceKernel("amf", (float(wmax),)))
+
+
+def _mask_sum() -> Combinator:
+    return Combinator(lambda a, b: a + b, 0, on_array=lambda arr: int(np.sum(arr)), kind="sum")
+
+
+def amf_detect(img: Grid, wmax: int = 7, *, partitions: int = 1,
+               mode=DeploymentMode.ONE_TO_N, group: Optional[WorkerGroup] = None) -> Grid:
+    """0/1 impulse map (apps/denoise.py:145-157)."""
+    if img.ndim != 2:
+        raise GridError("detection expects a 2D image")
+    if partitions == 1:
+        mode = DeploymentMode.ONE_TO_ONE
+    out, _ = parallel_loop(mode, partitions, wmax // 2, detect_kernel(wmax), _mask_sum(),
+                           stop_after(1), img, group=group)
+    return out
+
+
+def amf_frames(frames, wmax: int = 7, out=None, stream=None):
+    """Batched detection over a [F, H, W] uint8 CUDA tensor (one launch).
+    Returns (masks [F, H, W] uint8 0/1, flagged counts [F] int64)."""
+    import torch
+
+    lib = N.require_cuda()
+    if frames.dtype != torch.uint8 or frames.dim() != 3 or not frames.is_cuda:
+        raise GridError("amf_frames expects a [F, H, W] uint8 CUDA tensor")
+    F, H, W = frames.shape
+    if out is None:
+        out = torch.empty_like(frames)
+    counts = torch.empty(F, dtype=torch.int64, device=frames.device)
+    st = stream if stream is not None else torch.cuda.current_stream()
+    N.check(lib.sk_amf_frames(C.c_void_p(frames.data_ptr()), frames.stride(1), frames.stride(0),
+                              C.c_void_p(out.data_ptr()), out.stride(1), out.stride(0), F, H, W,
+                              wmax, C.c_void_p(counts.data_ptr()), N.stream_handle(st)))
+    return out, counts
+
+
+# ---------------------------------------------------------------- phase two
+
+
+def restore_kernel(cfg: RestoreConfig) -> ElementalFn:
+    """Ternary-search restoration of flagged pixels (apps/denoise.py:164-249)."""
+    return ElementalFn(point=_device_only, k=1, block=None, pad_mode="constant", pad_value=0.0,
+                       device=DeviceKernel("restore", (cfg.beta, cfg.phi_eps)))
+
+
+def _float_sum() -> Combinator:
+    return Combinator(lambda a, b: a + b, 0.0, on_array=lambda arr: float(np.sum(arr)), kind="sum")
+
+
+def _flagged_count(noise: Grid) -> int:
+    sd = noise.storage_dtype()
+    if sd.kind not in "iub":
+        raise GridError(f"noise map must be 0/1, found dtype {sd}")
+    if noise.is_device:
+        t = noise.tensor()
+        mn, mx = int(t.min().item()), int(t.max().item())
+        if mn < 0 or mx > 1:
+            raise GridError(f"noise map must be 0/1, found values in [{mn}, {mx}]")
+        return int(t.sum().item())
+    a = noise.to_array()
+    bad = (a != 0) & (a != 1)
+    if bad.any():
+        raise GridError(f"noise map must be 0/1, found {a[bad].ravel()[0]!r}")
+    return int(a.sum())
+
+
+def restore_regularize(img: Grid, noise: Grid, cfg: Optional[RestoreConfig] = None,
+                       *, partitions: int = 1, mode=DeploymentMode.ONE_TO_N,
+                       group: Optional[WorkerGroup] = None):
+    """Restore the flagged pixels; returns (fp64 grid, LoopReport)
+    (apps/denoise.py:262-288)."""
+    cfg = cfg or RestoreConfig()
+    if img.ndim != 2:
+        raise GridError("restoration expects a 2D image")
+    if noise.dims != img.dims:
+        raise GridError(f"noise map dims {noise.dims} do not match image {img.dims}")
+    denom = max(_flagged_count(noise), 1)
+    cond = Condition.mean_below(cfg.tol, denom, max_iterations=cfg.max_iterations)
+    if partitions == 1:
+        mode = DeploymentMode.ONE_TO_ONE
+    return parallel_loop(mode, partitions, 1, restore_kernel(cfg), _float_sum(), cond, img,
+                         env=noise, delta=abs_change(), indexed=True, group=group)
+
+
+# ---------------------------------------------------------------- inputs, video
+
+
+def salt_pepper(img: Grid, level: float, seed: int = 42):
+    """Corrupt a fraction of pixels to 0/255 with numpy's PCG64, exactly as the
+    reference (apps/denoise.py:295-304); returns (noisy, mask).  Host-side
+    input synthesis: identical streams of random numbers require numpy."""
+    if not 0 <= level <= 1:
+        raise GridError(f"noise level must be in [0, 1], got {level}")
+    rng = np.random.default_rng(seed)
+    a = img.to_array()
+    hit = rng.random(a.shape) < level
+    salt = rng.random(a.shape) < 0.5
+    noisy = np.where(hit, np.where(salt, 255, 0), a)
+    return Grid.from_array(noisy), Grid.from_array(hit.astype(np.int64))
+
+
+def video_restore_pipeline(frames: Iterable, *, width: int = 1, partitions: int = 1,
+                           mode=DeploymentMode.ONE_TO_ONE, cfg: Optional[RestoreConfig] = None,
+                           writer: Optional[Callable] = None, loader: Optional[Callable] = None,
+                           mask_writer: Optional[Callable] = None) -> StreamReport:
+    """read -> detect -> ordered_farm(restore, width) -> write
+    (apps/denoise.py:307-368)."""
+    mode = DeploymentMode.parse(mode)
+    if mode is DeploymentMode.ONE_TO_N and partitions < 2:
+        raise GridError("1:n deployment needs at least 2 partitions")
+    eff = partitions if mode is DeploymentMode.ONE_TO_N else 1
+    cfg = cfg or RestoreConfig()
+
+    read = Stage(loader or (lambda f: f), name="read")
+    detect_group = WorkerGroup(1)
+
+    def detect_fn(img: Grid):
+        mask = amf_detect(img, wmax=cfg.amf_wmax, group=detect_group)
+        if mask_writer is not None:
+            mask_writer(mask)
+        return img, mask
+
+    detect = Stage(detect_fn, name="detect")
+
+    def make_restorer():
+        grp = WorkerGroup(eff)
+
+        class _Restorer:
+            def __call__(self, pair):
+                img, mask = pair
+                out, _rep = restore_regularize(
+                    img, mask, cfg, partitions=eff,
+                    mode=mode if eff > 1 else DeploymentMode.ONE_TO_ONE, group=grp)
+                return out
+
+            def close(self):
+                grp.close()
+
+        return _Restorer()
+
+    restore = Stage(factory=make_restorer, name="restore")
+    if writer is None:
+        write = Stage(lambda g: g, name="write")
+    else:
+        def write_fn(g):
+            writer(g)
+            return g
+
+        write = Stage(write_fn, name="write")
+    top = pipeline(read, detect, ordered_farm(restore, width), write)
+    try:
+        return run_stream(frames, top, sink=lambda _item: None)
+    finally:
+        detect_group.close()

@@ -32,7 +32,8 @@ struct KernelOps {
 const KernelOps* helmholtz_ops();
 const KernelOps* life_ops();
 const KernelOps* restore_ops();
-const KernelOps* map_ops();  // single-pass map kernels (Sobel, AMF) behind the run API
+const KernelOps* u8_ops();   // Sobel / Life (sk_u8stencil.cu)
+const KernelOps* amf_ops();  // adaptive-median detection (sk_amf.cu)
 
 int device_sms(int device);
 

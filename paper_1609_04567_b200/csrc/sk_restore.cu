@@ -1,0 +1,387 @@
+// Variational restoration of flagged pixels (phase two of the denoiser).
+//
+// Reference: restore_kernel block route apps/denoise.py:209-246 (point route
+// :178-207), ring order _RING :35, search constants :37-45, |new-old| delta
+// and float sum :252-259, restore_regularize :262-288.
+//
+// For each flagged pixel (mask == 1), 18 ternary-search steps on [0, 255]
+// minimise F(u) = beta * sum_ring w * sqrt((u - v)^2 + eps), with w = 1 for a
+// flagged neighbour, 2 for a clean one, and off-image neighbours skipped (the
+// block route's weight-0 terms add +0.0, which leaves the sum unchanged).
+// Clean pixels never change.  All arithmetic is fp64 in the reference's
+// order with round-to-nearest intrinsics and IEEE sqrt; (hi - lo) / 3.0 uses
+// the exact 3-op division by a constant.  Result: bit-identical grids.
+//
+// FP64-pipe-bound (~1.5k flops + 288 sqrt per pixel-iteration), so work is
+// cut exactly, not approximately:
+//  * flagged list: only flagged pixels are visited (built once per run by a
+//    deterministic count/scan/scatter; in pixel order, so each partition's
+//    pixels are a contiguous sub-range).
+//  * exact active set: a pixel's output depends only on its 8 ring values
+//    (the mask is static), so if none of them changed in the previous
+//    iteration its output equals its previous output; it is copied, not
+//    recomputed.  Change flags are ping-ponged per iteration.
+//  * in-CTA compaction: active entries go to a shared-memory queue that all
+//    threads drain, so a sparse active set still keeps every lane busy.
+// The delta reduce is deterministic: each entry's |delta| lands at its fixed
+// position in the chunk, positions are summed in a fixed order, chunk
+// partials are folded per partition, partitions in ascending order.
+#include "sk_internal.h"
+
+namespace sk {
+
+constexpr int kRB = 128;        // threads per CTA
+constexpr int kPer = 4;         // list entries per thread per chunk
+constexpr int kCh = kRB * kPer;  // entries per chunk
+constexpr int kSteps = 18;      // ceil(log(1020) / log(1.5)), apps/denoise.py:39-45
+
+struct RestoreArgs {
+  const double* src;
+  double* buf[2];
+  const unsigned char* mask;
+  long long pitch, src_pitch, mask_pitch;
+  int rows, cols;
+  const int* list;            // flagged pixels, row * cols + col, ascending
+  unsigned char* chg[2];      // per-pixel change flags, ping-pong by iteration
+  int part_off[kMaxParts + 1];  // list offsets per partition
+  double beta, eps;
+  LoopCtl L;
+};
+
+__device__ __forceinline__ double F_eval(double u, const double* v, const double* w, int n,
+                                         double eps, double beta) {
+  double s = 0.0;
+  for (int k = 0; k < n; ++k) {
+    const double t = xsub(u, v[k]);
+    s = xadd(s, xmul(w[k], xsqrt(xadd(xmul(t, t), eps))));
+  }
+  return xmul(beta, s);
+}
+
+__device__ double restore_pixel(const RestoreArgs& a, const double* front, long long fp, int i,
+                                int j) {
+  double v[8], w[8];
+  int n = 0;
+  const int di[8] = {-1, -1, -1, 0, 0, 1, 1, 1};
+  const int dj[8] = {-1, 0, 1, -1, 1, -1, 0, 1};
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int ni = i + di[k], nj = j + dj[k];
+    if (ni >= 0 && ni < a.rows && nj >= 0 && nj < a.cols) {
+      v[n] = front[(long long)ni * fp + nj];
+      w[n] = a.mask[(long long)ni * a.mask_pitch + nj] == 1 ? 1.0 : 2.0;
+      ++n;
+    }
+  }
+  const double r3 = __drcp_rn(3.0);
+  double lo = 0.0, hi = 255.0;
+#pragma unroll 1
+  for (int s = 0; s < kSteps; ++s) {
+    const double third = div_const(xsub(hi, lo), 3.0, r3);
+    const double m1 = xadd(lo, third);
+    const double m2 = xsub(hi, third);
+    if (F_eval(m1, v, w, n, a.eps, a.beta) <= F_eval(m2, v, w, n, a.eps, a.beta)) hi = m2;
+    else lo = m1;
+  }
+  return xmul(0.5, xadd(lo, hi));
+}
+
+__global__ void __launch_bounds__(kRB) restore_sweep(const __grid_constant__ RestoreArgs a) {
+  __shared__ double sh[kRB / 32];
+  __shared__ double s_delta[kCh];
+  __shared__ short s_queue[kCh];
+  __shared__ int s_qlen;
+  __shared__ int s_chunk;
+  const long long it = loop_enter(a.L);
+  if (it == 0) return;
+  const double* front = it == 1 ? a.src : a.buf[(it - 1) & 1];
+  const long long fp = it == 1 ? a.src_pitch : a.pitch;
+  double* back = a.buf[it & 1];
+  const unsigned char* cprev = a.chg[(it - 1) & 1];
+  unsigned char* ccur = a.chg[it & 1];
+  const int total = a.L.part_chunk[a.L.nparts];
+  for (int c = next_chunk(a.L, &s_chunk); c < total; c = next_chunk(a.L, &s_chunk)) {
+    int p = 0;
+    while (p + 1 < a.L.nparts && c >= a.L.part_chunk[p + 1]) ++p;
+    const int e0 = a.part_off[p] + (c - a.L.part_chunk[p]) * kCh;
+    const int e1 = min(e0 + kCh, a.part_off[p + 1]);
+    if (threadIdx.x == 0) s_qlen = 0;
+    __syncthreads();
+    // phase 1: classify; inactive entries are settled immediately
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      const int pos = q * kRB + threadIdx.x;
+      const int e = e0 + pos;
+      s_delta[pos] = 0.0;
+      if (e < e1) {
+        const int pix = a.list[e];
+        const int i = pix / a.cols, j = pix - i * a.cols;
+        bool active = it == 1;
+        if (!active) {
+          for (int di = -1; di <= 1 && !active; ++di) {
+            const int ni = i + di;
+            if (ni < 0 || ni >= a.rows) continue;
+            for (int dj = -1; dj <= 1; ++dj) {
+              const int nj = j + dj;
+              if ((di | dj) == 0 || nj < 0 || nj >= a.cols) continue;
+              if (cprev[(long long)ni * a.cols + nj]) {
+                active = true;
+                break;
+              }
+            }
+          }
+        }
+        if (active) {
+          const int slot = atomicAdd(&s_qlen, 1);
+          s_queue[slot] = (short)pos;
+        } else {
+          back[(long long)i * a.pitch + j] = front[(long long)i * fp + j];
+          ccur[pix] = 0;
+        }
+      }
+    }
+    __syncthreads();
+    // phase 2: drain the active queue (any thread may take any entry; each
+    // result and |delta| goes to the entry's own position)
+    const int qlen = s_qlen;
+    for (int q = threadIdx.x; q < qlen; q += kRB) {
+      const int pos = s_queue[q];
+      const int pix = a.list[e0 + pos];
+      const int i = pix / a.cols, j = pix - i * a.cols;
+      const double old = front[(long long)i * fp + j];
+      const double nv = restore_pixel(a, front, fp, i, j);
+      back[(long long)i * a.pitch + j] = nv;
+      ccur[pix] = nv != old;
+      s_delta[pos] = fabs(xsub(nv, old));
+    }
+    __syncthreads();
+    double t = 0.0;
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) t = xadd(t, s_delta[q * kRB + threadIdx.x]);
+    const double v = block_reduce<kRB>(SK_REDUCE_SUM, t, sh);
+    if (threadIdx.x == 0) a.L.partials[c] = v;
+  }
+  loop_finalize<kRB>(a.L, it, sh);
+}
+
+// ---- flagged-list construction: count per segment, scan, scatter (ordered)
+
+constexpr int kSeg = 4096;  // pixels per segment (one CTA)
+
+__global__ void flag_count(const unsigned char* mask, long long mpitch, int rows, int cols,
+                           int* seg_count) {
+  const long long npix = (long long)rows * cols;
+  const long long s0 = (long long)blockIdx.x * kSeg;
+  int n = 0;
+  for (long long p = s0 + threadIdx.x; p < s0 + kSeg && p < npix; p += blockDim.x) {
+    const int i = (int)(p / cols), j = (int)(p - (long long)i * cols);
+    n += mask[(long long)i * mpitch + j] == 1;
+  }
+  n = __reduce_add_sync(0xffffffffu, n);
+  __shared__ int ws[32];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = n;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += ws[w];
+    seg_count[blockIdx.x] = t;
+  }
+}
+
+__global__ void flag_scan(int* seg, int nseg) {  // exclusive, single CTA
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < nseg; base += blockDim.x) {
+    const int i = base + threadIdx.x;
+    const int v = i < nseg ? seg[i] : 0;
+    // inclusive warp scan then block scan
+    int x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if ((threadIdx.x & 31) >= o) x += y;
+    }
+    __shared__ int wsum[32];
+    if ((threadIdx.x & 31) == 31) wsum[threadIdx.x >> 5] = x;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      int s = threadIdx.x < (blockDim.x >> 5) ? wsum[threadIdx.x] : 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, s, o);
+        if (threadIdx.x >= o) s += y;
+      }
+      wsum[threadIdx.x] = s;
+    }
+    __syncthreads();
+    const int w = threadIdx.x >> 5;
+    const int incl = x + (w ? wsum[w - 1] : 0) + carry;
+    if (i < nseg) seg[i] = incl - v;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = incl;
+    __syncthreads();
+  }
+}
+
+__global__ void flag_scatter(const unsigned char* mask, long long mpitch, int rows, int cols,
+                             const int* seg_off, int* list) {
+  const long long npix = (long long)rows * cols;
+  const long long s0 = (long long)blockIdx.x * kSeg;
+  __shared__ int base;
+  __shared__ int wcount[32];
+  if (threadIdx.x == 0) base = seg_off[blockIdx.x];
+  __syncthreads();
+  for (long long p0 = s0; p0 < s0 + kSeg && p0 < npix; p0 += blockDim.x) {
+    const long long p = p0 + threadIdx.x;
+    bool f = false;
+    if (p < s0 + kSeg && p < npix) {
+      const int i = (int)(p / cols), j = (int)(p - (long long)i * cols);
+      f = mask[(long long)i * mpitch + j] == 1;
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, f);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) wcount[w] = __popc(bal);
+    __syncthreads();
+    int before = 0;
+    for (int k = 0; k < w; ++k) before += wcount[k];
+    if (f) list[base + before + __popc(bal & ((1u << lane) - 1))] = (int)p;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int t = 0;
+      for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += wcount[k];
+      base += t;
+    }
+    __syncthreads();
+  }
+}
+
+// partition p's flagged pixels start at lower_bound(list, part_row[p] * cols)
+__global__ void list_bounds(const int* list, int n, const int* part_row, int nparts, int cols,
+                            int* off) {
+  const int p = threadIdx.x;
+  if (p > nparts) return;
+  if (p == nparts) {
+    off[p] = n;
+    return;
+  }
+  const long long key = (long long)part_row[p] * cols;
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if ((long long)list[mid] < key) lo = mid + 1;
+    else hi = mid;
+  }
+  off[p] = lo;
+}
+
+// ---------------------------------------------------------------- host side
+
+namespace {
+
+enum { AUX_LIST = 0, AUX_CHG = 1, AUX_SEG = 2, AUX_OFF = 3 };
+
+int setup(sk_run* r) {
+  const sk_plan& p = r->plan;
+  if (p.dtype != SK_F64 || p.reduce_op != SK_REDUCE_SUM || p.delta_op != SK_DELTA_ABS) {
+    set_error("restore: f64 grid with the |new-old| SUM reduce (restore_regularize) required");
+    return SK_ERR_UNSUPPORTED;
+  }
+  if (!r->env) {
+    set_error("restore: the noise map (env) is required");
+    return SK_ERR_ARG;
+  }
+  if ((long long)p.rows * p.cols >= (1ll << 31)) {
+    set_error("restore: grid too large for 32-bit pixel indices");
+    return SK_ERR_ARG;
+  }
+  cudaStream_t s = r->stream;
+  const long long npix = p.rows * p.cols;
+  const int nseg = (int)((npix + kSeg - 1) / kSeg);
+  const unsigned char* mask = static_cast<const unsigned char*>(r->env);
+  int* seg = nullptr;
+  SK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&seg), sizeof(int) * (nseg + 1 + 2 * (kMaxParts + 1)), s));
+  r->aux[AUX_SEG] = seg;
+  int* d_prow = seg + nseg + 1;
+  int* d_off = d_prow + kMaxParts + 1;
+  SK_CUDA(cudaMemsetAsync(seg + nseg, 0, sizeof(int), s));
+  flag_count<<<nseg, 256, 0, s>>>(mask, r->env_pitch, (int)p.rows, (int)p.cols, seg);
+  flag_scan<<<1, 1024, 0, s>>>(seg, nseg + 1);  // seg[nseg] = total
+  int nflag = 0;
+  SK_CUDA(cudaMemcpyAsync(&nflag, seg + nseg, sizeof(int), cudaMemcpyDeviceToHost, s));
+  SK_CUDA(cudaStreamSynchronize(s));
+  int* list = nullptr;
+  SK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&list), sizeof(int) * ((size_t)nflag + 1), s));
+  r->aux[AUX_LIST] = list;
+  r->aux_n[AUX_LIST] = nflag;
+  flag_scatter<<<nseg, 256, 0, s>>>(mask, r->env_pitch, (int)p.rows, (int)p.cols, seg, list);
+  SK_CUDA(cudaMemcpyAsync(d_prow, r->part_row, sizeof(int) * (r->nparts + 1),
+                          cudaMemcpyHostToDevice, s));
+  list_bounds<<<1, kMaxParts + 1, 0, s>>>(list, nflag, d_prow, r->nparts, (int)p.cols, d_off);
+  SK_CUDA(cudaGetLastError());
+  int* offs = new int[kMaxParts + 1];
+  r->aux[AUX_OFF] = offs;
+  SK_CUDA(cudaMemcpyAsync(offs, d_off, sizeof(int) * (r->nparts + 1), cudaMemcpyDeviceToHost, s));
+  unsigned char* chg = nullptr;
+  SK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&chg), (size_t)npix * 2, s));
+  r->aux[AUX_CHG] = chg;
+  SK_CUDA(cudaMemsetAsync(chg, 0, (size_t)npix * 2, s));
+  // both iteration buffers start as the input: clean pixels never change
+  for (int b = 0; b < 2; ++b)
+    SK_CUDA(cudaMemcpy2DAsync(r->buf[b], r->pitch * 8, r->src, r->src_pitch * 8, p.cols * 8,
+                              p.rows, cudaMemcpyDeviceToDevice, s));
+  SK_CUDA(cudaStreamSynchronize(s));
+  // work chunks per partition over its contiguous sub-range of the list
+  int nch = 0;
+  r->part_chunk[0] = 0;
+  for (int i = 0; i < r->nparts; ++i) {
+    nch += (offs[i + 1] - offs[i] + kCh - 1) / kCh;
+    r->part_chunk[i + 1] = nch;
+  }
+  r->nchunks = nch;
+  int per_sm = 0;
+  SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, restore_sweep, kRB, 0));
+  const long long slots = (long long)device_sms(r->device) * (per_sm > 0 ? per_sm : 1);
+  r->grid = (int)(slots < nch ? slots : nch);
+  if (r->grid < 1) r->grid = 1;
+  r->block = kRB;
+  return SK_OK;
+}
+
+int launch(sk_run* r, const LoopCtl& L, cudaStream_t s) {
+  RestoreArgs a{};
+  a.src = static_cast<const double*>(r->src);
+  a.buf[0] = static_cast<double*>(r->buf[0]);
+  a.buf[1] = static_cast<double*>(r->buf[1]);
+  a.mask = static_cast<const unsigned char*>(r->env);
+  a.pitch = r->pitch;
+  a.src_pitch = r->src_pitch;
+  a.mask_pitch = r->env_pitch;
+  a.rows = (int)r->plan.rows;
+  a.cols = (int)r->plan.cols;
+  a.list = static_cast<const int*>(r->aux[AUX_LIST]);
+  unsigned char* chg = static_cast<unsigned char*>(r->aux[AUX_CHG]);
+  a.chg[0] = chg;
+  a.chg[1] = chg + r->plan.rows * r->plan.cols;
+  const int* offs = static_cast<const int*>(r->aux[AUX_OFF]);
+  for (int i = 0; i <= r->nparts; ++i) a.part_off[i] = offs[i];
+  a.beta = r->plan.params[0];
+  a.eps = r->plan.params[1];
+  a.L = L;
+  restore_sweep<<<r->grid, kRB, 0, s>>>(a);
+  SK_CUDA(cudaGetLastError());
+  return SK_OK;
+}
+
+void teardown(sk_run* r) {
+  for (int k : {AUX_LIST, AUX_CHG, AUX_SEG})
+    if (r->aux[k]) cudaFreeAsync(r->aux[k], r->stream);
+  delete[] static_cast<int*>(r->aux[AUX_OFF]);
+  r->aux[AUX_OFF] = nullptr;
+}
+
+const KernelOps kOps = {setup, launch, teardown};
+
+}  // namespace
+
+const KernelOps* restore_ops() { return &kOps; }
+
+}  // namespace sk

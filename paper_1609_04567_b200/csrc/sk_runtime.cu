@@ -155,8 +155,8 @@ int sk_run_begin(const sk_plan* plan, const void* d_src, int64_t src_pitch, cons
     case SK_KERNEL_HELMHOLTZ: ops = helmholtz_ops(); break;
     case SK_KERNEL_LIFE: ops = life_ops(); break;
     case SK_KERNEL_RESTORE: ops = restore_ops(); break;
-    case SK_KERNEL_SOBEL:
-    case SK_KERNEL_AMF: ops = map_ops(); break;
+    case SK_KERNEL_SOBEL: ops = u8_ops(); break;
+    case SK_KERNEL_AMF: ops = amf_ops(); break;
     default:
       set_error("sk_run_begin: unknown kernel id");
       return SK_ERR_ARG;

@@ -1,0 +1,369 @@
+// u8 3x3 stencils: Sobel edge magnitude and Conway's Game of Life.
+//
+// Reference: Sobel block kernel apps/sobel.py:47-66 (point :33-44; pixel-sum
+// reduce :73-74); Life block kernel apps/life.py:35-43 (liveness :46-52).
+//
+// HBM-bound: 2 B/pixel (read 1 + write 1).  Each thread owns 8 contiguous
+// pixels of a row (one 8-byte load) and marches down a chunk of rows.  Both
+// stencils are separable, so each row is reduced once to per-pixel
+// horizontal features and the output combines the features of rows r-1, r,
+// r+1:
+//   Sobel: D = x[c+1] - x[c-1],  S = x[c-1] + 2 x[c] + x[c+1]
+//          gx = D(r-1) + 2 D(r) + D(r+1),  gy = S(r+1) - S(r-1)
+//   Life : T = x[c-1] + x[c] + x[c+1];  n = T(r-1) + T(r) + T(r+1) - x
+// Sobel's border rule (off-image neighbours read as the CENTRE pixel,
+// apps/sobel.py:53-56) is not separable; border pixels take a generic 9-tap
+// path.  Magnitude rounding: for every achievable n = gx^2 + gy^2,
+// min(255, rint(sqrt(n))) needs sqrt only to ~1e-6 relative (n is an integer,
+// so sqrt(n) is never within 4.9e-4 of a rounding boundary k+0.5 for k <= 255,
+// and n >= 255.5^2 clips to 255), so the hardware sqrt.approx is exact here;
+// tests compare every pixel against the reference.
+#include "sk_internal.h"
+#include "sk_sweep.cuh"
+
+namespace sk {
+
+enum { U8_SOBEL = 0, U8_LIFE = 1 };
+
+struct U8Args {
+  Sweep2D g;
+  LoopCtl L;
+  // batched frames (BATCH mode): frame f at src/out + f * stride
+  long long in_stride, out_stride;
+  const unsigned char* bin;
+  unsigned char* bout;
+  long long* sums;
+  int frames;
+  int chunks_per_frame;
+};
+
+__device__ __forceinline__ int byte_of(unsigned w, int k) {
+  return (int)__byte_perm(w, 0u, 0x4440u | (unsigned)k);
+}
+
+__device__ __forceinline__ int sobel_mag(int gx, int gy) {
+  const int n = gx * gx + gy * gy;
+  float s;
+  asm("sqrt.approx.f32 %0, %1;" : "=f"(s) : "f"((float)n));
+  const int m = __float2int_rn(s);
+  return m > 255 ? 255 : m;
+}
+
+// One image row as seen by a thread: 8 pixels plus the left/right neighbours.
+struct Row8 {
+  int x[10];  // x[0] = pixel col-1, x[1..8] = cols col..col+7, x[9] = col+8
+};
+
+template <int OP, int BLOCK, int REDUCE, bool BATCH>
+__global__ void __launch_bounds__(BLOCK) u8_sweep(const __grid_constant__ U8Args a) {
+  constexpr int VEC = 8;
+  constexpr unsigned FULL = 0xffffffffu;
+  __shared__ double sh[BLOCK / 32];
+  __shared__ int s_chunk;
+  const Sweep2D& g = a.g;
+  long long it = 1;
+  if (!BATCH) {
+    it = loop_enter(a.L);
+    if (it == 0) return;
+  }
+  const int lane = threadIdx.x & 31;
+  const int cols = g.cols, rows = g.rows;
+  const int total = BATCH ? a.frames * a.chunks_per_frame : a.L.part_chunk[a.L.nparts];
+
+  for (int c = next_chunk(a.L, &s_chunk); c < total; c = next_chunk(a.L, &s_chunk)) {
+    int frame = 0, cb, r0, r1, cc = c;
+    const unsigned char* front;
+    unsigned char* back;
+    long long fp, op;
+    if (BATCH) {
+      frame = c / a.chunks_per_frame;
+      cc = c - frame * a.chunks_per_frame;
+      front = a.bin + frame * a.in_stride;
+      back = a.bout + frame * a.out_stride;
+      fp = g.src_pitch;
+      op = g.pitch;
+    } else {
+      front = static_cast<const unsigned char*>(it == 1 ? g.src : g.buf[(it - 1) & 1]);
+      fp = it == 1 ? g.src_pitch : g.pitch;
+      back = static_cast<unsigned char*>(g.buf[it & 1]);
+      op = g.pitch;
+    }
+    chunk_geom(a.L, g, cc, &cb, &r0, &r1);
+    const int col = cb * (BLOCK * VEC) + (int)threadIdx.x * VEC;
+    const int nvalid = cols - col;
+    const bool active = nvalid > 0;
+    const bool has_l = lane == 0 && col > 0 && active;
+    const bool has_r = lane == 31 && nvalid > VEC;
+    // this thread touches the left/right image border
+    const bool edge_col = active && (col == 0 || nvalid <= VEC);
+
+    auto load_row = [&](int r, Row8& R) {
+      uint2 w = make_uint2(0u, 0u);
+      const bool in = active && r >= 0 && r < rows;
+      const unsigned char* p = front + (long long)r * fp + col;
+      if (in) w = __ldg(reinterpret_cast<const uint2*>(p));
+      int xl = (in && has_l) ? (int)__ldg(p - 1) : 0;
+      int xr = (in && has_r) ? (int)__ldg(p + VEC) : 0;
+      const unsigned lo_prev = __shfl_up_sync(FULL, w.y, 1);
+      const unsigned hi_next = __shfl_down_sync(FULL, w.x, 1);
+      if (lane != 0) xl = byte_of(lo_prev, 3);
+      if (lane != 31) xr = byte_of(hi_next, 0);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        R.x[1 + k] = byte_of(w.x, k);
+        R.x[5 + k] = byte_of(w.y, k);
+      }
+      R.x[0] = xl;
+      R.x[9] = xr;
+      // off-image columns are 0 here; Life wants exactly that (dead),
+      // Sobel's border pixels are recomputed by the generic path
+      if (nvalid < VEC + 1) {
+#pragma unroll
+        for (int k = 1; k <= VEC + 1; ++k)
+          if (k > nvalid) R.x[k] = 0;
+      }
+      if (col == 0) R.x[0] = 0;
+    };
+
+    double acc = REDUCE == SK_REDUCE_MAX ? -INFINITY : 0.0;
+    long long iacc = 0;
+    Row8 up, cen, dn;
+    load_row(r0 - 1, up);
+    load_row(r0, cen);
+    // horizontal features of rows r-1 and r
+    int hA[VEC], hB[VEC], hA2[VEC], hB2[VEC];  // Sobel: D, S ; Life: T in hA
+#pragma unroll
+    for (int k = 0; k < VEC; ++k) {
+      if (OP == U8_SOBEL) {
+        hA[k] = up.x[k + 2] - up.x[k];
+        hB[k] = up.x[k] + 2 * up.x[k + 1] + up.x[k + 2];
+        hA2[k] = cen.x[k + 2] - cen.x[k];
+        hB2[k] = cen.x[k] + 2 * cen.x[k + 1] + cen.x[k + 2];
+      } else {
+        hA[k] = up.x[k] + up.x[k + 1] + up.x[k + 2];
+        hA2[k] = cen.x[k] + cen.x[k + 1] + cen.x[k + 2];
+        hB[k] = hB2[k] = 0;
+      }
+    }
+    for (int r = r0; r < r1; ++r) {
+      load_row(r + 1, dn);
+      int out[VEC];
+#pragma unroll
+      for (int k = 0; k < VEC; ++k) {
+        if (OP == U8_SOBEL) {
+          const int d3 = dn.x[k + 2] - dn.x[k];
+          const int s3 = dn.x[k] + 2 * dn.x[k + 1] + dn.x[k + 2];
+          const int gx = hA[k] + 2 * hA2[k] + d3;
+          const int gy = s3 - hB[k];
+          out[k] = sobel_mag(gx, gy);
+          hA[k] = hA2[k];
+          hB[k] = hB2[k];
+          hA2[k] = d3;
+          hB2[k] = s3;
+        } else {
+          const int t3 = dn.x[k] + dn.x[k + 1] + dn.x[k + 2];
+          const int x = cen.x[k + 1];
+          const int n = hA[k] + hA2[k] + t3 - x;
+          out[k] = (n == 3 || (x == 1 && n == 2)) ? 1 : 0;
+          hA[k] = hA2[k];
+          hA2[k] = t3;
+        }
+      }
+      if (OP == U8_SOBEL && (r == 0 || r == rows - 1 || edge_col)) {
+        // generic 9-tap with off-image reads replaced by the centre pixel
+        const bool uok = r > 0, dok = r < rows - 1;
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) {
+          const int cc0 = col + k;
+          const bool lok = cc0 > 0, rok = cc0 + 1 < cols;
+          const int ctr = cen.x[k + 1];
+          const int nw = (uok && lok) ? up.x[k] : ctr, n = uok ? up.x[k + 1] : ctr;
+          const int ne = (uok && rok) ? up.x[k + 2] : ctr;
+          const int w = lok ? cen.x[k] : ctr, e = rok ? cen.x[k + 2] : ctr;
+          const int sw = (dok && lok) ? dn.x[k] : ctr, s = dok ? dn.x[k + 1] : ctr;
+          const int se = (dok && rok) ? dn.x[k + 2] : ctr;
+          const int gx = -nw + ne - 2 * w + 2 * e - sw + se;
+          const int gy = -nw - 2 * n - ne + sw + 2 * s + se;
+          out[k] = sobel_mag(gx, gy);
+        }
+      }
+      unsigned lo = 0, hi = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const bool in0 = k < nvalid, in1 = k + 4 < nvalid;
+        const int v0 = in0 ? out[k] : 0, v1 = in1 ? out[k + 4] : 0;
+        lo |= (unsigned)v0 << (8 * k);
+        hi |= (unsigned)v1 << (8 * k);
+        if (REDUCE == SK_REDUCE_MAX) {
+          if (in0) acc = fmax(acc, (double)v0);
+          if (in1) acc = fmax(acc, (double)v1);
+        } else {
+          iacc += v0 + v1;
+        }
+      }
+      if (active) *reinterpret_cast<uint2*>(back + (long long)r * op + col) = make_uint2(lo, hi);
+      up = cen;
+      cen = dn;
+    }
+    if (REDUCE == SK_REDUCE_SUM) acc = (double)iacc;
+    const double v = block_reduce<BLOCK>(REDUCE, acc, sh);
+    if (threadIdx.x == 0) {
+      if (BATCH) atomicAdd(reinterpret_cast<unsigned long long*>(&a.sums[frame]),
+                           (unsigned long long)(long long)v);
+      else a.L.partials[c] = v;
+    }
+  }
+  if (!BATCH) loop_finalize<BLOCK>(a.L, it, sh);
+}
+
+// ---------------------------------------------------------------- host side
+
+namespace {
+
+constexpr int kBlock = 128;
+constexpr int kVec = 8;
+
+using U8Fn = void (*)(const U8Args);
+
+U8Fn pick(int op, int reduce, bool batch) {
+  if (batch) return op == U8_SOBEL ? u8_sweep<U8_SOBEL, kBlock, SK_REDUCE_SUM, true>
+                                   : u8_sweep<U8_LIFE, kBlock, SK_REDUCE_SUM, true>;
+  if (op == U8_SOBEL)
+    return reduce == SK_REDUCE_MAX ? u8_sweep<U8_SOBEL, kBlock, SK_REDUCE_MAX, false>
+                                   : u8_sweep<U8_SOBEL, kBlock, SK_REDUCE_SUM, false>;
+  return reduce == SK_REDUCE_MAX ? u8_sweep<U8_LIFE, kBlock, SK_REDUCE_MAX, false>
+                                 : u8_sweep<U8_LIFE, kBlock, SK_REDUCE_SUM, false>;
+}
+
+// chunk geometry shared by loop and batch mode; returns slots (grid cap)
+int geometry(int device, U8Fn fn, long long rows, long long cols, int nparts, const int* part_row,
+             long long frames, int* colblocks, int* chunk_rows, int* part_chunk, int* nchunks,
+             int* grid) {
+  int per_sm = 0;
+  SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kBlock, 0));
+  const long long slots = (long long)device_sms(device) * (per_sm > 0 ? per_sm : 1);
+  *colblocks = (int)((cols + kBlock * kVec - 1) / (kBlock * kVec));
+  const long long want = slots * 4;
+  long long ch = (rows * (long long)*colblocks * frames + want - 1) / want;
+  ch = ch < 8 ? 8 : (ch > 256 ? 256 : ch);
+  *chunk_rows = (int)ch;
+  int n = 0;
+  part_chunk[0] = 0;
+  for (int i = 0; i < nparts; ++i) {
+    const int pr = part_row[i + 1] - part_row[i];
+    n += ((pr + *chunk_rows - 1) / *chunk_rows) * *colblocks;
+    part_chunk[i + 1] = n;
+  }
+  *nchunks = n;
+  const long long tot = (long long)n * frames;
+  *grid = (int)(slots < tot ? slots : tot);
+  if (*grid < 1) *grid = 1;
+  return SK_OK;
+}
+
+int op_of(const sk_run* r) { return r->plan.kernel == SK_KERNEL_LIFE ? U8_LIFE : U8_SOBEL; }
+
+int setup(sk_run* r) {
+  if (r->plan.dtype != SK_U8) {
+    set_error("sobel/life: grid must be u8");
+    return SK_ERR_UNSUPPORTED;
+  }
+  if (r->plan.delta_op != SK_DELTA_NONE) {
+    set_error("sobel/life: no delta reduce");
+    return SK_ERR_UNSUPPORTED;
+  }
+  U8Fn fn = pick(op_of(r), r->plan.reduce_op, false);
+  return geometry(r->device, fn, r->plan.rows, r->plan.cols, r->nparts, r->part_row, 1,
+                  &r->colblocks, &r->chunk_rows, r->part_chunk, &r->nchunks, &r->grid);
+}
+
+void fill_geom(const sk_run* r, Sweep2D& g) {
+  g.src = r->src;
+  g.src_pitch = r->src_pitch;
+  g.buf[0] = r->buf[0];
+  g.buf[1] = r->buf[1];
+  g.pitch = r->pitch;
+  g.env = nullptr;
+  g.env_pitch = 0;
+  g.rows = (int)r->plan.rows;
+  g.cols = (int)r->plan.cols;
+  g.halo_top = g.halo_bottom = 0;
+  g.colblocks = r->colblocks;
+  g.chunk_rows = r->chunk_rows;
+  for (int i = 0; i <= r->nparts; ++i) g.part_row[i] = r->part_row[i];
+}
+
+int launch(sk_run* r, const LoopCtl& L, cudaStream_t s) {
+  U8Args a{};
+  fill_geom(r, a.g);
+  a.L = L;
+  U8Fn fn = pick(op_of(r), r->plan.reduce_op, false);
+  fn<<<r->grid, kBlock, 0, s>>>(a);
+  SK_CUDA(cudaGetLastError());
+  return SK_OK;
+}
+
+void teardown(sk_run*) {}
+
+const KernelOps kOps = {setup, launch, teardown};
+
+}  // namespace
+
+const KernelOps* u8_ops() { return &kOps; }
+
+// Batched Sobel over frames (stream mode).  Uses a small device scratch for
+// the chunk counter (Status) allocated per call on the stream's pool.
+int sobel_frames(const uint8_t* in, long long in_pitch, long long in_fs, uint8_t* out,
+                 long long out_pitch, long long out_fs, int frames, long long rows, long long cols,
+                 long long* sums, cudaStream_t s) {
+  if (!in || !out || !sums || frames < 1 || rows < 1 || cols < 1 || in_pitch < cols ||
+      out_pitch < cols || (in_pitch % 8) || (out_pitch % 8) || (in_fs % 8) || (out_fs % 8) ||
+      (reinterpret_cast<uintptr_t>(in) % 8) || (reinterpret_cast<uintptr_t>(out) % 8)) {
+    set_error("sk_sobel_frames: bad arguments (pitches/strides/pointers must be 8-byte aligned)");
+    return SK_ERR_ARG;
+  }
+  int dev = 0;
+  SK_CUDA(cudaGetDevice(&dev));
+  U8Fn fn = pick(U8_SOBEL, SK_REDUCE_SUM, true);
+  U8Args a{};
+  int part_row[2] = {0, (int)rows};
+  int nch = 0, grid = 0;
+  int rc = geometry(dev, fn, rows, cols, 1, part_row, frames, &a.g.colblocks, &a.g.chunk_rows,
+                    a.L.part_chunk, &nch, &grid);
+  if (rc) return rc;
+  a.L.nparts = 1;
+  a.g.part_row[0] = 0;
+  a.g.part_row[1] = (int)rows;
+  a.g.rows = (int)rows;
+  a.g.cols = (int)cols;
+  a.g.src_pitch = in_pitch;
+  a.g.pitch = out_pitch;
+  a.bin = in;
+  a.bout = out;
+  a.in_stride = in_fs;
+  a.out_stride = out_fs;
+  a.sums = sums;
+  a.frames = frames;
+  a.chunks_per_frame = nch;
+  Status* st = nullptr;
+  SK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&st), sizeof(Status), s));
+  SK_CUDA(cudaMemsetAsync(st, 0, sizeof(Status), s));
+  SK_CUDA(cudaMemsetAsync(sums, 0, sizeof(long long) * frames, s));
+  a.L.st = st;
+  fn<<<grid, kBlock, 0, s>>>(a);
+  cudaError_t e = cudaGetLastError();
+  cudaFreeAsync(st, s);
+  if (e != cudaSuccess) return cuda_fail(e, "sobel_frames launch");
+  return SK_OK;
+}
+
+}  // namespace sk
+
+extern "C" int sk_sobel_frames(const uint8_t* d_in, int64_t in_pitch, int64_t in_frame_stride,
+                               uint8_t* d_out, int64_t out_pitch, int64_t out_frame_stride,
+                               int32_t frames, int64_t rows, int64_t cols, int64_t* d_sums,
+                               void* stream) {
+  return sk::sobel_frames(d_in, in_pitch, in_frame_stride, d_out, out_pitch, out_frame_stride,
+                          frames, rows, cols, reinterpret_cast<long long*>(d_sums),
+                          static_cast<cudaStream_t>(stream));
+}

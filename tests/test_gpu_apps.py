@@ -1,0 +1,149 @@
+"""Sobel, adaptive-median detection, restoration and Life on the device vs
+the reference's own outputs (golden fixtures from tests/golden/make_golden.py).
+
+Bar: bit-exact output images/masks, bit-exact fp64 restored grids, identical
+iteration counts and exhaustion flags; integer reduce values equal; the
+restore SUM reduce within rel 1e-12 (deterministic fp64 sum in a different
+order than numpy's pairwise sum).
+"""
+
+import numpy as np
+import pytest
+
+import paper_1609_04567_b200 as sk
+from paper_1609_04567_b200.apps import (GolConfig, RestoreConfig, amf_detect, amf_frames,
+                                        game_of_life, restore_regularize, sobel_filter,
+                                        sobel_frames)
+
+pytestmark = pytest.mark.gpu
+
+
+def _P(m):
+    return m.get("P", 1)
+
+
+def test_sobel_cases(golden):
+    for name in golden.cases("sobel"):
+        m = golden.meta[name]
+        img = golden[name + "/in"]
+        P = _P(m)
+        out, rep = sobel_filter(sk.Grid.from_array(img.astype(np.int64)), partitions=P,
+                                mode="1:n" if P > 1 else "1:1", with_report=True)
+        a = out.to_array()
+        assert a.dtype == np.int64
+        assert np.array_equal(a.astype(np.uint8), golden[name + "/out"]), name
+        assert rep.final_reduce == m["final_reduce"] and isinstance(rep.final_reduce, int), name
+        assert rep.iterations == 1
+        assert vars(rep.copies) == m["ledger"], name
+
+
+def test_sobel_frames_batched(golden):
+    import torch
+
+    names = ["sobel_130x259", "sobel_64x48_P3"]
+    for name in names:
+        img = golden[name + "/in"]
+        H, W = img.shape
+        Wp = -(-W // 8) * 8
+        frames = torch.zeros((3, H, Wp), dtype=torch.uint8, device="cuda")
+        for f in range(3):
+            frames[f, :, :W] = torch.from_numpy(np.roll(img, f, axis=0))
+        out = torch.zeros_like(frames)
+        # the kernel works on [H, W] inside a pitched [H, Wp] buffer
+        view = frames[:, :, :W]
+        edges, sums = sobel_frames(view, out=out[:, :, :W])
+        for f in range(3):
+            ref = golden[name + "/out"] if f == 0 else None
+            got = edges[f].cpu().numpy()
+            if ref is not None:
+                assert np.array_equal(got, ref), name
+            assert int(sums[f]) == int(got.astype(np.int64).sum())
+
+
+def test_amf_cases(golden):
+    for name in golden.cases("amf"):
+        m = golden.meta[name]
+        img = golden[name + "/in"]
+        P = _P(m)
+        mask = amf_detect(sk.Grid.from_array(img.astype(np.int64)), wmax=m["wmax"], partitions=P,
+                          mode="1:n" if P > 1 else "1:1")
+        a = mask.to_array()
+        assert np.array_equal(a.astype(np.uint8), golden[name + "/out"]), name
+        assert int(a.sum()) == m["flagged"]
+
+
+def test_amf_frames_batched(golden):
+    import torch
+
+    name = "amf_grad50_96"
+    img = torch.from_numpy(golden[name + "/in"]).cuda()
+    frames = torch.stack([img, img.flip(0), img.flip(1)])
+    masks, counts = amf_frames(frames)
+    assert np.array_equal(masks[0].cpu().numpy(), golden[name + "/out"])
+    assert np.array_equal(masks[1].cpu().numpy(), golden[name + "/out"][::-1])
+    assert int(counts[0]) == golden.meta[name]["flagged"]
+
+
+def test_restore_cases(golden):
+    for name in golden.cases("restore"):
+        m = golden.meta[name]
+        if not golden.has(name + "/in"):
+            continue
+        P = _P(m)
+        cfg = RestoreConfig(max_iterations=m["max_iterations"])
+        out, rep = restore_regularize(sk.Grid.from_array(golden[name + "/in"].astype(np.int64)),
+                                      sk.Grid.from_array(golden[name + "/mask"].astype(np.int64)),
+                                      cfg, partitions=P, mode="1:n" if P > 1 else "1:1")
+        assert rep.iterations == m["iterations"], name
+        assert rep.exhausted == m["exhausted"], name
+        assert np.array_equal(out.to_array(), golden[name + "/out"]), name
+        assert rep.final_reduce == pytest.approx(m["final_reduce"], rel=1e-12), name
+        assert vars(rep.copies) == m["ledger"], name
+
+
+def test_restore_empty_mask_one_iteration():
+    img = sk.Grid.from_array(np.arange(64, dtype=np.int64).reshape(8, 8))
+    out, rep = restore_regularize(img, sk.Grid.filled((8, 8), 0))
+    assert rep.iterations == 1 and rep.final_reduce == 0.0
+    assert out.data == [float(v) for v in range(64)]
+
+
+def test_life_cases(golden):
+    for name in golden.cases("life"):
+        m = golden.meta[name]
+        P = _P(m)
+        out, rep = game_of_life(sk.Grid.from_array(golden[name + "/in"].astype(np.int64)),
+                                config=GolConfig(m["rows"], m["cols"], steps=m["steps"]),
+                                partitions=P, mode="1:n" if P > 1 else "1:1")
+        assert np.array_equal(out.to_array().astype(np.uint8), golden[name + "/out"]), name
+        assert rep.final_reduce == m["final_reduce"]
+
+
+def test_life_blinker_and_glider():
+    blinker = [[0, 0, 0, 0, 0], [0, 0, 1, 0, 0], [0, 0, 1, 0, 0], [0, 0, 1, 0, 0], [0] * 5]
+    flipped = [[0] * 5, [0] * 5, [0, 1, 1, 1, 0], [0] * 5, [0] * 5]
+    one = game_of_life(sk.Grid.from_rows(blinker), config=GolConfig(5, 5, steps=1))[0]
+    two = game_of_life(one, config=GolConfig(5, 5, steps=1))[0]
+    assert one.to_rows() == flipped and two.to_rows() == blinker
+
+
+def test_video_pipeline_order_and_identity(golden):
+    from paper_1609_04567_b200.apps import salt_pepper, video_restore_pipeline
+
+    r = np.arange(12)[:, None]
+    c = np.arange(12)[None, :]
+    base = sk.Grid.from_array(((r * 3 + c * 2) % 200 + 20).astype(np.int64))
+    frames = [salt_pepper(base, 0.2, seed=60 + i)[0] for i in range(6)]
+    outs = {}
+    for width in (1, 3):
+        got = []
+        rep = video_restore_pipeline(frames, width=width, writer=lambda g: got.append(g))
+        assert rep.items_out == 6 and rep.failures == []
+        outs[width] = got
+    for a, b in zip(outs[1], outs[3]):
+        assert a == b
+    # each frame equals a standalone restore of that frame
+    for f, o in zip(frames, outs[1]):
+        mask = amf_detect(f)
+        ref, _ = restore_regularize(f, mask)
+        assert o == ref

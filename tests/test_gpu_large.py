@@ -1,0 +1,81 @@
+"""Benchmark-config parity on the device: the BASELINE configs (or their
+largest reference-runnable sizes) against the reference's own outputs
+(SHA-256 of the output bytes, iteration counts) from golden_large.json."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+import paper_1609_04567_b200 as sk
+from oracle import stencil_oracle as O
+from paper_1609_04567_b200.apps import (HelmholtzConfig, amf_detect, helmholtz_kernel,
+                                        helmholtz_solve, restore_regularize, sobel_filter)
+
+pytestmark = pytest.mark.gpu
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def test_c1_helmholtz_1024_fp32_max(golden_large):
+    for name, rhs in (("C1_helm_f32_max_unit_1024", np.ones((1024, 1024), np.float32)),
+                      ("C1_helm_f32_max_rand0_1024",
+                       np.random.default_rng(0).random((1024, 1024)).astype(np.float32))):
+        m = golden_large.meta[name]
+        u0 = sk.Grid((1024, 1024), np.zeros((1024, 1024), np.float32))
+        for P in (1, 8):
+            out, rep = sk.parallel_loop("1:n" if P > 1 else "1:1", P, 1,
+                                        helmholtz_kernel(HelmholtzConfig(1024, 1024)),
+                                        sk.max_combinator(0.0), sk.Condition.below(1e-4), u0,
+                                        env=sk.Grid(rhs.shape, rhs), delta=sk.abs_change())
+            assert rep.iterations == m["iterations"]
+            assert rep.final_reduce == m["final_reduce"]
+            assert sha(out.to_array()) == m["sha"], name
+
+
+def test_c1_helmholtz_solve_fp64(golden_large):
+    m = golden_large.meta["C1_helm_f64_solve_unit_1024"]
+    cfg = HelmholtzConfig(1024, 1024, tol=m["tol"])
+    u, rep = helmholtz_solve(cfg, sk.Grid.filled((1024, 1024), 1.0), partitions=8)
+    assert rep.iterations == m["iterations"]
+    assert sha(u.to_array()) == m["sha"]
+    assert rep.final_reduce == pytest.approx(m["final_reduce"], rel=1e-12)
+
+
+def test_c2_sobel_2048(golden_large):
+    for seed in (0, 42, 43):
+        m = golden_large.meta[f"C2_sobel_rng{seed}_2048"]
+        img = np.random.default_rng(seed).integers(0, 256, (2048, 2048))
+        out, rep = sobel_filter(sk.Grid.from_array(img), with_report=True)
+        assert rep.final_reduce == m["final_reduce"]
+        assert sha(out.to_array().astype(np.uint8)) == m["sha"]
+
+
+def test_c3_denoise_512(golden_large):
+    noisy, _ = O.salt_pepper(O.gradient_image(512, 512), 0.5, seed=42)
+    ma = golden_large.meta["C3_amf_grad50_512"]
+    mask = amf_detect(sk.Grid.from_array(noisy))
+    assert sha(mask.to_array().astype(np.uint8)) == ma["sha"]
+    mr = golden_large.meta["C3_restore_grad50_512_P8"]
+    out, rep = restore_regularize(sk.Grid.from_array(noisy), mask, partitions=8)
+    assert rep.iterations == mr["iterations"] and rep.exhausted == mr["exhausted"]
+    assert sha(out.to_array()) == mr["sha"]
+    assert rep.final_reduce == pytest.approx(mr["final_reduce"], rel=1e-12)
+
+
+@pytest.mark.parametrize("i", [0, 1, 2, 3])
+def test_c5_frames(golden_large, i):
+    noisy, _ = O.salt_pepper(O.synthetic_frame(1080, 1920, i), 0.1, seed=42 + i)
+    ma = golden_large.meta[f"C5_amf_frame{i}"]
+    mask = amf_detect(sk.Grid.from_array(noisy))
+    assert sha(mask.to_array().astype(np.uint8)) == ma["sha"]
+    mr = golden_large.meta[f"C5_restore_frame{i}_P8"]
+    for P in (1, 8):
+        out, rep = restore_regularize(sk.Grid.from_array(noisy), mask, partitions=P,
+                                      mode="1:n" if P > 1 else "1:1")
+        assert rep.iterations == mr["iterations"]
+        a = out.to_array()
+        assert sha(a) == mr["sha"]
+        assert sha(np.clip(np.rint(a), 0, 255).astype(np.uint8)) == mr["sha_u8"]
