@@ -136,6 +136,21 @@ int sk_run_result(sk_run* run, int64_t it, int32_t* which);
  * iteration -- the per-rank partial a multi-GPU driver all-gathers. */
 int sk_run_value_ptr(sk_run* run, void** d_value);
 
+/* Multi-GPU (one run per rank, row blocks): after iteration t's sweep and
+ * the all-gather of every rank's sk_run_value_ptr value into d_partials[n]
+ * (rank order), fold them in ascending rank order from the identity (the
+ * reference's host combine, partition.py:642-646), evaluate `cond` for
+ * iteration t on the device and stop the run if it holds.  Enqueued on the
+ * run's stream; later sweeps of a stopped run are no-ops, so a driver may
+ * enqueue several iterations ahead without reading anything back. */
+int sk_run_combine(sk_run* run, const double* d_partials, int32_t n, const sk_cond* cond);
+
+/* Synchronise the run's stream and read its loop status: completed
+ * iterations, the last combined value (cross-rank if sk_run_combine is used),
+ * whether the loop stopped and whether the cap was hit. */
+int sk_run_status(sk_run* run, int64_t* iterations, double* value, int32_t* stopped,
+                  int32_t* exhausted);
+
 /* Sum of CUDA-event durations of all timed sweep launches (SK_FLAG_TIMING). */
 int sk_run_kernel_time(sk_run* run, double* total_ms, int64_t* launches);
 

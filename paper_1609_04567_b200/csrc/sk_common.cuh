@@ -28,9 +28,11 @@ struct Status {
   int exhausted;        // cap hit without cond
   int cond_true;        // the device condition said stop
   int pad;
-  double value;         // combined reduce value of iteration `iter`
+  double value;         // combined reduce value of iteration `iter` (this run's partitions)
   unsigned int ticket;  // last-CTA-done counter
   unsigned int work;    // dynamic work-chunk counter
+  double gvalue;        // value combined across ranks (sk_run_combine), multi-GPU runs
+  long long gdecided;   // iterations the cross-rank combine has evaluated
 };
 
 constexpr int kMaxParts = 64;

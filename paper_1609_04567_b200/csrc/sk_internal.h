@@ -73,6 +73,7 @@ struct sk_run {
   double* d_ring = nullptr;  // device alias of h_ring
   long long launched = 0;
   long long total_launches = 0;
+  bool combined = false;  // cross-rank combine in use
   cudaEvent_t ev_done[sk::kRing] = {};
 
   // optional per-sweep timing

@@ -120,6 +120,28 @@ static int launch_timed(sk_run* r, const LoopCtl& L) {
   return SK_OK;
 }
 
+// Cross-rank combine: one thread folds the gathered per-rank partials in
+// rank order from the identity and decides the iteration.
+__global__ void combine_kernel(Status* st, const double* parts, int n, int reduce,
+                               double identity, CondDev cond, volatile double* ring) {
+  const long long it = st->iter;
+  if (st->stop || it == 0 || st->gdecided >= it) return;  // no new iteration to decide
+  double acc = identity;
+  for (int i = 0; i < n; ++i) {
+    const double v = parts[i];
+    if (reduce == SK_REDUCE_SUM) acc = acc + v;
+    else acc = (v < acc) ? acc : v;
+  }
+  const int c = eval_cond(cond, acc, it);
+  const int capped = it >= cond.max_it;
+  st->gvalue = acc;
+  st->gdecided = it;
+  st->cond_true = c;
+  st->exhausted = !c && capped;
+  st->stop = c || capped;
+  if (ring) ring[it % kRing] = acc;
+}
+
 }  // namespace sk
 
 using namespace sk;
@@ -364,6 +386,39 @@ int sk_run_kernel_time(sk_run* r, double* total_ms, int64_t* launches) {
   }
   *total_ms = tot;
   *launches = n;
+  return SK_OK;
+}
+
+int sk_run_combine(sk_run* r, const double* d_partials, int32_t n, const sk_cond* c) {
+  if (!r || !d_partials || n < 1 || !c) {
+    set_error("sk_run_combine: bad argument");
+    return SK_ERR_ARG;
+  }
+  CondDev cd;
+  cd.kind = c->kind;
+  cd.a = c->a;
+  cd.n = c->n;
+  cd.max_it = c->max_iterations;
+  combine_kernel<<<1, 1, 0, r->stream>>>(r->d_status, d_partials, n, r->plan.reduce_op,
+                                         r->plan.identity, cd, r->d_ring);
+  SK_CUDA(cudaGetLastError());
+  r->combined = true;
+  return SK_OK;
+}
+
+int sk_run_status(sk_run* r, int64_t* iterations, double* value, int32_t* stopped,
+                  int32_t* exhausted) {
+  if (!r) {
+    set_error("sk_run_status: null run");
+    return SK_ERR_ARG;
+  }
+  Status st;
+  SK_CUDA(cudaMemcpyAsync(&st, r->d_status, sizeof(Status), cudaMemcpyDeviceToHost, r->stream));
+  SK_CUDA(cudaStreamSynchronize(r->stream));
+  if (iterations) *iterations = st.iter;
+  if (value) *value = r->combined ? st.gvalue : st.value;
+  if (stopped) *stopped = st.stop;
+  if (exhausted) *exhausted = st.exhausted;
   return SK_OK;
 }
 

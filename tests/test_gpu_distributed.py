@@ -1,0 +1,75 @@
+"""The multi-GPU rank-block engine on one B200: two ranks (processes) share
+cuda:0 over gloo (halo rows and partials staged through the host -- NCCL
+refuses two ranks per GPU), each running the native DeviceBlock (fused sweep
+with real halo rows + device-side rank-ordered combine).  The gathered grid
+must equal the single-GPU solve of the same global grid bit for bit, with the
+same iteration count and final MAX value."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _worker(rank, world, port, n, m, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1609_04567_b200.distributed import DeviceBlock, make_cond, run_block_loop
+        from paper_1609_04567_b200.partition import _split_ranges
+
+        torch.cuda.set_device(0)
+        rhs = np.random.default_rng(5).random((n, m)).astype(np.float32)
+        lo, hi = _split_ranges(n, world)[rank]
+        u0 = torch.zeros((hi - lo, m), dtype=torch.float32, device="cuda")
+        f = torch.from_numpy(rhs[lo:hi]).cuda()
+        consts = (4.0, 16.0, 40.5, 1.0 - 0.8, 0.8)  # alpha .5, dx .5, dy .25, relax .8
+        blk = DeviceBlock(u0, f, consts, rank=rank, world=world)
+        res = run_block_loop(blk, make_cond("lt", 1e-4), batch=3)
+        out = res.out.contiguous().cpu()
+        blk.close()
+        parts = [torch.zeros((b - a, m), dtype=torch.float32) for a, b in _split_ranges(n, world)]
+        for r in range(world):
+            dist.broadcast(out if r == rank else parts[r], src=r)
+        parts[rank] = out
+        if rank == 0:
+            q.put((res.iterations, res.final_reduce, torch.cat(parts).numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def _port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("world,n", [(2, 200), (3, 131)])
+def test_two_ranks_one_gpu_equal_single_gpu(world, n):
+    import paper_1609_04567_b200 as sk
+    from paper_1609_04567_b200.apps import HelmholtzConfig, helmholtz_kernel
+
+    m = 160
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    ps = [ctx.Process(target=_worker, args=(r, world, port, n, m, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    it, val, grid = q.get(timeout=300)
+    for p in ps:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    rhs = np.random.default_rng(5).random((n, m)).astype(np.float32)
+    cfg = HelmholtzConfig(n, m, alpha=0.5, dx=0.5, dy=0.25, relax=0.8)
+    out, rep = sk.parallel_loop("1:1", 1, 1, helmholtz_kernel(cfg), sk.max_combinator(0.0),
+                                sk.Condition.below(1e-4), sk.Grid(rhs.shape, np.zeros_like(rhs)),
+                                env=sk.Grid(rhs.shape, rhs), delta=sk.abs_change())
+    assert it == rep.iterations and val == rep.final_reduce
+    assert np.array_equal(grid.view(np.uint32), out.to_array().view(np.uint32))
