@@ -3,6 +3,7 @@
 //
 // Maps the reference's Executor protocol (loop.py:124-137) and _drive
 // (loop.py:198-224) onto device state.  See include/stencilkit_b200.h.
+#include <cstdlib>
 #include <mutex>
 #include <string>
 
@@ -272,7 +273,10 @@ int sk_run_loop(sk_run* r, const sk_cond* c, int64_t* iterations, double* final_
     return SK_ERR_STATE;
   }
   int rc = SK_OK;
-  bool use_graph = !r->timing;
+  // SK_NO_GRAPH=1 forces plain launches (profilers cannot see kernels inside
+  // conditional graph nodes)
+  const char* ng = getenv("SK_NO_GRAPH");
+  bool use_graph = !r->timing && !(ng && ng[0] == '1');
   if (use_graph) {
     // One graph: conditional WHILE node whose body is one sweep; the sweep's
     // finalizing CTA clears the condition when the loop is over.

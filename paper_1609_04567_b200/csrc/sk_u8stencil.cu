@@ -54,12 +54,27 @@ struct Row8 {
   int x[10];  // x[0] = pixel col-1, x[1..8] = cols col..col+7, x[9] = col+8
 };
 
+struct RawRow {  // a row as loaded, before neighbour exchange
+  uint2 w;
+  int xl, xr;
+};
+
+__device__ __forceinline__ unsigned pack4(int a, int b, int c, int d) {
+  const unsigned ab = __byte_perm((unsigned)a, (unsigned)b, 0x0040u);
+  const unsigned cd = __byte_perm((unsigned)c, (unsigned)d, 0x0040u);
+  return __byte_perm(ab, cd, 0x5410u);
+}
+
+// Warp-granular work: a chunk is one warp's 256-pixel-wide strip of rows, so
+// no block barrier is ever needed inside the sweep; warps pull chunk ids from
+// the run's atomic counter.  Rows are prefetched U at a time (memory-level
+// parallelism), then turned into features and outputs.
 template <int OP, int BLOCK, int REDUCE, bool BATCH>
 __global__ void __launch_bounds__(BLOCK) u8_sweep(const __grid_constant__ U8Args a) {
   constexpr int VEC = 8;
+  constexpr int U = 4;
   constexpr unsigned FULL = 0xffffffffu;
   __shared__ double sh[BLOCK / 32];
-  __shared__ int s_chunk;
   const Sweep2D& g = a.g;
   long long it = 1;
   if (!BATCH) {
@@ -70,7 +85,11 @@ __global__ void __launch_bounds__(BLOCK) u8_sweep(const __grid_constant__ U8Args
   const int cols = g.cols, rows = g.rows;
   const int total = BATCH ? a.frames * a.chunks_per_frame : a.L.part_chunk[a.L.nparts];
 
-  for (int c = next_chunk(a.L, &s_chunk); c < total; c = next_chunk(a.L, &s_chunk)) {
+  for (;;) {
+    int c = 0;
+    if (lane == 0) c = (int)atomicAdd(&a.L.st->work, 1u);
+    c = __shfl_sync(FULL, c, 0);
+    if (c >= total) break;
     int frame = 0, cb, r0, r1, cc = c;
     const unsigned char* front;
     unsigned char* back;
@@ -89,49 +108,51 @@ __global__ void __launch_bounds__(BLOCK) u8_sweep(const __grid_constant__ U8Args
       op = g.pitch;
     }
     chunk_geom(a.L, g, cc, &cb, &r0, &r1);
-    const int col = cb * (BLOCK * VEC) + (int)threadIdx.x * VEC;
+    const int col = cb * (32 * VEC) + lane * VEC;
     const int nvalid = cols - col;
     const bool active = nvalid > 0;
     const bool has_l = lane == 0 && col > 0 && active;
     const bool has_r = lane == 31 && nvalid > VEC;
-    // this thread touches the left/right image border
     const bool edge_col = active && (col == 0 || nvalid <= VEC);
 
-    auto load_row = [&](int r, Row8& R) {
-      uint2 w = make_uint2(0u, 0u);
-      const bool in = active && r >= 0 && r < rows;
-      const unsigned char* p = front + (long long)r * fp + col;
-      if (in) w = __ldg(reinterpret_cast<const uint2*>(p));
-      int xl = (in && has_l) ? (int)__ldg(p - 1) : 0;
-      int xr = (in && has_r) ? (int)__ldg(p + VEC) : 0;
-      const unsigned lo_prev = __shfl_up_sync(FULL, w.y, 1);
-      const unsigned hi_next = __shfl_down_sync(FULL, w.x, 1);
-      if (lane != 0) xl = byte_of(lo_prev, 3);
-      if (lane != 31) xr = byte_of(hi_next, 0);
+    auto fetch = [&](int r) -> RawRow {
+      RawRow R;
+      R.w = make_uint2(0u, 0u);
+      R.xl = R.xr = 0;
+      if (active && r >= 0 && r < rows) {
+        const unsigned char* p = front + (long long)r * fp + col;
+        R.w = __ldg(reinterpret_cast<const uint2*>(p));
+        if (has_l) R.xl = __ldg(p - 1);
+        if (has_r) R.xr = __ldg(p + VEC);
+      }
+      return R;
+    };
+    auto expand = [&](const RawRow& R, Row8& X) {
+      const unsigned lo_prev = __shfl_up_sync(FULL, R.w.y, 1);
+      const unsigned hi_next = __shfl_down_sync(FULL, R.w.x, 1);
+      X.x[0] = lane != 0 ? byte_of(lo_prev, 3) : R.xl;
+      X.x[9] = lane != 31 ? byte_of(hi_next, 0) : R.xr;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        R.x[1 + k] = byte_of(w.x, k);
-        R.x[5 + k] = byte_of(w.y, k);
+        X.x[1 + k] = byte_of(R.w.x, k);
+        X.x[5 + k] = byte_of(R.w.y, k);
       }
-      R.x[0] = xl;
-      R.x[9] = xr;
-      // off-image columns are 0 here; Life wants exactly that (dead),
-      // Sobel's border pixels are recomputed by the generic path
+      // off-image columns read 0 (Life: dead); Sobel border pixels are
+      // recomputed by the generic path
       if (nvalid < VEC + 1) {
 #pragma unroll
         for (int k = 1; k <= VEC + 1; ++k)
-          if (k > nvalid) R.x[k] = 0;
+          if (k > nvalid) X.x[k] = 0;
       }
-      if (col == 0) R.x[0] = 0;
+      if (col == 0) X.x[0] = 0;
     };
 
-    double acc = REDUCE == SK_REDUCE_MAX ? -INFINITY : 0.0;
-    long long iacc = 0;
+    int acc_i = 0;                                // SUM (fits: 255*8*256)
+    int acc_m = REDUCE == SK_REDUCE_MAX ? -1 : 0;  // MAX
     Row8 up, cen, dn;
-    load_row(r0 - 1, up);
-    load_row(r0, cen);
-    // horizontal features of rows r-1 and r
-    int hA[VEC], hB[VEC], hA2[VEC], hB2[VEC];  // Sobel: D, S ; Life: T in hA
+    expand(fetch(r0 - 1), up);
+    expand(fetch(r0), cen);
+    int hA[VEC], hB[VEC], hA2[VEC], hB2[VEC];  // Sobel: D, S of rows r-1, r; Life: T in hA
 #pragma unroll
     for (int k = 0; k < VEC; ++k) {
       if (OP == U8_SOBEL) {
@@ -145,71 +166,83 @@ __global__ void __launch_bounds__(BLOCK) u8_sweep(const __grid_constant__ U8Args
         hB[k] = hB2[k] = 0;
       }
     }
-    for (int r = r0; r < r1; ++r) {
-      load_row(r + 1, dn);
-      int out[VEC];
+    for (int r = r0; r < r1; r += U) {
+      RawRow pre[U];
 #pragma unroll
-      for (int k = 0; k < VEC; ++k) {
-        if (OP == U8_SOBEL) {
-          const int d3 = dn.x[k + 2] - dn.x[k];
-          const int s3 = dn.x[k] + 2 * dn.x[k + 1] + dn.x[k + 2];
-          const int gx = hA[k] + 2 * hA2[k] + d3;
-          const int gy = s3 - hB[k];
-          out[k] = sobel_mag(gx, gy);
-          hA[k] = hA2[k];
-          hB[k] = hB2[k];
-          hA2[k] = d3;
-          hB2[k] = s3;
-        } else {
-          const int t3 = dn.x[k] + dn.x[k + 1] + dn.x[k + 2];
-          const int x = cen.x[k + 1];
-          const int n = hA[k] + hA2[k] + t3 - x;
-          out[k] = (n == 3 || (x == 1 && n == 2)) ? 1 : 0;
-          hA[k] = hA2[k];
-          hA2[k] = t3;
+      for (int u = 0; u < U; ++u)
+        if (r + u < r1) pre[u] = fetch(r + u + 1);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int rr = r + u;
+        if (rr < r1) {
+          expand(pre[u], dn);
+          int out[VEC];
+#pragma unroll
+          for (int k = 0; k < VEC; ++k) {
+            if (OP == U8_SOBEL) {
+              const int d3 = dn.x[k + 2] - dn.x[k];
+              const int s3 = dn.x[k] + 2 * dn.x[k + 1] + dn.x[k + 2];
+              out[k] = sobel_mag(hA[k] + 2 * hA2[k] + d3, s3 - hB[k]);
+              hA[k] = hA2[k];
+              hB[k] = hB2[k];
+              hA2[k] = d3;
+              hB2[k] = s3;
+            } else {
+              const int t3 = dn.x[k] + dn.x[k + 1] + dn.x[k + 2];
+              const int x = cen.x[k + 1];
+              const int n = hA[k] + hA2[k] + t3 - x;
+              out[k] = (n == 3 || (x == 1 && n == 2)) ? 1 : 0;
+              hA[k] = hA2[k];
+              hA2[k] = t3;
+            }
+          }
+          if (OP == U8_SOBEL && (rr == 0 || rr == rows - 1 || edge_col)) {
+            // generic 9-tap: off-image reads are replaced by the centre pixel
+            const bool uok = rr > 0, dok = rr < rows - 1;
+#pragma unroll
+            for (int k = 0; k < VEC; ++k) {
+              const int cc0 = col + k;
+              const bool lok = cc0 > 0, rok = cc0 + 1 < cols;
+              const int ctr = cen.x[k + 1];
+              const int nw = (uok && lok) ? up.x[k] : ctr, n = uok ? up.x[k + 1] : ctr;
+              const int ne = (uok && rok) ? up.x[k + 2] : ctr;
+              const int w = lok ? cen.x[k] : ctr, e = rok ? cen.x[k + 2] : ctr;
+              const int sw = (dok && lok) ? dn.x[k] : ctr, s = dok ? dn.x[k + 1] : ctr;
+              const int se = (dok && rok) ? dn.x[k + 2] : ctr;
+              out[k] = sobel_mag(-nw + ne - 2 * w + 2 * e - sw + se,
+                                 -nw - 2 * n - ne + sw + 2 * s + se);
+            }
+          }
+          if (nvalid < VEC) {
+#pragma unroll
+            for (int k = 0; k < VEC; ++k)
+              if (k >= nvalid) out[k] = 0;  // row padding stays zero; not reduced
+          }
+#pragma unroll
+          for (int k = 0; k < VEC; ++k) {
+            if (REDUCE == SK_REDUCE_MAX) acc_m = k < nvalid ? max(acc_m, out[k]) : acc_m;
+            else acc_i += out[k];
+          }
+          if (active)
+            *reinterpret_cast<uint2*>(back + (long long)rr * op + col) = make_uint2(
+                pack4(out[0], out[1], out[2], out[3]), pack4(out[4], out[5], out[6], out[7]));
+          up = cen;
+          cen = dn;
         }
       }
-      if (OP == U8_SOBEL && (r == 0 || r == rows - 1 || edge_col)) {
-        // generic 9-tap with off-image reads replaced by the centre pixel
-        const bool uok = r > 0, dok = r < rows - 1;
-#pragma unroll
-        for (int k = 0; k < VEC; ++k) {
-          const int cc0 = col + k;
-          const bool lok = cc0 > 0, rok = cc0 + 1 < cols;
-          const int ctr = cen.x[k + 1];
-          const int nw = (uok && lok) ? up.x[k] : ctr, n = uok ? up.x[k + 1] : ctr;
-          const int ne = (uok && rok) ? up.x[k + 2] : ctr;
-          const int w = lok ? cen.x[k] : ctr, e = rok ? cen.x[k + 2] : ctr;
-          const int sw = (dok && lok) ? dn.x[k] : ctr, s = dok ? dn.x[k + 1] : ctr;
-          const int se = (dok && rok) ? dn.x[k + 2] : ctr;
-          const int gx = -nw + ne - 2 * w + 2 * e - sw + se;
-          const int gy = -nw - 2 * n - ne + sw + 2 * s + se;
-          out[k] = sobel_mag(gx, gy);
-        }
-      }
-      unsigned lo = 0, hi = 0;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const bool in0 = k < nvalid, in1 = k + 4 < nvalid;
-        const int v0 = in0 ? out[k] : 0, v1 = in1 ? out[k + 4] : 0;
-        lo |= (unsigned)v0 << (8 * k);
-        hi |= (unsigned)v1 << (8 * k);
-        if (REDUCE == SK_REDUCE_MAX) {
-          if (in0) acc = fmax(acc, (double)v0);
-          if (in1) acc = fmax(acc, (double)v1);
-        } else {
-          iacc += v0 + v1;
-        }
-      }
-      if (active) *reinterpret_cast<uint2*>(back + (long long)r * op + col) = make_uint2(lo, hi);
-      up = cen;
-      cen = dn;
     }
-    if (REDUCE == SK_REDUCE_SUM) acc = (double)iacc;
-    const double v = block_reduce<BLOCK>(REDUCE, acc, sh);
-    if (threadIdx.x == 0) {
+    double v;
+    if (REDUCE == SK_REDUCE_MAX) {
+      int m = acc_m;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(FULL, m, o));
+      v = m < 0 ? -INFINITY : (double)m;
+    } else {
+      v = (double)__reduce_add_sync(FULL, (unsigned)acc_i);
+    }
+    if (lane == 0) {
       if (BATCH) atomicAdd(reinterpret_cast<unsigned long long*>(&a.sums[frame]),
-                           (unsigned long long)(long long)v);
+                           (unsigned long long)v);
       else a.L.partials[c] = v;
     }
   }
@@ -242,10 +275,11 @@ int geometry(int device, U8Fn fn, long long rows, long long cols, int nparts, co
   int per_sm = 0;
   SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kBlock, 0));
   const long long slots = (long long)device_sms(device) * (per_sm > 0 ? per_sm : 1);
-  *colblocks = (int)((cols + kBlock * kVec - 1) / (kBlock * kVec));
-  const long long want = slots * 4;
+  *colblocks = (int)((cols + 32 * kVec - 1) / (32 * kVec));  // one warp per chunk
+  const long long want = slots * (kBlock / 32) * 4;
   long long ch = (rows * (long long)*colblocks * frames + want - 1) / want;
   ch = ch < 8 ? 8 : (ch > 256 ? 256 : ch);
+  ch = (ch + 3) / 4 * 4;  // whole prefetch groups
   *chunk_rows = (int)ch;
   int n = 0;
   part_chunk[0] = 0;

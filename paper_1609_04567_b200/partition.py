@@ -209,6 +209,30 @@ def _u8_from(grid: Grid, what: str, lo: int, hi: int, dev):
     return t
 
 
+def _our_grid(g):
+    if g is None or isinstance(g, Grid):
+        return g
+    if hasattr(g, "dims") and hasattr(g, "data"):  # the reference's list-backed Grid
+        return Grid(g.dims, g.data)
+    if isinstance(g, tuple):
+        return tuple(_our_grid(x) for x in g)
+    return g
+
+
+def _adapt(plan, grid):
+    """Accept the reference package's own LoopPlan/Grid objects (when this
+    executor is passed to stencilkit's loop_stencil_reduce*): its _as_plan
+    wraps our ElementalFn as the `point` of its own ElementalFn."""
+    fn = plan.fn
+    if getattr(fn, "device", None) is None and getattr(getattr(fn, "point", None), "device", None):
+        fn = fn.point
+    env = _our_grid(plan.env)
+    if fn is not plan.fn or env is not plan.env or not isinstance(plan, LoopPlan):
+        plan = LoopPlan(fn=fn, k=plan.k, op=plan.op, env=env, indexed=plan.indexed,
+                        delta=plan.delta)
+    return plan, _our_grid(grid)
+
+
 class DeviceExecutor(Executor):
     """Executor over the native engine: `partitions` row partitions on one GPU."""
 
@@ -229,6 +253,7 @@ class DeviceExecutor(Executor):
     def begin(self, plan: LoopPlan, grid: Grid) -> _DevRun:
         lib = N.require_cuda()
         torch = _torch()
+        plan, grid = _adapt(plan, grid)
         _check_env(plan.env, grid.dims)
         dk = plan.fn.device if hasattr(plan.fn, "device") else None
         if dk is None:

@@ -131,7 +131,7 @@ def _probe(fn, expect) -> bool:
 
 def combinator_kind(op: Combinator) -> str:
     """'sum' or 'max' for the device reduce, else DeviceUnsupported."""
-    if op.kind is not None:
+    if getattr(op, "kind", None) is not None:
         return op.kind
     if _probe(op.fn, lambda a, b: a + b):
         return "sum"
@@ -144,7 +144,7 @@ def delta_kind(d: Optional[Delta]) -> str:
     """'none', 'abs' or 'square' for the device delta, else DeviceUnsupported."""
     if d is None:
         return "none"
-    if d.kind is not None:
+    if getattr(d, "kind", None) is not None:
         return d.kind
     if _probe(d.fn, lambda n, o: abs(n - o)):
         return "abs"

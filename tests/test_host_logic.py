@@ -180,3 +180,21 @@ def test_product_path_has_no_cpu_fallback():
     with pytest.raises(_native.DeviceUnavailable):
         sk.loop_stencil_reduce(1, lambda nb, env: nb.center, sk.sum_combinator(0),
                                sk.stop_after(1), g)
+
+
+def test_adapts_reference_plan_objects():
+    """The executor accepts the reference's own LoopPlan/Grid shapes (plugin route)."""
+    from types import SimpleNamespace
+
+    from paper_1609_04567_b200.partition import _adapt
+
+    ours = helmholtz_kernel(HelmholtzConfig(4, 4))
+    ref_fn = SimpleNamespace(point=ours, k=1, device=None)  # stencilkit wraps bare callables
+    ref_grid = SimpleNamespace(dims=(4, 4), data=[0.0] * 16)
+    ref_env = SimpleNamespace(dims=(4, 4), data=[1.0] * 16)
+    ref_plan = SimpleNamespace(fn=ref_fn, k=1, op=SimpleNamespace(fn=lambda a, b: a + b,
+                                                                   identity=0.0),
+                               env=ref_env, indexed=False, delta=None)
+    plan, grid = _adapt(ref_plan, ref_grid)
+    assert plan.fn is ours and isinstance(grid, sk.Grid) and isinstance(plan.env, sk.Grid)
+    assert combinator_kind(plan.op) == "sum"
