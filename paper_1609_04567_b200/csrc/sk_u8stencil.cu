@@ -249,6 +249,250 @@ __global__ void __launch_bounds__(BLOCK) u8_sweep(const __grid_constant__ U8Args
   if (!BATCH) loop_finalize<BLOCK>(a.L, it, sh);
 }
 
+// ---------------------------------------------------------------- Sobel, SWAR
+// Packed form of the separable Sobel: two pixels per 32-bit register in
+// 16-bit lanes, biased so no lane ever borrows from its neighbour.
+//   P_i = (x_{2i}, x_{2i+1}),  F_i = (x_{2i-1}, x_{2i})  (funnel shifts)
+//   L_i = F_i, R_i = F_{i+1}
+//   S_i = L_i + 2 P_i + R_i                 in [0, 1020]
+//   D_i = R_i - L_i + 256                   in [1, 511]
+//   gx' = D(r-1) + 2 D(r) + D(r+1)          = gx + 1024 in [4, 2044]
+//   gy' = S(r+1) - S(r-1) + 1024            = gy + 1024 in [4, 2044]
+// Each lane becomes an exact fp32 (2^23 + v, magic), n = gx^2 + gy^2 is exact
+// in fp32 (< 2^24), and cvt.rni.sat.u8 rounds half-to-even and clips to 255
+// in one instruction -- the reference's min(255, rint(sqrt(n))).
+__device__ __forceinline__ unsigned lane_lo(unsigned p) { return __byte_perm(p, 0x4B000000u, 0x7610u); }
+__device__ __forceinline__ unsigned lane_hi(unsigned p) { return __byte_perm(p, 0x4B000000u, 0x7632u); }
+
+__device__ __forceinline__ unsigned sobel_byte(unsigned gxm, unsigned gym) {
+  const float gx = __fsub_rn(__uint_as_float(gxm), 8389632.0f);  // (2^23 + gx') - (2^23 + 1024)
+  const float gy = __fsub_rn(__uint_as_float(gym), 8389632.0f);
+  const float n = __fmaf_rn(gy, gy, __fmul_rn(gx, gx));  // exact: every term < 2^24
+  float s;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(s) : "f"(n));
+  unsigned b;
+  asm("cvt.rni.sat.u8.f32 %0, %1;" : "=r"(b) : "f"(s));
+  return b;
+}
+
+// One border pixel with the reference's rule (off-image reads = centre),
+// reading the three rows straight from memory.  Out of line: border work is
+// rare, and inlining it would bloat the hot loop's instruction footprint.
+__device__ __noinline__ unsigned sobel_border_px(const unsigned char* front, long long fp, int r,
+                                                 int c, int rows, int cols) {
+  const int ctr = front[(long long)r * fp + c];
+  auto at = [&](int i, int j) -> int {
+    return (i < 0 || i >= rows || j < 0 || j >= cols) ? ctr : (int)front[(long long)i * fp + j];
+  };
+  const int nw = at(r - 1, c - 1), n = at(r - 1, c), ne = at(r - 1, c + 1);
+  const int w = at(r, c - 1), e = at(r, c + 1);
+  const int sw = at(r + 1, c - 1), so = at(r + 1, c), se = at(r + 1, c + 1);
+  return (unsigned)sobel_mag(-nw + ne - 2 * w + 2 * e - sw + se, -nw - 2 * n - ne + sw + 2 * so + se);
+}
+
+template <int BLOCK, int REDUCE, bool BATCH>
+__global__ void __launch_bounds__(BLOCK) sobel_sweep(const __grid_constant__ U8Args a) {
+  constexpr int VEC = 8;
+  constexpr int U = 6;  // multiple of the 3-row feature rotation: no register moves
+  constexpr unsigned FULL = 0xffffffffu;
+  __shared__ double sh[BLOCK / 32];
+  const Sweep2D& g = a.g;
+  long long it = 1;
+  if (!BATCH) {
+    it = loop_enter(a.L);
+    if (it == 0) return;
+  }
+  const int lane = threadIdx.x & 31;
+  const int cols = g.cols, rows = g.rows;
+  const int total = BATCH ? a.frames * a.chunks_per_frame : a.L.part_chunk[a.L.nparts];
+
+  for (;;) {
+    int c = 0;
+    if (lane == 0) c = (int)atomicAdd(&a.L.st->work, 1u);
+    c = __shfl_sync(FULL, c, 0);
+    if (c >= total) break;
+    int frame = 0, cb, r0, r1, cc = c;
+    const unsigned char* front;
+    unsigned char* back;
+    long long fp, op;
+    if (BATCH) {
+      frame = c / a.chunks_per_frame;
+      cc = c - frame * a.chunks_per_frame;
+      front = a.bin + frame * a.in_stride;
+      back = a.bout + frame * a.out_stride;
+      fp = g.src_pitch;
+      op = g.pitch;
+    } else {
+      front = static_cast<const unsigned char*>(it == 1 ? g.src : g.buf[(it - 1) & 1]);
+      fp = it == 1 ? g.src_pitch : g.pitch;
+      back = static_cast<unsigned char*>(g.buf[it & 1]);
+      op = g.pitch;
+    }
+    chunk_geom(a.L, g, cc, &cb, &r0, &r1);
+    const int col = cb * (32 * VEC) + lane * VEC;
+    const int nvalid = cols - col;
+    const bool active = nvalid > 0;
+    const int lsh = (lane == 0 && col > 0 && active) ? -1 : 0;        // edge-lane scalar loads
+    const int rsh = (lane == 31 && nvalid > VEC) ? VEC : 0;
+    const bool ledge = lane == 0, redge = lane == 31;
+
+    // Row r (may be -1 or rows: zeros; never read past the image).
+    auto fetch = [&](int r, uint2& w, unsigned& xl, unsigned& xr) {
+      w = make_uint2(0u, 0u);
+      xl = xr = 0u;
+      if (active && r >= 0 && r < rows) {
+        const unsigned char* p = front + (long long)r * fp + col;
+        w = __ldg(reinterpret_cast<const uint2*>(p));
+        xl = __ldg(p + lsh);  // lanes without a left neighbour load their own byte (unused)
+        xr = __ldg(p + rsh);
+      }
+    };
+    auto features = [&](uint2 w, unsigned exl, unsigned exr, unsigned* S, unsigned* D) {
+      const unsigned lo_prev = __shfl_up_sync(FULL, w.y, 1);
+      const unsigned hi_next = __shfl_down_sync(FULL, w.x, 1);
+      const unsigned xl = ledge ? exl : (lo_prev >> 24);
+      const unsigned xr = redge ? exr : (hi_next & 0xffu);
+      unsigned P[4], F[5];
+      P[0] = __byte_perm(w.x, 0u, 0x4140u);
+      P[1] = __byte_perm(w.x, 0u, 0x4342u);
+      P[2] = __byte_perm(w.y, 0u, 0x4140u);
+      P[3] = __byte_perm(w.y, 0u, 0x4342u);
+      F[0] = __funnelshift_l(xl << 16, P[0], 16);
+      F[1] = __funnelshift_l(P[0], P[1], 16);
+      F[2] = __funnelshift_l(P[1], P[2], 16);
+      F[3] = __funnelshift_l(P[2], P[3], 16);
+      F[4] = __funnelshift_l(P[3], xr, 16);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        S[i] = F[i] + F[i + 1] + (P[i] << 1);
+        D[i] = F[i + 1] - F[i] + 0x01000100u;
+      }
+    };
+    auto emit = [&](const unsigned* Sm, const unsigned* Dm, const unsigned* Dc, const unsigned* Sp,
+                    const unsigned* Dp, unsigned char* po, unsigned& acc, int& accm) {
+      unsigned ob[8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const unsigned gxp = Dm[i] + (Dc[i] << 1) + Dp[i];
+        const unsigned gyp = Sp[i] - Sm[i] + 0x04000400u;
+        ob[2 * i] = sobel_byte(lane_lo(gxp), lane_lo(gyp));
+        ob[2 * i + 1] = sobel_byte(lane_hi(gxp), lane_hi(gyp));
+      }
+      const unsigned lo = pack4((int)ob[0], (int)ob[1], (int)ob[2], (int)ob[3]);
+      const unsigned hi = pack4((int)ob[4], (int)ob[5], (int)ob[6], (int)ob[7]);
+      if (REDUCE == SK_REDUCE_MAX) {
+        const unsigned m = __vmaxu4(lo, hi);
+        const unsigned m2 = __vmaxu4(m, m >> 16);
+        accm = max(accm, (int)max(m2 & 0xffu, (m2 >> 8) & 0xffu));
+      } else {
+        acc = __dp4a(lo, 0x01010101u, acc);
+        acc = __dp4a(hi, 0x01010101u, acc);
+      }
+      if (active) *reinterpret_cast<uint2*>(po) = make_uint2(lo, hi);
+    };
+
+    unsigned acc = 0;
+    int accm = -1;
+    unsigned S0[4], D0[4], S1[4], D1[4], S2[4], D2[4];
+    {
+      uint2 w;
+      unsigned xl, xr;
+      fetch(r0 - 1, w, xl, xr);
+      features(w, xl, xr, S0, D0);
+      fetch(r0, w, xl, xr);
+      features(w, xl, xr, S1, D1);
+    }
+    unsigned char* po = back + (long long)r0 * op + col;
+    int r = r0;
+    for (; r + U <= r1; r += U) {  // full groups: no per-row checks
+      uint2 w[U];
+      unsigned xl[U], xr[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) fetch(r + u + 1, w[u], xl[u], xr[u]);
+      // rows r..r+5 rotate the feature sets S0/S1/S2 by renaming
+      features(w[0], xl[0], xr[0], S2, D2);
+      emit(S0, D0, D1, S2, D2, po, acc, accm);
+      po += op;
+      features(w[1], xl[1], xr[1], S0, D0);
+      emit(S1, D1, D2, S0, D0, po, acc, accm);
+      po += op;
+      features(w[2], xl[2], xr[2], S1, D1);
+      emit(S2, D2, D0, S1, D1, po, acc, accm);
+      po += op;
+      features(w[3], xl[3], xr[3], S2, D2);
+      emit(S0, D0, D1, S2, D2, po, acc, accm);
+      po += op;
+      features(w[4], xl[4], xr[4], S0, D0);
+      emit(S1, D1, D2, S0, D0, po, acc, accm);
+      po += op;
+      features(w[5], xl[5], xr[5], S1, D1);
+      emit(S2, D2, D0, S1, D1, po, acc, accm);
+      po += op;
+    }
+#pragma unroll 1
+    for (; r < r1; ++r) {  // tail rows
+      uint2 w;
+      unsigned xl, xr;
+      fetch(r + 1, w, xl, xr);
+      features(w, xl, xr, S2, D2);
+      emit(S0, D0, D1, S2, D2, po, acc, accm);
+      po += op;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        S0[i] = S1[i];
+        D0[i] = D1[i];
+        S1[i] = S2[i];
+        D1[i] = D2[i];
+      }
+    }
+    // Fix-up pass: border pixels (image rows 0 / rows-1, columns 0 / cols-1)
+    // follow the centre-substitution rule, and bytes past the image width are
+    // zero.  Each lane rewrites its own bytes, reading what it just stored.
+    const bool top = r0 == 0, bottom = r1 == rows;
+    const bool lcol = active && col == 0, rcol = active && nvalid <= VEC;
+    if (active && (top || bottom || lcol || rcol)) {
+      auto redo = [&](int rr, int k) {
+        unsigned char* q = back + (long long)rr * op + col + k;
+        const unsigned old = *q;
+        const unsigned nv = k < nvalid ? sobel_border_px(front, fp, rr, col + k, rows, cols) : 0u;
+        *q = (unsigned char)nv;
+        acc += nv - old;
+      };
+      for (int rr = r0; rr < r1; ++rr) {
+        if ((top && rr == 0) || (bottom && rr == rows - 1)) {
+          for (int k = 0; k < VEC; ++k) redo(rr, k);
+        } else {
+          if (lcol) redo(rr, 0);
+          if (rcol) {
+            for (int k = nvalid - 1; k < VEC; ++k) redo(rr, k);
+          }
+        }
+      }
+      if (REDUCE == SK_REDUCE_MAX) {  // rare: recompute this lane's max from what it stored
+        accm = -1;
+        for (int rr = r0; rr < r1; ++rr)
+          for (int k = 0; k < VEC && k < nvalid; ++k)
+            accm = max(accm, (int)back[(long long)rr * op + col + k]);
+      }
+    }
+    double v;
+    if (REDUCE == SK_REDUCE_MAX) {
+      int m = active ? accm : -1;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(FULL, m, o));
+      v = m < 0 ? -INFINITY : (double)m;
+    } else {
+      v = (double)__reduce_add_sync(FULL, active ? acc : 0u);
+    }
+    if (lane == 0) {
+      if (BATCH) atomicAdd(reinterpret_cast<unsigned long long*>(&a.sums[frame]),
+                           (unsigned long long)v);
+      else a.L.partials[c] = v;
+    }
+  }
+  if (!BATCH) loop_finalize<BLOCK>(a.L, it, sh);
+}
+
 // ---------------------------------------------------------------- host side
 
 namespace {
@@ -259,11 +503,11 @@ constexpr int kVec = 8;
 using U8Fn = void (*)(const U8Args);
 
 U8Fn pick(int op, int reduce, bool batch) {
-  if (batch) return op == U8_SOBEL ? u8_sweep<U8_SOBEL, kBlock, SK_REDUCE_SUM, true>
+  if (batch) return op == U8_SOBEL ? sobel_sweep<kBlock, SK_REDUCE_SUM, true>
                                    : u8_sweep<U8_LIFE, kBlock, SK_REDUCE_SUM, true>;
   if (op == U8_SOBEL)
-    return reduce == SK_REDUCE_MAX ? u8_sweep<U8_SOBEL, kBlock, SK_REDUCE_MAX, false>
-                                   : u8_sweep<U8_SOBEL, kBlock, SK_REDUCE_SUM, false>;
+    return reduce == SK_REDUCE_MAX ? sobel_sweep<kBlock, SK_REDUCE_MAX, false>
+                                   : sobel_sweep<kBlock, SK_REDUCE_SUM, false>;
   return reduce == SK_REDUCE_MAX ? u8_sweep<U8_LIFE, kBlock, SK_REDUCE_MAX, false>
                                  : u8_sweep<U8_LIFE, kBlock, SK_REDUCE_SUM, false>;
 }
@@ -279,7 +523,7 @@ int geometry(int device, U8Fn fn, long long rows, long long cols, int nparts, co
   const long long want = slots * (kBlock / 32) * 4;
   long long ch = (rows * (long long)*colblocks * frames + want - 1) / want;
   ch = ch < 8 ? 8 : (ch > 256 ? 256 : ch);
-  ch = (ch + 3) / 4 * 4;  // whole prefetch groups
+  ch = (ch + 11) / 12 * 12;  // whole prefetch groups (Life: 4 rows, Sobel: 6)
   *chunk_rows = (int)ch;
   int n = 0;
   part_chunk[0] = 0;

@@ -11,6 +11,7 @@ import numpy as np
 import pytest
 
 import paper_1609_04567_b200 as sk
+import paper_1609_04567_b200.apps
 from paper_1609_04567_b200.apps import (GolConfig, RestoreConfig, amf_detect, amf_frames,
                                         game_of_life, restore_regularize, sobel_filter,
                                         sobel_frames)
@@ -147,3 +148,31 @@ def test_video_pipeline_order_and_identity(golden):
         mask = amf_detect(f)
         ref, _ = restore_regularize(f, mask)
         assert o == ref
+
+
+def test_sobel_max_combinator_and_odd_shapes():
+    """MAX reduce and widths/heights that exercise partial vectors, border
+    fix-ups and tail rows of the SWAR kernel."""
+    from oracle import stencil_oracle as O
+
+    rng = np.random.default_rng(99)
+    for shape in ((3, 3), (7, 9), (13, 250), (61, 257), (258, 263), (2, 520)):
+        img = rng.integers(0, 256, shape)
+        ref = O.sobel(img)
+        out, rep = sk.parallel_loop("1:1", 1, 1, sk.apps.sobel_kernel, sk.max_combinator(-1),
+                                    sk.stop_after(1), sk.Grid.from_array(img))
+        assert np.array_equal(out.to_array().astype(np.uint8), ref), shape
+        assert rep.final_reduce == int(ref.max())
+        out2 = sobel_filter(sk.Grid.from_array(img))
+        assert np.array_equal(out2.to_array().astype(np.uint8), ref), shape
+
+
+def test_sobel_iterated_twice():
+    from oracle import stencil_oracle as O
+
+    img = np.random.default_rng(7).integers(0, 256, (40, 72))
+    out, rep = sk.parallel_loop("1:1", 1, 1, sk.apps.sobel_kernel, sk.sum_combinator(0),
+                                sk.stop_after(2), sk.Grid.from_array(img))
+    ref = O.sobel(O.sobel(img))
+    assert np.array_equal(out.to_array().astype(np.uint8), ref)
+    assert rep.final_reduce == int(ref.astype(np.int64).sum())
