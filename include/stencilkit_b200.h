@@ -108,7 +108,8 @@ int sk_abi_version(void);
  * d_buf0/1: the executor's two iteration buffers (PartitionSet.buffer_allocations,
  *           partition.py:160), layout (halo_top + rows + halo_bottom) x pitch.
  * pitch / src_pitch / env_pitch must be multiples of 16 bytes / sizeof(elem)
- * and the pointers 16-byte aligned (the Python layer stages otherwise). */
+ * (Helmholtz: also of 4 elements) and the pointers 16-byte aligned (the
+ * Python layer stages otherwise). */
 int sk_run_begin(const sk_plan* plan, const void* d_src, int64_t src_pitch,
                  const void* d_env, int64_t env_pitch, void* d_buf0, void* d_buf1,
                  int64_t pitch, void* stream, sk_run** out);

@@ -60,7 +60,8 @@ _lib = None
 
 
 def lib_path() -> str:
-    return _build.lib_path()
+    # SK_LIB_PATH: load an alternative build (kernel-variant experiments)
+    return os.environ.get("SK_LIB_PATH") or _build.lib_path()
 
 
 def load(build_if_missing: bool = True):
@@ -70,7 +71,7 @@ def load(build_if_missing: bool = True):
         if _lib is not None:
             return _lib
         path = lib_path()
-        if build_if_missing and _build.needs_build():
+        if build_if_missing and path == _build.lib_path() and _build.needs_build():
             try:
                 _build.build()
             except Exception as e:  # no toolkit here: only a prebuilt .so can work

@@ -6,7 +6,8 @@
 // _step_block (partition.py:302-316); the host combine partition.py:642-646.
 //
 // HBM-bound: 12 B/cell (fp32: read u 4 + read f 4 + write u' 4), 24 B/cell
-// fp64.  Each thread owns 16 contiguous bytes of a row (float4 / double2)
+// fp64.  Each thread owns 4 contiguous elements of a row (one float4 / two
+// double2 loads)
 // and marches down a chunk of rows keeping the up/centre/down rows in
 // registers, so every u row is read from DRAM once per chunk (+2 halo rows
 // per chunk); horizontal neighbours come from warp shuffles plus one scalar
@@ -23,6 +24,13 @@
 #include "sk_internal.h"
 #include "sk_sweep.cuh"
 
+#ifndef SK_F64_UNROLL
+#define SK_F64_UNROLL 1
+#endif
+#ifndef SK_F64_MINB
+#define SK_F64_MINB 8
+#endif
+
 namespace sk {
 
 template <typename T>
@@ -37,9 +45,9 @@ __device__ __forceinline__ float rcp_rn(float b) { return __frcp_rn(b); }
 __device__ __forceinline__ double rcp_rn(double b) { return __drcp_rn(b); }
 
 template <typename T, int BLOCK, int U, int DELTA, int REDUCE>
-__global__ void __launch_bounds__(BLOCK)
+__global__ void __launch_bounds__(BLOCK, (sizeof(T) == 8 ? SK_F64_MINB : 1))
     helmholtz_sweep(const __grid_constant__ HelmArgs<T> a) {
-  constexpr int VEC = 16 / sizeof(T);
+  constexpr int VEC = 4;
   constexpr unsigned FULL = 0xffffffffu;
   __shared__ double sh[BLOCK / 32];
   __shared__ int s_chunk;
@@ -76,27 +84,27 @@ __global__ void __launch_bounds__(BLOCK)
     const bool has_r = (lane == 31) && nvalid > VEC;
     const bool top_zero = !g.halo_top, bot_zero = !g.halo_bottom;
 
-    auto ldrow = [&](int r) -> V16<T> {
-      if (!active || (r < 0 && top_zero) || (r >= rows && bot_zero)) return zero16<T>();
-      return ldg16(front + (long long)r * fp + col);
+    auto ldrow = [&](int r) -> Vec4<T> {
+      if (!active || (r < 0 && top_zero) || (r >= rows && bot_zero)) return zero4<T>();
+      return ldg4(front + (long long)r * fp + col);
     };
 
     T accm = -INFINITY;  // MAX accumulator (exact in T)
     double accs = 0.0;   // SUM accumulator
-    V16<T> up = ldrow(r0 - 1);
-    V16<T> cen = ldrow(r0);
+    Vec4<T> up = ldrow(r0 - 1);
+    Vec4<T> cen = ldrow(r0);
     const T* pc = front + (long long)r0 * fp + col;  // centre row r
     const T* pe = env + (long long)r0 * g.env_pitch + col;
     T* po = back + (long long)r0 * g.pitch + col;
     for (int r = r0; r < r1; r += U) {
-      V16<T> dn[U], fv[U];
+      Vec4<T> dn[U], fv[U];
       T ls[U], rs[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int rr = r + u;
         if (rr < r1) {
           dn[u] = ldrow(rr + 1);
-          fv[u] = active ? ldg16(pe + u * g.env_pitch) : zero16<T>();
+          fv[u] = active ? ldg4(pe + u * g.env_pitch) : zero4<T>();
           ls[u] = has_l ? __ldg(pc + u * fp - 1) : T(0);
           rs[u] = has_r ? __ldg(pc + u * fp + VEC) : T(0);
         }
@@ -129,7 +137,7 @@ __global__ void __launch_bounds__(BLOCK)
 #pragma unroll
             for (int e = 0; e < VEC; ++e) q[e] = xdiv(num[e], b);
           }
-          V16<T> o;
+          Vec4<T> o;
           T dd[VEC];
 #pragma unroll
           for (int e = 0; e < VEC; ++e) {
@@ -154,11 +162,10 @@ __global__ void __launch_bounds__(BLOCK)
           }
           if (REDUCE == SK_REDUCE_SUM) {
             T s4;
-            if (VEC == 4) s4 = xadd(xadd(dd[0], dd[1]), xadd(dd[2], dd[VEC - 1]));
-            else s4 = xadd(dd[0], dd[VEC - 1]);
+            s4 = xadd(xadd(dd[0], dd[1]), xadd(dd[2], dd[3]));
             accs += (double)s4;
           }
-          if (active) *reinterpret_cast<float4*>(po) = o.raw;
+          if (active) st4(po, o);
           up = cen;
           cen = dn[u];
           pc += fp;
@@ -179,7 +186,9 @@ __global__ void __launch_bounds__(BLOCK)
 namespace {
 
 constexpr int kBlock = 128;
-constexpr int kUnroll = 4;
+constexpr int kUnroll = 4;  // rows prefetched per group (fp32)
+template <typename T>
+constexpr int unroll_for() { return sizeof(T) == 8 ? SK_F64_UNROLL : kUnroll; }
 
 template <typename T>
 using KernelFn = void (*)(const HelmArgs<T>);
@@ -187,7 +196,7 @@ using KernelFn = void (*)(const HelmArgs<T>);
 template <typename T>
 KernelFn<T> pick(int delta, int reduce) {
 #define SK_H(D, R) \
-  if (delta == D && reduce == R) return helmholtz_sweep<T, kBlock, kUnroll, D, R>;
+  if (delta == D && reduce == R) return helmholtz_sweep<T, kBlock, unroll_for<T>(), D, R>;
   SK_H(SK_DELTA_NONE, SK_REDUCE_SUM)
   SK_H(SK_DELTA_NONE, SK_REDUCE_MAX)
   SK_H(SK_DELTA_ABS, SK_REDUCE_SUM)
@@ -201,7 +210,7 @@ KernelFn<T> pick(int delta, int reduce) {
 template <typename T>
 int setup_t(sk_run* r) {
   const sk_plan& p = r->plan;
-  constexpr int VEC = 16 / sizeof(T);
+  constexpr int VEC = 4;
   KernelFn<T> fn = pick<T>(p.delta_op, p.reduce_op);
   if (!fn) {
     set_error("helmholtz: unsupported delta/reduce combination");

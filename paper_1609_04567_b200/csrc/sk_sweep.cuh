@@ -52,4 +52,44 @@ __device__ __forceinline__ V16<T> zero16() {
   return r;
 }
 
+// Four contiguous elements (16 B for float, 32 B for double), loaded and
+// stored as 16-byte vectors.  Giving every thread 4 elements in both
+// precisions keeps 4 independent arithmetic chains per thread, which the
+// fp64 sweep needs to cover its longer DP latencies.
+template <typename T>
+struct Vec4 {
+  T v[4];
+};
+
+template <typename T>
+__device__ __forceinline__ Vec4<T> ldg4(const T* p) {
+  Vec4<T> r;
+  constexpr int N = sizeof(T) * 4 / 16;
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    const float4 x = __ldg(reinterpret_cast<const float4*>(p) + i);
+    memcpy(reinterpret_cast<char*>(r.v) + 16 * i, &x, 16);
+  }
+  return r;
+}
+
+template <typename T>
+__device__ __forceinline__ void st4(T* p, const Vec4<T>& v) {
+  constexpr int N = sizeof(T) * 4 / 16;
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    float4 x;
+    memcpy(&x, reinterpret_cast<const char*>(v.v) + 16 * i, 16);
+    reinterpret_cast<float4*>(p)[i] = x;
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ Vec4<T> zero4() {
+  Vec4<T> r;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) r.v[i] = T(0);
+  return r;
+}
+
 }  // namespace sk

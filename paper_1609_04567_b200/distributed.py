@@ -129,7 +129,7 @@ class DeviceBlock:
         self.hb = 1 if rank < world - 1 else 0
         R = self.ht + rows + self.hb
         dt = u0.dtype
-        vec = 16 // u0.element_size()
+        vec = max(16 // u0.element_size(), 4)  # whole 4-element thread vectors
         pitch = -(-cols // vec) * vec
         self.pitch = pitch
         dev = u0.device

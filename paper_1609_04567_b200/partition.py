@@ -329,7 +329,9 @@ class DeviceExecutor(Executor):
             raise DeviceUnsupported(f"unknown device kernel {name!r}")
 
         esize = src.element_size()
-        vec = 16 // esize
+        # row pitch: whole 16-byte vectors, and whole 4-element thread vectors
+        # for the Helmholtz sweep (fp64 threads load 2 x 16 B)
+        vec = max(16 // esize, 4) if name == "helmholtz" else 16 // esize
         pitch = -(-cols // vec) * vec
         staged = pitch != cols or src.data_ptr() % 16 != 0
         if staged:
