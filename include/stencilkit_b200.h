@@ -62,12 +62,15 @@ extern "C" {
  *   RMS_LT   : sqrt(value / n) < a            (apps/helmholtz.py:128-131)
  *   MEAN_LT  : value / n < a                  (apps/denoise.py:282-283)
  *   ITER_GE  : iteration >= n                 (stop_after, loop.py:70-74)
+ *   MEAN_FLAGGED_LT : value / max(F, 1) < a   with F the run's flagged-pixel
+ *              count (restore runs; restore_regularize, apps/denoise.py:279-283)
  * all evaluated in fp64 exactly as the Python predicate. */
 #define SK_COND_HOST 0
 #define SK_COND_LT 1
 #define SK_COND_RMS_LT 2
 #define SK_COND_MEAN_LT 3
 #define SK_COND_ITER_GE 4
+#define SK_COND_MEAN_FLAGGED_LT 5
 
 /* One loop plan = the reference's LoopPlan (loop.py:101-110) reduced to
  * device terms.  Grids are row-major with a row pitch in elements. */

@@ -18,6 +18,7 @@ SK_KERNEL_HELMHOLTZ, SK_KERNEL_SOBEL, SK_KERNEL_AMF, SK_KERNEL_RESTORE, SK_KERNE
 SK_REDUCE_SUM, SK_REDUCE_MAX = 1, 2
 SK_DELTA_NONE, SK_DELTA_ABS, SK_DELTA_SQUARE = 0, 1, 2
 SK_COND_HOST, SK_COND_LT, SK_COND_RMS_LT, SK_COND_MEAN_LT, SK_COND_ITER_GE = 0, 1, 2, 3, 4
+SK_COND_MEAN_FLAGGED_LT = 5
 SK_FLAG_TIMING = 1
 
 # every symbol include/stencilkit_b200.h declares

@@ -24,7 +24,7 @@ import numpy as np
 
 from .. import _native as N
 from ..grid import Grid, GridError
-from ..loop import Condition, stop_after
+from ..loop import Condition, DeviceCond, stop_after
 from ..partition import DeploymentMode, WorkerGroup, parallel_loop
 from ..patterns import Combinator, DeviceKernel, DeviceUnsupported, ElementalFn, abs_change
 from ..streams import Stage, StreamReport, ordered_farm, pipeline, run_stream
@@ -114,6 +114,28 @@ def _float_sum() -> Combinator:
     return Combinator(lambda a, b: a + b, 0.0, on_array=lambda arr: float(np.sum(arr)), kind="sum")
 
 
+def _check_mask(noise: Grid) -> None:
+    """The reference rejects anything but 0/1 (apps/denoise.py:276-278).  Host
+    masks are checked on the host; detector outputs carry a (0, 1) range tag;
+    other device masks are checked on the device."""
+    sd = noise.storage_dtype()
+    if sd.kind not in "iub":
+        raise GridError(f"noise map must be 0/1, found dtype {sd}")
+    rng = noise.value_range
+    if rng is not None and rng[0] >= 0 and rng[1] <= 1:
+        return
+    if noise.is_device:
+        t = noise.tensor()
+        mn, mx = int(t.min().item()), int(t.max().item())
+        if mn < 0 or mx > 1:
+            raise GridError(f"noise map must be 0/1, found values in [{mn}, {mx}]")
+        return
+    a = noise._host()
+    bad = (a != 0) & (a != 1)
+    if bad.any():
+        raise GridError(f"noise map must be 0/1, found {a[bad].ravel()[0]!r}")
+
+
 def _flagged_count(noise: Grid) -> int:
     sd = noise.storage_dtype()
     if sd.kind not in "iub":
@@ -141,8 +163,17 @@ def restore_regularize(img: Grid, noise: Grid, cfg: Optional[RestoreConfig] = No
         raise GridError("restoration expects a 2D image")
     if noise.dims != img.dims:
         raise GridError(f"noise map dims {noise.dims} do not match image {img.dims}")
-    denom = max(_flagged_count(noise), 1)
-    cond = Condition.mean_below(cfg.tol, denom, max_iterations=cfg.max_iterations)
+    _check_mask(noise)
+    # value / max(flagged, 1) < tol: on the device the run counts the flagged
+    # pixels itself; a host-evaluated loop counts them once, on first use
+    denom = []
+
+    def stop(value, it, state):
+        if not denom:
+            denom.append(max(_flagged_count(noise), 1))
+        return value / denom[0] < cfg.tol
+
+    cond = Condition(stop, cfg.max_iterations, DeviceCond("mean_flagged_lt", float(cfg.tol)))
     if partitions == 1:
         mode = DeploymentMode.ONE_TO_ONE
     return parallel_loop(mode, partitions, 1, restore_kernel(cfg), _float_sum(), cond, img,

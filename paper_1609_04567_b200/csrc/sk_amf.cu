@@ -80,11 +80,8 @@ __global__ void __launch_bounds__(kTW * kTH) amf_kernel(const __grid_constant__ 
   __shared__ unsigned char tile[TH * TW];
   __shared__ double sh[kTW * kTH / 32];
   __shared__ int s_chunk;
-  long long it = 1;
-  if (!BATCH) {
-    it = loop_enter(a.L);
-    if (it == 0) return;
-  }
+  for (long long it = BATCH ? 1 : loop_enter(a.L); it != 0;
+       it = BATCH ? 0 : loop_next<kTW * kTH>(a.L, it, sh)) {
   const unsigned char* front0;
   unsigned char* back0;
   if (BATCH) {
@@ -139,7 +136,7 @@ __global__ void __launch_bounds__(kTW * kTH) amf_kernel(const __grid_constant__ 
       else a.L.partials[c] = v;
     }
   }
-  if (!BATCH) loop_finalize<kTW * kTH>(a.L, it, sh);
+  }  // iterations
 }
 
 // ---------------------------------------------------------------- host side
@@ -199,8 +196,7 @@ int launch(sk_run* r, const LoopCtl& L, cudaStream_t s) {
   a.tiles_x = r->colblocks;
   a.tiles_per_frame = r->nchunks;
   a.L = L;
-  pick<false>(wmax)<<<r->grid, kTW * kTH, 0, s>>>(a);
-  SK_CUDA(cudaGetLastError());
+  SK_CUDA(launch_kernel(pick<false>(wmax), r->grid, kTW * kTH, a, s, L.persistent != 0));
   return SK_OK;
 }
 

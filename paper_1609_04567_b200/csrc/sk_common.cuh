@@ -33,6 +33,8 @@ struct Status {
   unsigned int work;    // dynamic work-chunk counter
   double gvalue;        // value combined across ranks (sk_run_combine), multi-GPU runs
   long long gdecided;   // iterations the cross-rank combine has evaluated
+  unsigned int gen;     // grid-barrier generation (persistent loops)
+  unsigned int pad3;
 };
 
 constexpr int kMaxParts = 64;
@@ -50,12 +52,15 @@ struct LoopCtl {
   double* partials;         // one slot per work chunk
   int nparts;
   int part_chunk[kMaxParts + 1];  // chunk ranges per partition (ascending rows)
+  const int* part_chunk_dev;      // if set: device-resident chunk ranges (restore)
+  const int* flagged_dev;         // if set: the run's flagged count (MEAN_FLAGGED_LT)
   int reduce;               // SK_REDUCE_SUM / SK_REDUCE_MAX
   double identity;
   volatile double* ring;    // host-mapped per-iteration values (may be null)
   CondDev cond;
   cudaGraphConditionalHandle gh;
   int use_graph;
+  int persistent;  // whole loop inside one cooperative launch (loop_barrier)
 };
 
 // ---------------------------------------------------------------- exact math
@@ -151,8 +156,13 @@ __device__ __forceinline__ double block_reduce(int op, double v, double* sh) {
 // reference's conditions; loop.py:43-57, apps/helmholtz.py:128-131,
 // apps/denoise.py:282-283, loop.py:70-74).  Same fp64 expression as the
 // Python predicate, so the decision is bit-identical.
-__device__ __forceinline__ int eval_cond(const CondDev& c, double v, long long it) {
+__device__ __forceinline__ int eval_cond(const CondDev& c, double v, long long it,
+                                         const int* flagged = nullptr) {
   switch (c.kind) {
+    case SK_COND_MEAN_FLAGGED_LT: {
+      const int f = flagged ? *flagged : 0;
+      return xdiv(v, (double)(f > 1 ? f : 1)) < c.a;
+    }
     case SK_COND_LT: return v < c.a;
     case SK_COND_RMS_LT: return xsqrt(xdiv(v, c.n)) < c.a;
     case SK_COND_MEAN_LT: return xdiv(v, c.n) < c.a;
@@ -185,30 +195,21 @@ __device__ __forceinline__ int next_chunk(const LoopCtl& L, int* s_chunk) {
   return *s_chunk;
 }
 
-// Last-CTA-done finalize, called by every CTA once it runs out of chunks.
-// Folds chunk partials per partition (fixed strided split + fixed tree),
-// then partitions in ascending order from the identity, evaluates the
-// condition and publishes the iteration.
+// Fold + decide, run by all threads of the last CTA to finish an iteration:
+// chunk partials per partition (fixed strided split + fixed tree), then
+// partitions in ascending order from the identity (partition.py:642-646),
+// then the loop condition (loop.py:209-218).  Publishes the iteration;
+// returns the stop decision (valid in every thread).
 template <int BLOCK>
-__device__ void loop_finalize(const LoopCtl& L, long long it, double* sh) {
-  __shared__ int s_last;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    unsigned prev = atomicAdd(&L.st->ticket, 1u);
-    s_last = (prev == gridDim.x - 1);
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
+__device__ __noinline__ int fold_and_decide(const LoopCtl& L, long long it, double* sh) {
+  __shared__ int s_stop;
   const int op = L.reduce;
-  double acc = L.identity;  // host combine from the identity, ascending partitions
+  double acc = L.identity;
   for (int p = 0; p < L.nparts; ++p) {
-    const int c0 = L.part_chunk[p], c1 = L.part_chunk[p + 1];
+    const int c0 = L.part_chunk_dev ? L.part_chunk_dev[p] : L.part_chunk[p];
+    const int c1 = L.part_chunk_dev ? L.part_chunk_dev[p + 1] : L.part_chunk[p + 1];
     double v;
     if (op == SK_REDUCE_SUM) {
-      // the partition's CTA partials: fixed strided split over the block,
-      // then a fixed shuffle/warp tree -- same order on every run
       double t = 0.0;
       for (int c = c0 + (int)threadIdx.x; c < c1; c += BLOCK) t += __ldcg(&L.partials[c]);
       v = block_reduce<BLOCK>(op, t, sh);
@@ -224,8 +225,8 @@ __device__ void loop_finalize(const LoopCtl& L, long long it, double* sh) {
   }
   if (threadIdx.x == 0) {
     Status* st = L.st;
-    int c = eval_cond(L.cond, acc, it);
-    int capped = (it >= L.cond.max_it);
+    const int c = eval_cond(L.cond, acc, it, L.flagged_dev);
+    const int capped = (it >= L.cond.max_it);
     st->value = acc;
     st->cond_true = c;
     st->exhausted = (!c && capped);
@@ -234,9 +235,91 @@ __device__ void loop_finalize(const LoopCtl& L, long long it, double* sh) {
     st->ticket = 0;
     st->work = 0;
     if (L.ring) L.ring[it % kRing] = acc;
-    __threadfence_system();
-    if (L.use_graph) cudaGraphSetConditional(L.gh, (c || capped) ? 0u : 1u);
+    s_stop = c || capped;
   }
+  __syncthreads();
+  return s_stop;
+}
+
+// End of a launched iteration (one launch per iteration, or a graph WHILE
+// body): every CTA arrives; the last one folds, decides and -- in graph
+// mode -- clears the WHILE condition.
+template <int BLOCK>
+__device__ void loop_finalize(const LoopCtl& L, long long it, double* sh) {
+  __shared__ int s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    unsigned prev = atomicAdd(&L.st->ticket, 1u);
+    s_last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int stop = fold_and_decide<BLOCK>(L, it, sh);
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    if (L.use_graph) cudaGraphSetConditional(L.gh, stop ? 0u : 1u);
+  }
+}
+
+// Persistent mode (one cooperative launch runs the whole loop): a grid
+// barrier per iteration whose last arriver folds and decides before it
+// releases the others -- one barrier carries both the data dependency (the
+// next sweep reads what every CTA just wrote) and the loop test.  The
+// gpu-scope fences on both sides also invalidate L1, so the next sweep's
+// read-only loads see the fresh buffer.  Returns the next iteration or 0.
+template <int BLOCK>
+__device__ long long loop_barrier(const LoopCtl& L, long long it, double* sh) {
+  __shared__ int s_last;
+  __shared__ unsigned s_gen;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* genp = &L.st->gen;
+    s_gen = *genp;
+    __threadfence();
+    const unsigned prev = atomicAdd(&L.st->ticket, 1u);
+    s_last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    fold_and_decide<BLOCK>(L, it, sh);
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(&L.st->gen, 1u);  // release
+    }
+  } else if (threadIdx.x == 0) {
+    volatile unsigned* genp = &L.st->gen;
+    while (*genp == s_gen) __nanosleep(64);
+  }
+  __syncthreads();
+  __threadfence();
+  volatile Status* st = L.st;
+  return st->stop ? 0 : it + 1;
+}
+
+// Compile-time variant: PERSIST = false lets the compiler drop the
+// iteration loop entirely (the one-launch-per-iteration kernels keep their
+// register budget).
+template <int BLOCK, bool PERSIST>
+__device__ __forceinline__ long long loop_next_t(const LoopCtl& L, long long it, double* sh) {
+  if (!PERSIST) {
+    loop_finalize<BLOCK>(L, it, sh);
+    return 0;
+  }
+  return loop_barrier<BLOCK>(L, it, sh);
+}
+
+// Iteration driver used by every sweep kernel:
+//   for (long long it = loop_enter(L); it; it = loop_next<BLOCK>(L, it, sh)) { sweep it }
+template <int BLOCK>
+__device__ __forceinline__ long long loop_next(const LoopCtl& L, long long it, double* sh) {
+  if (!L.persistent) {
+    loop_finalize<BLOCK>(L, it, sh);
+    return 0;
+  }
+  return loop_barrier<BLOCK>(L, it, sh);
 }
 
 }  // namespace sk

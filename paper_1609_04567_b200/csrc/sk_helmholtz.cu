@@ -27,6 +27,9 @@
 #ifndef SK_F64_UNROLL
 #define SK_F64_UNROLL 1
 #endif
+#ifndef SK_F32_MINB
+#define SK_F32_MINB 5
+#endif
 #ifndef SK_F64_MINB
 #define SK_F64_MINB 8
 #endif
@@ -44,17 +47,18 @@ struct HelmArgs {
 __device__ __forceinline__ float rcp_rn(float b) { return __frcp_rn(b); }
 __device__ __forceinline__ double rcp_rn(double b) { return __drcp_rn(b); }
 
-template <typename T, int BLOCK, int U, int DELTA, int REDUCE>
-__global__ void __launch_bounds__(BLOCK, (sizeof(T) == 8 ? SK_F64_MINB : 1))
+template <typename T, int BLOCK, int U, int DELTA, int REDUCE, bool PERSIST>
+__global__ void __launch_bounds__(BLOCK, (sizeof(T) == 8 ? (PERSIST ? 4 : SK_F64_MINB) : SK_F32_MINB))
     helmholtz_sweep(const __grid_constant__ HelmArgs<T> a) {
   constexpr int VEC = 4;
   constexpr unsigned FULL = 0xffffffffu;
   __shared__ double sh[BLOCK / 32];
   __shared__ int s_chunk;
 
-  const long long it = loop_enter(a.L);
-  if (it == 0) return;
   const Sweep2D& g = a.g;
+  long long it = loop_enter(a.L);
+  if (it == 0) return;
+  for (;;) {
   const T* front;
   long long fp;
   if (it == 1) {
@@ -178,7 +182,13 @@ __global__ void __launch_bounds__(BLOCK, (sizeof(T) == 8 ? SK_F64_MINB : 1))
     const double v = block_reduce<BLOCK>(REDUCE, mine, sh);
     if (threadIdx.x == 0) a.L.partials[c] = v;
   }
-  loop_finalize<BLOCK>(a.L, it, sh);
+  if (!PERSIST) {  // one launch per iteration: no loop back edge at all
+    loop_finalize<BLOCK>(a.L, it, sh);
+    return;
+  }
+  it = loop_barrier<BLOCK>(a.L, it, sh);
+  if (it == 0) return;
+  }  // iterations
 }
 
 // ---------------------------------------------------------------- host side
@@ -186,6 +196,9 @@ __global__ void __launch_bounds__(BLOCK, (sizeof(T) == 8 ? SK_F64_MINB : 1))
 namespace {
 
 constexpr int kBlock = 128;
+// Above this size a sweep is long enough that per-iteration graph launches
+// cost nothing; below it the whole loop runs as one persistent launch.
+constexpr long long kPersistMaxCells = 1ll << 24;
 constexpr int kUnroll = 4;  // rows prefetched per group (fp32)
 template <typename T>
 constexpr int unroll_for() { return sizeof(T) == 8 ? SK_F64_UNROLL : kUnroll; }
@@ -194,9 +207,11 @@ template <typename T>
 using KernelFn = void (*)(const HelmArgs<T>);
 
 template <typename T>
-KernelFn<T> pick(int delta, int reduce) {
-#define SK_H(D, R) \
-  if (delta == D && reduce == R) return helmholtz_sweep<T, kBlock, unroll_for<T>(), D, R>;
+KernelFn<T> pick(int delta, int reduce, bool persist = false) {
+#define SK_H(D, R)                                                                            \
+  if (delta == D && reduce == R)                                                              \
+    return persist ? helmholtz_sweep<T, kBlock, unroll_for<T>(), D, R, true>                  \
+                   : helmholtz_sweep<T, kBlock, unroll_for<T>(), D, R, false>;
   SK_H(SK_DELTA_NONE, SK_REDUCE_SUM)
   SK_H(SK_DELTA_NONE, SK_REDUCE_MAX)
   SK_H(SK_DELTA_ABS, SK_REDUCE_SUM)
@@ -277,9 +292,22 @@ int launch_t(sk_run* r, const LoopCtl& L, cudaStream_t s) {
   a.keep = (T)p.params[3];
   a.relax = (T)p.params[4];
   a.fast_div = r->aux_n[0] ? 1 : 0;
-  KernelFn<T> fn = pick<T>(p.delta_op, p.reduce_op);
-  fn<<<r->grid, r->block, 0, s>>>(a);
-  SK_CUDA(cudaGetLastError());
+  const bool persist = L.persistent != 0;
+  if (persist && (long long)p.rows * p.cols > kPersistMaxCells) {
+    set_error("helmholtz: persistent loop reserved for small grids");
+    return SK_ERR_UNSUPPORTED;  // caller falls back to the graph loop
+  }
+  KernelFn<T> fn = pick<T>(p.delta_op, p.reduce_op, persist);
+  if (persist) {
+    // the persistent variant has its own register budget: size the grid to
+    // what is co-resident
+    int per_sm = 0;
+    SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, r->block, 0));
+    const int slots = device_sms(r->device) * (per_sm > 0 ? per_sm : 1);
+    SK_CUDA(launch_kernel(fn, r->grid < slots ? r->grid : slots, r->block, a, s, true));
+  } else {
+    SK_CUDA(launch_kernel(fn, r->grid, r->block, a, s, false));
+  }
   return SK_OK;
 }
 

@@ -37,6 +37,19 @@ const KernelOps* amf_ops();  // adaptive-median detection (sk_amf.cu)
 
 int device_sms(int device);
 
+// Plain launch, or a cooperative launch for persistent (whole-loop) kernels,
+// which guarantees every CTA is co-resident for the in-kernel grid barrier.
+template <typename A>
+cudaError_t launch_kernel(void (*fn)(A), int grid, int block, const A& args, cudaStream_t s,
+                          bool cooperative) {
+  if (!cooperative) {
+    fn<<<grid, block, 0, s>>>(args);
+    return cudaGetLastError();
+  }
+  void* params[] = {const_cast<A*>(&args)};
+  return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(fn), grid, block, params, 0, s);
+}
+
 // mismatches of div_const vs IEEE division over all safe fp32 numerators
 // (cached per divisor; -1 if the check could not run)
 long long verify_div_f32(float b, cudaStream_t s);
@@ -65,6 +78,8 @@ struct sk_run {
   int colblocks = 1;
   int chunk_rows = 1;
   int nchunks = 0;
+  const int* part_chunk_dev = nullptr;  // device-computed chunk ranges (restore)
+  const int* flagged_dev = nullptr;     // device-computed flagged count (restore)
 
   // device loop state
   sk::Status* d_status = nullptr;
@@ -74,6 +89,7 @@ struct sk_run {
   long long launched = 0;
   long long total_launches = 0;
   bool combined = false;  // cross-rank combine in use
+  bool persistent_done = false;  // the loop ran as one persistent launch
   cudaEvent_t ev_done[sk::kRing] = {};
 
   // optional per-sweep timing

@@ -43,15 +43,19 @@ struct RestoreArgs {
   int rows, cols;
   const int* list;            // flagged pixels, row * cols + col, ascending
   unsigned char* chg[2];      // per-pixel change flags, ping-pong by iteration
-  int part_off[kMaxParts + 1];  // list offsets per partition
+  const int* part_off;        // device: list offsets per partition [nparts + 1]
   double beta, eps;
   LoopCtl L;
 };
 
-__device__ __forceinline__ double F_eval(double u, const double* v, const double* w, int n,
+// F(u) = beta * sum over the 8 ring terms, in ring order, of w * sqrt((u-v)^2 + eps).
+// Off-image neighbours carry weight 0 exactly as in the block route
+// (apps/denoise.py:230-233): they add +0.0, which leaves the sum unchanged.
+__device__ __forceinline__ double F_eval(double u, const double (&v)[8], const double (&w)[8],
                                          double eps, double beta) {
   double s = 0.0;
-  for (int k = 0; k < n; ++k) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
     const double t = xsub(u, v[k]);
     s = xadd(s, xmul(w[k], xsqrt(xadd(xmul(t, t), eps))));
   }
@@ -61,17 +65,14 @@ __device__ __forceinline__ double F_eval(double u, const double* v, const double
 __device__ double restore_pixel(const RestoreArgs& a, const double* front, long long fp, int i,
                                 int j) {
   double v[8], w[8];
-  int n = 0;
-  const int di[8] = {-1, -1, -1, 0, 0, 1, 1, 1};
-  const int dj[8] = {-1, 0, 1, -1, 1, -1, 0, 1};
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
-    const int ni = i + di[k], nj = j + dj[k];
-    if (ni >= 0 && ni < a.rows && nj >= 0 && nj < a.cols) {
-      v[n] = front[(long long)ni * fp + nj];
-      w[n] = a.mask[(long long)ni * a.mask_pitch + nj] == 1 ? 1.0 : 2.0;
-      ++n;
-    }
+    const int di = k < 3 ? -1 : (k < 5 ? 0 : 1);               // _RING order
+    const int dj = k < 3 ? k - 1 : (k < 5 ? (k == 3 ? -1 : 1) : k - 6);
+    const int ni = i + di, nj = j + dj;
+    const bool in = ni >= 0 && ni < a.rows && nj >= 0 && nj < a.cols;
+    v[k] = in ? front[(long long)ni * fp + nj] : 0.0;
+    w[k] = in ? (a.mask[(long long)ni * a.mask_pitch + nj] == 1 ? 1.0 : 2.0) : 0.0;
   }
   const double r3 = __drcp_rn(3.0);
   double lo = 0.0, hi = 255.0;
@@ -80,30 +81,32 @@ __device__ double restore_pixel(const RestoreArgs& a, const double* front, long 
     const double third = div_const(xsub(hi, lo), 3.0, r3);
     const double m1 = xadd(lo, third);
     const double m2 = xsub(hi, third);
-    if (F_eval(m1, v, w, n, a.eps, a.beta) <= F_eval(m2, v, w, n, a.eps, a.beta)) hi = m2;
+    if (F_eval(m1, v, w, a.eps, a.beta) <= F_eval(m2, v, w, a.eps, a.beta)) hi = m2;
     else lo = m1;
   }
   return xmul(0.5, xadd(lo, hi));
 }
 
-__global__ void __launch_bounds__(kRB) restore_sweep(const __grid_constant__ RestoreArgs a) {
+__global__ void __launch_bounds__(kRB, 6) restore_sweep(const __grid_constant__ RestoreArgs a) {
   __shared__ double sh[kRB / 32];
   __shared__ double s_delta[kCh];
   __shared__ short s_queue[kCh];
   __shared__ int s_qlen;
   __shared__ int s_chunk;
-  const long long it = loop_enter(a.L);
-  if (it == 0) return;
+  for (long long it = loop_enter(a.L); it != 0; it = loop_next<kRB>(a.L, it, sh)) {
   const double* front = it == 1 ? a.src : a.buf[(it - 1) & 1];
   const long long fp = it == 1 ? a.src_pitch : a.pitch;
   double* back = a.buf[it & 1];
   const unsigned char* cprev = a.chg[(it - 1) & 1];
   unsigned char* ccur = a.chg[it & 1];
-  const int total = a.L.part_chunk[a.L.nparts];
+  // chunk geometry lives on the device (built by the setup kernels, so the
+  // host never waits for the flagged count)
+  const int* pch = a.L.part_chunk_dev;
+  const int total = pch[a.L.nparts];
   for (int c = next_chunk(a.L, &s_chunk); c < total; c = next_chunk(a.L, &s_chunk)) {
     int p = 0;
-    while (p + 1 < a.L.nparts && c >= a.L.part_chunk[p + 1]) ++p;
-    const int e0 = a.part_off[p] + (c - a.L.part_chunk[p]) * kCh;
+    while (p + 1 < a.L.nparts && c >= pch[p + 1]) ++p;
+    const int e0 = a.part_off[p] + (c - pch[p]) * kCh;
     const int e1 = min(e0 + kCh, a.part_off[p + 1]);
     if (threadIdx.x == 0) s_qlen = 0;
     __syncthreads();
@@ -161,7 +164,7 @@ __global__ void __launch_bounds__(kRB) restore_sweep(const __grid_constant__ Res
     const double v = block_reduce<kRB>(SK_REDUCE_SUM, t, sh);
     if (threadIdx.x == 0) a.L.partials[c] = v;
   }
-  loop_finalize<kRB>(a.L, it, sh);
+  }  // iterations
 }
 
 // ---- flagged-list construction: count per segment, scan, scatter (ordered)
@@ -254,23 +257,33 @@ __global__ void flag_scatter(const unsigned char* mask, long long mpitch, int ro
   }
 }
 
-// partition p's flagged pixels start at lower_bound(list, part_row[p] * cols)
-__global__ void list_bounds(const int* list, int n, const int* part_row, int nparts, int cols,
-                            int* off) {
+// partition p's flagged pixels start at lower_bound(list, part_row[p] * cols);
+// then one thread turns the offsets into per-partition chunk ranges
+__global__ void list_bounds(const int* list, const int* n_ptr, const int* part_row, int nparts,
+                            int cols, int* off, int* pchunk) {
   const int p = threadIdx.x;
-  if (p > nparts) return;
-  if (p == nparts) {
+  const int n = *n_ptr;
+  if (p < nparts) {
+    const long long key = (long long)part_row[p] * cols;
+    int lo = 0, hi = n;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if ((long long)list[mid] < key) lo = mid + 1;
+      else hi = mid;
+    }
+    off[p] = lo;
+  } else if (p == nparts) {
     off[p] = n;
-    return;
   }
-  const long long key = (long long)part_row[p] * cols;
-  int lo = 0, hi = n;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if ((long long)list[mid] < key) lo = mid + 1;
-    else hi = mid;
+  __syncthreads();
+  if (p == 0) {
+    int acc = 0;
+    pchunk[0] = 0;
+    for (int i = 0; i < nparts; ++i) {
+      acc += (off[i + 1] - off[i] + kCh - 1) / kCh;
+      pchunk[i + 1] = acc;
+    }
   }
-  off[p] = lo;
 }
 
 // ---------------------------------------------------------------- host side
@@ -293,33 +306,31 @@ int setup(sk_run* r) {
     set_error("restore: grid too large for 32-bit pixel indices");
     return SK_ERR_ARG;
   }
+  // Entirely stream-ordered: no host synchronisation, so a farm of restore
+  // runs never stalls its host thread here.
   cudaStream_t s = r->stream;
   const long long npix = p.rows * p.cols;
   const int nseg = (int)((npix + kSeg - 1) / kSeg);
   const unsigned char* mask = static_cast<const unsigned char*>(r->env);
   int* seg = nullptr;
-  SK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&seg), sizeof(int) * (nseg + 1 + 2 * (kMaxParts + 1)), s));
+  const size_t small = (size_t)nseg + 1 + 3 * (kMaxParts + 1);
+  SK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&seg), sizeof(int) * small, s));
   r->aux[AUX_SEG] = seg;
   int* d_prow = seg + nseg + 1;
   int* d_off = d_prow + kMaxParts + 1;
+  int* d_pch = d_off + kMaxParts + 1;
   SK_CUDA(cudaMemsetAsync(seg + nseg, 0, sizeof(int), s));
   flag_count<<<nseg, 256, 0, s>>>(mask, r->env_pitch, (int)p.rows, (int)p.cols, seg);
-  flag_scan<<<1, 1024, 0, s>>>(seg, nseg + 1);  // seg[nseg] = total
-  int nflag = 0;
-  SK_CUDA(cudaMemcpyAsync(&nflag, seg + nseg, sizeof(int), cudaMemcpyDeviceToHost, s));
-  SK_CUDA(cudaStreamSynchronize(s));
-  int* list = nullptr;
-  SK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&list), sizeof(int) * ((size_t)nflag + 1), s));
+  flag_scan<<<1, 1024, 0, s>>>(seg, nseg + 1);  // seg[nseg] = total flagged
+  int* list = nullptr;  // capacity: every pixel (the count is not read back)
+  SK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&list), sizeof(int) * ((size_t)npix + 1), s));
   r->aux[AUX_LIST] = list;
-  r->aux_n[AUX_LIST] = nflag;
   flag_scatter<<<nseg, 256, 0, s>>>(mask, r->env_pitch, (int)p.rows, (int)p.cols, seg, list);
   SK_CUDA(cudaMemcpyAsync(d_prow, r->part_row, sizeof(int) * (r->nparts + 1),
                           cudaMemcpyHostToDevice, s));
-  list_bounds<<<1, kMaxParts + 1, 0, s>>>(list, nflag, d_prow, r->nparts, (int)p.cols, d_off);
+  list_bounds<<<1, kMaxParts + 1, 0, s>>>(list, seg + nseg, d_prow, r->nparts, (int)p.cols, d_off,
+                                         d_pch);
   SK_CUDA(cudaGetLastError());
-  int* offs = new int[kMaxParts + 1];
-  r->aux[AUX_OFF] = offs;
-  SK_CUDA(cudaMemcpyAsync(offs, d_off, sizeof(int) * (r->nparts + 1), cudaMemcpyDeviceToHost, s));
   unsigned char* chg = nullptr;
   SK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&chg), (size_t)npix * 2, s));
   r->aux[AUX_CHG] = chg;
@@ -328,19 +339,16 @@ int setup(sk_run* r) {
   for (int b = 0; b < 2; ++b)
     SK_CUDA(cudaMemcpy2DAsync(r->buf[b], r->pitch * 8, r->src, r->src_pitch * 8, p.cols * 8,
                               p.rows, cudaMemcpyDeviceToDevice, s));
-  SK_CUDA(cudaStreamSynchronize(s));
-  // work chunks per partition over its contiguous sub-range of the list
-  int nch = 0;
-  r->part_chunk[0] = 0;
-  for (int i = 0; i < r->nparts; ++i) {
-    nch += (offs[i + 1] - offs[i] + kCh - 1) / kCh;
-    r->part_chunk[i + 1] = nch;
-  }
-  r->nchunks = nch;
+  r->aux[AUX_OFF] = d_off;
+  r->part_chunk_dev = d_pch;
+  r->flagged_dev = seg + nseg;
+  // partial slots for the largest possible chunk count
+  r->nchunks = (int)((npix + kCh - 1) / kCh) + r->nparts;
   int per_sm = 0;
   SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, restore_sweep, kRB, 0));
   const long long slots = (long long)device_sms(r->device) * (per_sm > 0 ? per_sm : 1);
-  r->grid = (int)(slots < nch ? slots : nch);
+  const long long most = r->nchunks;
+  r->grid = (int)(slots < most ? slots : most);
   if (r->grid < 1) r->grid = 1;
   r->block = kRB;
   return SK_OK;
@@ -361,21 +369,18 @@ int launch(sk_run* r, const LoopCtl& L, cudaStream_t s) {
   unsigned char* chg = static_cast<unsigned char*>(r->aux[AUX_CHG]);
   a.chg[0] = chg;
   a.chg[1] = chg + r->plan.rows * r->plan.cols;
-  const int* offs = static_cast<const int*>(r->aux[AUX_OFF]);
-  for (int i = 0; i <= r->nparts; ++i) a.part_off[i] = offs[i];
+  a.part_off = static_cast<const int*>(r->aux[AUX_OFF]);
   a.beta = r->plan.params[0];
   a.eps = r->plan.params[1];
   a.L = L;
-  restore_sweep<<<r->grid, kRB, 0, s>>>(a);
-  SK_CUDA(cudaGetLastError());
+  SK_CUDA(launch_kernel(restore_sweep, r->grid, kRB, a, s, L.persistent != 0));
   return SK_OK;
 }
 
 void teardown(sk_run* r) {
   for (int k : {AUX_LIST, AUX_CHG, AUX_SEG})
     if (r->aux[k]) cudaFreeAsync(r->aux[k], r->stream);
-  delete[] static_cast<int*>(r->aux[AUX_OFF]);
-  r->aux[AUX_OFF] = nullptr;
+  r->aux[AUX_OFF] = nullptr;  // lives inside the AUX_SEG block
 }
 
 const KernelOps kOps = {setup, launch, teardown};

@@ -79,6 +79,8 @@ static LoopCtl make_ctl(sk_run* r, const sk_cond* c, bool graph, cudaGraphCondit
   L.partials = r->d_partials;
   L.nparts = r->nparts;
   for (int i = 0; i <= r->nparts; ++i) L.part_chunk[i] = r->part_chunk[i];
+  L.part_chunk_dev = r->part_chunk_dev;
+  L.flagged_dev = r->flagged_dev;
   L.reduce = r->plan.reduce_op;
   L.identity = r->plan.identity;
   L.ring = r->d_ring;
@@ -95,6 +97,7 @@ static LoopCtl make_ctl(sk_run* r, const sk_cond* c, bool graph, cudaGraphCondit
   }
   L.gh = gh;
   L.use_graph = graph ? 1 : 0;
+  L.persistent = 0;
   return L;
 }
 
@@ -276,8 +279,25 @@ int sk_run_loop(sk_run* r, const sk_cond* c, int64_t* iterations, double* final_
   // SK_NO_GRAPH=1 forces plain launches (profilers cannot see kernels inside
   // conditional graph nodes)
   const char* ng = getenv("SK_NO_GRAPH");
+  const char* np = getenv("SK_NO_PERSIST");
   bool use_graph = !r->timing && !(ng && ng[0] == '1');
-  if (use_graph) {
+  bool persistent = !r->timing && !(np && np[0] == '1');
+  if (persistent) {
+    // One cooperative launch runs every iteration (in-kernel grid barrier
+    // carrying the convergence decision); no per-iteration launches at all.
+    LoopCtl L = make_ctl(r, c, false, 0);
+    L.persistent = 1;
+    rc = r->ops->launch(r, L, r->stream);
+    if (rc == SK_OK) {
+      use_graph = false;
+      r->total_launches += 1;
+      r->persistent_done = true;
+    } else {
+      cudaGetLastError();  // e.g. cooperative launch unavailable: fall back
+      rc = SK_OK;
+    }
+  }
+  if (use_graph && !r->persistent_done) {
     // One graph: conditional WHILE node whose body is one sweep; the sweep's
     // finalizing CTA clears the condition when the loop is over.
     cudaGraph_t g = nullptr;
@@ -323,7 +343,7 @@ int sk_run_loop(sk_run* r, const sk_cond* c, int64_t* iterations, double* final_
       use_graph = false;
     }
   }
-  if (!use_graph) {
+  if (!use_graph && !r->persistent_done) {
     // Batched launches: iterations after the device-decided stop are no-ops.
     LoopCtl L = make_ctl(r, c, false, 0);
     const int batch = 8;

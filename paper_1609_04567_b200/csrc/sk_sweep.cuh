@@ -57,38 +57,37 @@ __device__ __forceinline__ V16<T> zero16() {
 // precisions keeps 4 independent arithmetic chains per thread, which the
 // fp64 sweep needs to cover its longer DP latencies.
 template <typename T>
-struct Vec4 {
-  T v[4];
+union Vec4;
+template <>
+union Vec4<float> {
+  float4 q[1];
+  float v[4];
+};
+template <>
+union Vec4<double> {
+  float4 q[2];
+  double v[4];
 };
 
 template <typename T>
 __device__ __forceinline__ Vec4<T> ldg4(const T* p) {
   Vec4<T> r;
-  constexpr int N = sizeof(T) * 4 / 16;
 #pragma unroll
-  for (int i = 0; i < N; ++i) {
-    const float4 x = __ldg(reinterpret_cast<const float4*>(p) + i);
-    memcpy(reinterpret_cast<char*>(r.v) + 16 * i, &x, 16);
-  }
+  for (int i = 0; i < (int)(sizeof(r.q) / 16); ++i) r.q[i] = __ldg(reinterpret_cast<const float4*>(p) + i);
   return r;
 }
 
 template <typename T>
 __device__ __forceinline__ void st4(T* p, const Vec4<T>& v) {
-  constexpr int N = sizeof(T) * 4 / 16;
 #pragma unroll
-  for (int i = 0; i < N; ++i) {
-    float4 x;
-    memcpy(&x, reinterpret_cast<const char*>(v.v) + 16 * i, 16);
-    reinterpret_cast<float4*>(p)[i] = x;
-  }
+  for (int i = 0; i < (int)(sizeof(v.q) / 16); ++i) reinterpret_cast<float4*>(p)[i] = v.q[i];
 }
 
 template <typename T>
 __device__ __forceinline__ Vec4<T> zero4() {
   Vec4<T> r;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) r.v[i] = T(0);
+  for (int i = 0; i < (int)(sizeof(r.q) / 16); ++i) r.q[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   return r;
 }
 

@@ -76,11 +76,8 @@ __global__ void __launch_bounds__(BLOCK) u8_sweep(const __grid_constant__ U8Args
   constexpr unsigned FULL = 0xffffffffu;
   __shared__ double sh[BLOCK / 32];
   const Sweep2D& g = a.g;
-  long long it = 1;
-  if (!BATCH) {
-    it = loop_enter(a.L);
-    if (it == 0) return;
-  }
+  for (long long it = BATCH ? 1 : loop_enter(a.L); it != 0;
+       it = BATCH ? 0 : loop_next<BLOCK>(a.L, it, sh)) {
   const int lane = threadIdx.x & 31;
   const int cols = g.cols, rows = g.rows;
   const int total = BATCH ? a.frames * a.chunks_per_frame : a.L.part_chunk[a.L.nparts];
@@ -246,7 +243,7 @@ __global__ void __launch_bounds__(BLOCK) u8_sweep(const __grid_constant__ U8Args
       else a.L.partials[c] = v;
     }
   }
-  if (!BATCH) loop_finalize<BLOCK>(a.L, it, sh);
+  }  // iterations
 }
 
 // ---------------------------------------------------------------- Sobel, SWAR
@@ -297,11 +294,8 @@ __global__ void __launch_bounds__(BLOCK) sobel_sweep(const __grid_constant__ U8A
   constexpr unsigned FULL = 0xffffffffu;
   __shared__ double sh[BLOCK / 32];
   const Sweep2D& g = a.g;
-  long long it = 1;
-  if (!BATCH) {
-    it = loop_enter(a.L);
-    if (it == 0) return;
-  }
+  for (long long it = BATCH ? 1 : loop_enter(a.L); it != 0;
+       it = BATCH ? 0 : loop_next<BLOCK>(a.L, it, sh)) {
   const int lane = threadIdx.x & 31;
   const int cols = g.cols, rows = g.rows;
   const int total = BATCH ? a.frames * a.chunks_per_frame : a.L.part_chunk[a.L.nparts];
@@ -490,7 +484,7 @@ __global__ void __launch_bounds__(BLOCK) sobel_sweep(const __grid_constant__ U8A
       else a.L.partials[c] = v;
     }
   }
-  if (!BATCH) loop_finalize<BLOCK>(a.L, it, sh);
+  }  // iterations
 }
 
 // ---------------------------------------------------------------- host side
@@ -576,8 +570,7 @@ int launch(sk_run* r, const LoopCtl& L, cudaStream_t s) {
   fill_geom(r, a.g);
   a.L = L;
   U8Fn fn = pick(op_of(r), r->plan.reduce_op, false);
-  fn<<<r->grid, kBlock, 0, s>>>(a);
-  SK_CUDA(cudaGetLastError());
+  SK_CUDA(launch_kernel(fn, r->grid, kBlock, a, s, L.persistent != 0));
   return SK_OK;
 }
 

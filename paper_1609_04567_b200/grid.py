@@ -76,7 +76,7 @@ class Grid:
     ints do.
     """
 
-    __slots__ = ("dims", "_list", "_arr", "_t", "_ldtype", "_src")
+    __slots__ = ("dims", "_list", "_arr", "_t", "_ldtype", "_src", "value_range")
 
     def __init__(self, dims: Sequence[int], data: Sequence[Any]):
         dims = _check_dims(dims)
@@ -85,6 +85,7 @@ class Grid:
             size *= d
         self._list = self._arr = self._t = None
         self._ldtype = None
+        self.value_range = None  # (lo, hi) known bound of every element, if any
         if isinstance(data, np.ndarray):
             if data.size != size:
                 raise GridError(
@@ -171,6 +172,7 @@ class Grid:
         self._list = list(value)
         self._arr = self._t = None
         self._src = "list"
+        self.value_range = None
 
     @property
     def is_device(self) -> bool:
@@ -304,6 +306,7 @@ class Grid:
         self._list = self._t = None
         self._ldtype = None
         self._src = "arr"
+        self.value_range = None
 
 
 def _numpy_dtype_of(tdtype):

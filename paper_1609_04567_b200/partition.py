@@ -163,7 +163,10 @@ _KERNEL_IDS = {"helmholtz": N.SK_KERNEL_HELMHOLTZ, "sobel": N.SK_KERNEL_SOBEL,
 _REDUCE = {"sum": N.SK_REDUCE_SUM, "max": N.SK_REDUCE_MAX}
 _DELTA = {"none": N.SK_DELTA_NONE, "abs": N.SK_DELTA_ABS, "square": N.SK_DELTA_SQUARE}
 _COND = {"lt": N.SK_COND_LT, "rms_lt": N.SK_COND_RMS_LT, "mean_lt": N.SK_COND_MEAN_LT,
-         "iter_ge": N.SK_COND_ITER_GE}
+         "iter_ge": N.SK_COND_ITER_GE, "mean_flagged_lt": N.SK_COND_MEAN_FLAGGED_LT}
+# value range every output pixel of a u8 kernel lies in (tags the result grid
+# so the next device stage can skip re-validating it)
+_OUT_RANGE = {"sobel": (0, 255), "amf": (0, 1), "life": (0, 1)}
 
 
 def _torch():
@@ -195,18 +198,31 @@ class _DevRun:
 
 
 def _u8_from(grid: Grid, what: str, lo: int, hi: int, dev):
-    """Integer image -> device uint8 tensor, values checked in [lo, hi]."""
+    """Integer image -> device uint8 tensor, values checked in [lo, hi].
+
+    Host grids are checked and narrowed to uint8 on the host (1 byte per
+    pixel crosses PCIe); device grids tagged with a known value range by the
+    kernel that produced them skip the check (no host synchronisation)."""
     torch = _torch()
     sd = grid.storage_dtype()
     if sd.kind not in "iub":
         raise GridError(f"{what} expects integer pixels, got dtype {sd}")
+    rng = grid.value_range
+    known = rng is not None and rng[0] >= lo and rng[1] <= hi
+    if not grid.is_device:
+        a = grid._host()
+        if not known and sd != np.uint8 or (sd == np.uint8 and hi < 255 and not known):
+            mn, mx = (int(a.min()), int(a.max())) if a.size else (lo, lo)
+            if mn < lo or mx > hi:
+                raise GridError(
+                    f"{what}: pixel values must lie in [{lo}, {hi}], found [{mn}, {mx}]")
+        return torch.from_numpy(np.ascontiguousarray(a, dtype=np.uint8)).to(dev)
     t = grid.tensor(device=dev)
-    if t.dtype != torch.uint8:
+    if not known and (t.dtype != torch.uint8 or hi < 255):
         mn, mx = int(t.min().item()), int(t.max().item())
         if mn < lo or mx > hi:
             raise GridError(f"{what}: pixel values must lie in [{lo}, {hi}], found [{mn}, {mx}]")
-        t = t.to(torch.uint8)
-    return t
+    return t if t.dtype == torch.uint8 else t.to(torch.uint8)
 
 
 def _our_grid(g):
@@ -427,7 +443,9 @@ class DeviceExecutor(Executor):
         if run.pitch != run.cols:
             out = out.contiguous()
         led = model_ledger(run.dims, run.P, run.plan.k, it)
-        return Grid.from_tensor(out, logical_dtype=run.out_dtype), led
+        g = Grid.from_tensor(out, logical_dtype=run.out_dtype)
+        g.value_range = _OUT_RANGE.get(run.plan.fn.device.name)
+        return g, led
 
     def abort(self, run: _DevRun) -> None:
         self._release(run)

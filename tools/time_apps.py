@@ -39,8 +39,23 @@ def med(fn, reps=7):
     return statistics.median(ts)
 
 
-which = sys.argv[1].split(",") if len(sys.argv) > 1 else ["sobel", "amf", "restore", "c5"]
+which = sys.argv[1].split(",") if len(sys.argv) > 1 else ["sobel", "amf", "restore", "c5", "c1"]
 warm()
+if "c1" in which:
+    from paper_1609_04567_b200.apps import HelmholtzConfig, helmholtz_kernel, helmholtz_solve
+    u0 = torch.zeros((1024, 1024), dtype=torch.float32, device="cuda")
+    f = torch.ones((1024, 1024), dtype=torch.float32, device="cuda")
+    kern = helmholtz_kernel(HelmholtzConfig(1024, 1024))
+
+    def c1():
+        return sk.loop_stencil_reduce_d(1, kern, sk.abs_change(), sk.max_combinator(0.0),
+                                        sk.Condition.below(1e-4), sk.Grid.from_tensor(u0),
+                                        env=sk.Grid.from_tensor(f))
+    c1()
+    ms = med(c1, reps=9)
+    print(json.dumps({"workload": "C1 1024^2 fp32 36 sweeps (graph loop, incl. begin/finish)",
+                      "ms": ms, "us_per_iteration": ms * 1e3 / 36,
+                      "cell_updates_per_s": 36 * 1024 * 1024 / ms * 1e3}))
 if "sobel" in which:
     F, H, W = 128, 2048, 2048
     fr = torch.randint(0, 256, (F, H, W), dtype=torch.uint8, device="cuda")
