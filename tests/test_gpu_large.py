@@ -79,3 +79,23 @@ def test_c5_frames(golden_large, i):
         a = out.to_array()
         assert sha(a) == mr["sha"]
         assert sha(np.clip(np.rint(a), 0, 255).astype(np.uint8)) == mr["sha_u8"]
+
+
+def test_c3_denoise_4096_full_size():
+    """BASELINE config C3 at its real size: 4096^2, 50% noise, AMF then 100
+    restore iterations (the reference took ~11 min on 8 cores to produce it)."""
+    import json
+    import os
+
+    path = os.path.join(os.path.dirname(__file__), "golden", "golden_c3_4096.json")
+    m = json.load(open(path))["C3_denoise_4096"]
+    noisy, _ = O.salt_pepper(O.gradient_image(4096, 4096), 0.5, seed=42)
+    mask = amf_detect(sk.Grid.from_array(noisy.astype(np.uint8)))
+    ma = mask.to_array().astype(np.uint8)
+    assert int(ma.sum()) == m["flagged"] and sha(ma) == m["sha_mask"]
+    out, rep = restore_regularize(sk.Grid.from_array(noisy.astype(np.uint8)), mask, partitions=8)
+    assert rep.iterations == m["iterations"] and rep.exhausted == m["exhausted"]
+    a = out.to_array()
+    assert sha(a) == m["sha"]
+    assert sha(np.clip(np.rint(a), 0, 255).astype(np.uint8)) == m["sha_u8"]
+    assert rep.final_reduce == pytest.approx(m["final_reduce"], rel=1e-12)
