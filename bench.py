@@ -127,6 +127,33 @@ def cpu_reference(n_cells_target: float, steps: int):
 # ----------------------------------------------------------------------------- GPU arm
 
 
+def run_workload(args):
+    """--workload c1|c2|c3|c5 (bench_workloads.py); c4 is run_ours below."""
+    import torch
+
+    import bench_workloads as W
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    fn = getattr(W, args.workload)
+    if args.workload in ("c2", "c5"):
+        line = fn(args, ClockSampler, measured_peaks, local=local, world=world, rank=rank)
+    else:  # replicas only: every rank solves its own copy
+        line = fn(args, ClockSampler, measured_peaks, local=local)
+        if world > 1:
+            line["n_gpus"] = world
+            line["value"] *= world
+            line["config"]["parallelism"] = f"{world} independent replicas (no collective)"
+    if rank == 0:
+        print(json.dumps(line))
+
+
 def run_ours(args):
     import torch
 
@@ -286,9 +313,13 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=32768)
+    ap.add_argument("--workload", default="c4", choices=["c1", "c2", "c3", "c4", "c5"],
+                    help="BASELINE.json config (default c4: the cell-updates/s headline)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
+    elif args.workload != "c4":
+        run_workload(args)
     else:
         run_ours(args)
 

@@ -1,0 +1,455 @@
+"""The non-default bench workloads (BASELINE.json configs C1, C2, C3, C5).
+
+Used by `bench.py --workload c1|c2|c3|c5`; each returns the contract's JSON
+line (same keys as the C4 line in bench.py).  The CPU legs time the numpy
+restatement in oracle/ (bit-identical to the reference) on bounded samples.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import statistics
+import time
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+
+
+def fp64_peak():
+    """Measured FP64 rates (tools/fp64_peak.cu on this pool's B200)."""
+    p = os.path.join(ROOT, "profiles", "r01_fp64_peak.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["dfma_per_s"]), float(d["dsqrt_per_s"]), "measured (profiles/r01_fp64_peak.json)"
+    return 18.5e12, 1.25e12, "fallback (nominal)"
+
+
+# Per active flagged pixel and iteration the restore search does 18 steps x 2
+# evaluations of F, each 8 ring terms of (sub, mul, add, sqrt, mul, add) plus
+# beta*s, plus the step bookkeeping: ~1550 DP add/mul + 288 IEEE sqrt.  In
+# DFMA-equivalents (one IEEE DSQRT costs dfma_rate / dsqrt_rate of them):
+RESTORE_DP_OPS = 1550
+RESTORE_SQRT = 288
+
+
+def restore_roofline(flagged, t_iter1_ms):
+    dfma, dsq, src = fp64_peak()
+    eq = RESTORE_DP_OPS + RESTORE_SQRT * dfma / dsq
+    achieved = flagged * eq / (t_iter1_ms / 1e3)
+    return {"bound": "fp64", "achieved": achieved / 1e12, "peak": dfma / 1e12,
+            "unit": "TDFMA-eq/s", "frac": achieved / dfma, "traffic": None,
+            "kernel": "restore_sweep (iteration 1: every flagged pixel active)",
+            "work_per_unit": f"{eq:.0f} DFMA-eq per flagged pixel-iteration "
+                             f"({RESTORE_DP_OPS} DP add/mul + {RESTORE_SQRT} DSQRT)",
+            "avg_kernel_ms": t_iter1_ms, "peak_source": src}
+
+
+def _events():
+    import torch
+
+    return torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+
+def _base(args, metric, unit, value, ms, dtype, workload, extra=None):
+    d = {"metric": metric, "value": value, "unit": unit, "n_gpus": 1, "steps": args.steps,
+         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+         "vs_baseline": None, "dtype": dtype, "data": "synthetic",
+         "config": {"workload": workload}}
+    if extra:
+        d["config"].update(extra)
+    return d
+
+
+# ----------------------------------------------------------------------------- C1
+
+
+def c1(args, ClockSampler, measured_peaks, local=0):
+    """1024^2 fp32 Helmholtz, MAX|delta| < 1e-4 (36 sweeps): the reference's
+    own CPU-scale config.  L2-resident and latency-bound: the whole loop is
+    one persistent cooperative launch."""
+    import torch
+
+    import paper_1609_04567_b200 as sk
+    from paper_1609_04567_b200.apps import HelmholtzConfig, helmholtz_kernel
+    from oracle import stencil_oracle as O
+
+    n, per_step = 1024, 50
+    kern = helmholtz_kernel(HelmholtzConfig(n, n))
+    u0 = torch.zeros((n, n), dtype=torch.float32, device="cuda")
+    f = torch.ones((n, n), dtype=torch.float32, device="cuda")
+    g0, gf = sk.Grid.from_tensor(u0), sk.Grid.from_tensor(f)
+    ex = sk.DeviceExecutor(1)
+
+    def solve():
+        return sk.loop_stencil_reduce_d(1, kern, sk.abs_change(), sk.max_combinator(0.0),
+                                        sk.Condition.below(1e-4), g0, env=gf, executor=ex)
+
+    for _ in range(args.warmup * per_step):
+        out, rep = solve()
+    assert rep.iterations == 36
+    ex.launches = 0
+    s, e = _events()
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        s.record()
+        for _ in range(args.steps * per_step):
+            out, rep = solve()
+        e.record()
+        torch.cuda.synchronize()
+    ms = s.elapsed_time(e) / args.steps
+    cells = 36.0 * n * n * per_step
+    # e2e: host numpy in, host numpy out, through the public API
+    h0 = np.zeros((n, n), np.float32)
+    hf = np.ones((n, n), np.float32)
+    sk.loop_stencil_reduce_d(1, kern, sk.abs_change(), sk.max_combinator(0.0),
+                             sk.Condition.below(1e-4), sk.Grid((n, n), h0),
+                             env=sk.Grid((n, n), hf))[0].to_array()
+    t0 = time.perf_counter()
+    for _ in range(per_step):
+        o, _ = sk.loop_stencil_reduce_d(1, kern, sk.abs_change(), sk.max_combinator(0.0),
+                                        sk.Condition.below(1e-4), sk.Grid((n, n), h0),
+                                        env=sk.Grid((n, n), hf))
+        o.to_array()
+    e2e_s = (time.perf_counter() - t0) / per_step
+    # roofline: the persistent loop's time per sweep (barrier + fold included)
+    peak, pk = measured_peaks()
+    sweep_ms = ms / per_step / 36
+    ach = 12.0 * n * n / (sweep_ms / 1e3) / 1e9
+    t0 = time.perf_counter()
+    O.helmholtz_loop(np.zeros((n, n), np.float32), np.ones((n, n), np.float32),
+                     O.helmholtz_consts(), delta="abs", op="max", cond=lambda v, it: v < 1e-4,
+                     P=os.cpu_count() or 1, threads=os.cpu_count() or 1)
+    cpu = 36.0 * n * n / (time.perf_counter() - t0)
+    line = _base(args, "stencil cell-updates/s", "cell-updates/s", cells / (ms / 1e3), ms, "f32",
+                 "C1 Helmholtz 1024x1024 fp32, MAX|delta|<1e-4 (36 sweeps), "
+                 f"{per_step} solves per step", {"l2": "12.6 MB working set is L2-resident "
+                                                       "by design (the config's own size)"})
+    line.update({
+        "gpu_launches": ex.launches,
+        "e2e": {"value": 36.0 * n * n / e2e_s, "unit": "cell-updates/s",
+                "h2d_bytes_per_step": 8 * n * n * per_step,
+                "d2h_bytes_per_step": 4 * n * n * per_step, "ms_per_solve": e2e_s * 1e3},
+        "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                     "frac": ach / peak, "traffic": None, "avg_kernel_ms": sweep_ms,
+                     "kernel": "helmholtz_sweep<float, persistent> per sweep incl. grid barrier",
+                     "note": "latency-bound (L2-resident); one cooperative launch per solve",
+                     "peak_source": pk},
+        "cpu_baseline": {"value": cpu, "unit": "cell-updates/s", "cores": os.cpu_count(),
+                         "kind": "port", "sample": "the full C1 solve (36 sweeps) with the "
+                                                   "numpy restatement, P=cores threads"},
+        "clocks": clk.summary(),
+    })
+    return line
+
+
+# ----------------------------------------------------------------------------- C2
+
+
+def _sobel_cpu(frames=8):
+    from oracle import stencil_oracle as O
+
+    rng = np.random.default_rng(0)
+    imgs = [rng.integers(0, 256, (2048, 2048)).astype(np.uint8) for _ in range(frames)]
+    cores = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(cores) as pool:
+        list(pool.map(O.sobel, imgs))
+    dt = time.perf_counter() - t0
+    return frames / dt, cores, f"{frames} random 2048x2048 frames, oracle Sobel on {cores} threads"
+
+
+def c2(args, ClockSampler, measured_peaks, local=0, world=1, rank=0):
+    """Sobel over a stream of 512 synthetic 2048x2048 uint8 frames.
+    value: frames resident in HBM, batched launches of 64 frames;
+    e2e: frames from pinned host memory, H2D / kernel / D2H overlapped over
+    3 CUDA streams (the stream mode)."""
+    import torch
+
+    from paper_1609_04567_b200.apps import sobel_frames
+
+    F_all, B, H, W = 512, 64, 2048, 2048
+    F = F_all // world
+    gen = torch.Generator(device="cuda").manual_seed(rank)
+    frames = torch.randint(0, 256, (F, H, W), dtype=torch.uint8, device="cuda", generator=gen)
+    out = torch.empty_like(frames)
+
+    def step(timed=None):
+        for b in range(0, F, B):
+            if timed is not None:
+                a, z = _events()
+                a.record()
+            sobel_frames(frames[b:b + B], out=out[b:b + B])
+            if timed is not None:
+                z.record()
+                timed.append((a, z))
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    ev = []
+    s, e = _events()
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        s.record()
+        for _ in range(args.steps):
+            step(ev)
+        e.record()
+        torch.cuda.synchronize()
+    ms = s.elapsed_time(e) / args.steps
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    kms = statistics.mean(a.elapsed_time(z) for a, z in ev)
+    peak, pk = measured_peaks()
+    ach = 2.0 * B * H * W / (kms / 1e3) / 1e9
+    # e2e stream mode
+    hin = torch.randint(0, 256, (F, H, W), dtype=torch.uint8).pin_memory()
+    hout = torch.empty((F, H, W), dtype=torch.uint8).pin_memory()
+    nb, S = 16, 3
+    streams = [torch.cuda.Stream() for _ in range(S)]
+    dev_in = [torch.empty((nb, H, W), dtype=torch.uint8, device="cuda") for _ in range(S)]
+    dev_out = [torch.empty((nb, H, W), dtype=torch.uint8, device="cuda") for _ in range(S)]
+
+    def stream_pass():
+        for i, b in enumerate(range(0, F, nb)):
+            st = streams[i % S]
+            with torch.cuda.stream(st):
+                dev_in[i % S].copy_(hin[b:b + nb], non_blocking=True)
+                sobel_frames(dev_in[i % S], out=dev_out[i % S], stream=st)
+                hout[b:b + nb].copy_(dev_out[i % S], non_blocking=True)
+        for st in streams:
+            st.synchronize()
+
+    stream_pass()
+    t0 = time.perf_counter()
+    stream_pass()
+    e2e_s = time.perf_counter() - t0
+    cpu, cores, sample = _sobel_cpu() if rank == 0 else (None, None, None)
+    line = _base(args, "frames/s", "frames/s", F * world / (ms / 1e3), ms, "u8",
+                 f"C2 Sobel over {F_all} synthetic 2048x2048 uint8 frames (batches of {B})",
+                 {"frames": F_all, "parallelism": f"frames split over {world} GPU(s)",
+                  "l2": f"{F * H * W * 2 / 1e9:.1f} GB per step > L2"})
+    line["n_gpus"] = world
+    line.update({
+        "gpu_launches": args.steps * (F // B),
+        "e2e": {"value": F * world / e2e_s, "unit": "frames/s",
+                "h2d_bytes_per_step": F * H * W, "d2h_bytes_per_step": F * H * W,
+                "mode": "pinned host frames, H2D/kernel/D2H overlapped on 3 streams"},
+        "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                     "frac": ach / peak, "traffic": None, "avg_kernel_ms": kms,
+                     "kernel": f"sobel_sweep batched ({B} frames/launch), 2 B/pixel",
+                     "note": "instruction-issue-bound: exact per-pixel sqrt/round path",
+                     "peak_source": pk},
+        "cpu_baseline": None if cpu is None else
+        {"value": cpu, "unit": "frames/s", "cores": cores, "kind": "port", "sample": sample},
+        "clocks": clk.summary(),
+    })
+    return line
+
+
+# ----------------------------------------------------------------------------- C3
+
+
+def _c3_input(n=4096):
+    from oracle import stencil_oracle as O
+
+    noisy, _ = O.salt_pepper(O.gradient_image(n, n), 0.5, seed=42)
+    return noisy.astype(np.uint8)
+
+
+def _restore_iter1_ms(sk, img_t, mask_t):
+    """Duration of restore iteration 1 (every flagged pixel active): CUDA events
+    around that launch (timing executor, same kernels)."""
+    from paper_1609_04567_b200.apps.denoise import RestoreConfig, _float_sum, restore_kernel
+
+    ex = sk.DeviceExecutor(1, timing=True)
+    mk = sk.Grid.from_tensor(mask_t)
+    mk.value_range = (0, 1)
+    sk.loop_stencil_reduce_d(1, restore_kernel(RestoreConfig()), sk.abs_change(), _float_sum(),
+                             sk.stop_after(1), sk.Grid.from_tensor(img_t), env=mk, executor=ex,
+                             indexed=True)
+    return ex.last_kernel_time[0] / max(ex.last_kernel_time[1], 1)
+
+
+def c3(args, ClockSampler, measured_peaks, local=0):
+    """Two-phase restoration of one 4096^2 image with 50% salt-and-pepper
+    noise: AMF detection + 100 restore iterations (the cap; bit-exact)."""
+    import torch
+
+    import paper_1609_04567_b200 as sk
+    from paper_1609_04567_b200.apps import amf_detect, restore_regularize
+    from oracle import stencil_oracle as O
+
+    noisy = _c3_input()
+    img = torch.from_numpy(noisy).cuda()
+    g = sk.Grid.from_tensor(img)
+
+    def step():
+        mask = amf_detect(g)
+        out, rep = restore_regularize(g, mask)
+        return out, rep, mask
+
+    for _ in range(args.warmup):
+        out, rep, mask = step()
+    assert rep.iterations == 100 and rep.exhausted
+    s, e = _events()
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        s.record()
+        for _ in range(args.steps):
+            out, rep, mask = step()
+        e.record()
+        torch.cuda.synchronize()
+    ms = s.elapsed_time(e) / args.steps
+    flagged = int(mask.tensor().sum().item())
+    t1 = _restore_iter1_ms(sk, img, mask.tensor())
+    # e2e: host uint8 image in, host fp64 restored image out
+    def e2e():
+        gh = sk.Grid.from_array(noisy)
+        m2 = amf_detect(gh)
+        o2, _ = restore_regularize(gh, m2)
+        return o2.to_array()
+
+    e2e()
+    t0 = time.perf_counter()
+    e2e()
+    e2e_s = time.perf_counter() - t0
+    # CPU: the port on a 1024^2 crop of the same image family, extrapolated x16
+    small = _c3_input(1024)
+    t0 = time.perf_counter()
+    m = O.amf_detect(small)
+    t_amf = time.perf_counter() - t0
+    work = small.astype(np.float64)
+    t0 = time.perf_counter()
+    for _ in range(3):
+        work = O.restore_sweep(work, m)
+    t_it = (time.perf_counter() - t0) / 3
+    cpu_s = 16 * (t_amf + 100 * t_it)
+    line = _base(args, "frames/s (denoise)", "images/s", 1e3 / ms, ms, "f64",
+                 "C3 two-phase denoise 4096x4096 uint8, 50% noise: AMF + 100 restore iterations",
+                 {"flagged": flagged, "iterations": rep.iterations})
+    line.update({
+        "gpu_launches": None,
+        "e2e": {"value": 1.0 / e2e_s, "unit": "images/s", "h2d_bytes_per_step": noisy.size,
+                "d2h_bytes_per_step": 8 * noisy.size},
+        "roofline": restore_roofline(flagged, t1),
+        "cpu_baseline": {"value": 1.0 / cpu_s, "unit": "images/s", "cores": 1, "kind": "port",
+                         "sample": "oracle AMF + 3 restore sweeps on a 1024^2 image "
+                                   "(same generator), extrapolated to 4096^2 x 100 iterations "
+                                   "(x16 pixels)"},
+        "clocks": clk.summary(),
+    })
+    line["gpu_launches"] = 2 * (args.steps)  # one persistent launch per phase per image
+    return line
+
+
+# ----------------------------------------------------------------------------- C5
+
+
+def _c5_frames(k=32):
+    from oracle import stencil_oracle as O
+
+    return [O.salt_pepper(O.synthetic_frame(1080, 1920, i), 0.1, seed=42 + i)[0].astype(np.uint8)
+            for i in range(k)]
+
+
+def c5(args, ClockSampler, measured_peaks, local=0, world=1, rank=0, width=8):
+    """Streaming video denoise: 1000 synthetic 1920x1080 frames (10% noise),
+    a farm of stencil-reduce loops (one WorkerGroup / CUDA stream per replica).
+    value: frames resident in HBM, batched AMF + farmed restores;
+    e2e: video_restore_pipeline from host uint8 frames to host fp64 frames."""
+    import torch
+
+    import paper_1609_04567_b200 as sk
+    from paper_1609_04567_b200.apps import (amf_frames, restore_regularize,
+                                            video_restore_pipeline)
+    from oracle import stencil_oracle as O
+
+    total = 1000 // world
+    distinct = _c5_frames(32)
+    dev = torch.from_numpy(np.stack(distinct)).cuda()
+    import queue
+
+    groups = [sk.WorkerGroup(1) for _ in range(width)]
+    free = queue.Queue()
+    for g in groups:
+        free.put(g)
+
+    def step(n=total):
+        masks, _ = amf_frames(dev)
+        torch.cuda.current_stream().synchronize()
+
+        def work(i):
+            g = free.get()  # one in-flight run per worker group (= CUDA stream)
+            try:
+                j = i % len(distinct)
+                mk = sk.Grid.from_tensor(masks[j])
+                mk.value_range = (0, 1)
+                o, r = restore_regularize(sk.Grid.from_tensor(dev[j]), mk, group=g)
+                return r.iterations
+            finally:
+                free.put(g)
+
+        with ThreadPoolExecutor(width) as pool:
+            its = list(pool.map(work, range(n)))
+        for g in groups:
+            g.stream.synchronize()
+        return its
+
+    for _ in range(args.warmup):
+        step(64)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            its = step()
+        torch.cuda.synchronize()
+        sec = (time.perf_counter() - t0) / args.steps
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([sec], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        sec = float(t.item())
+    # roofline: iteration 1 of frame 0 (all flagged pixels active)
+    masks, counts = amf_frames(dev[:1])
+    t1 = _restore_iter1_ms(sk, dev[0], masks[0])
+    # e2e: the reference's pipeline shape, host frames in / host frames out
+    frames = [sk.Grid.from_array(distinct[i % len(distinct)]) for i in range(min(total, 256))]
+    video_restore_pipeline(frames[:16], width=width, writer=lambda g: g.to_array())  # warm
+    got = []
+    t0 = time.perf_counter()
+    video_restore_pipeline(frames, width=width, writer=lambda g: got.append(g.to_array()))
+    e2e_s = time.perf_counter() - t0
+    line = _base(args, "frames/s (denoise)", "frames/s", total * world / sec, sec * 1e3, "f64",
+                 f"C5 video denoise 1000 synthetic 1920x1080 frames, 10% noise "
+                 f"({len(distinct)} distinct frames cycled), restore farm width {width}",
+                 {"mean_iterations": float(np.mean(its)), "farm_width": width,
+                  "parallelism": f"frames split over {world} GPU(s)"})
+    line["n_gpus"] = world
+    cpu_line = None
+    if rank == 0:
+        t0 = time.perf_counter()
+        m = O.amf_detect(distinct[0])
+        O.restore_loop(distinct[0], m)
+        cpu_line = {"value": 1.0 / (time.perf_counter() - t0), "unit": "frames/s", "cores": 1,
+                    "kind": "port", "sample": "one 1920x1080 frame: oracle AMF + restore loop "
+                                              "to convergence, single thread"}
+    line.update({
+        "gpu_launches": None,
+        "e2e": {"value": len(frames) / e2e_s, "unit": "frames/s",
+                "h2d_bytes_per_step": len(frames) * 1080 * 1920,
+                "d2h_bytes_per_step": len(frames) * 1080 * 1920 * 8,
+                "mode": f"video_restore_pipeline(width={width}) over {len(frames)} host frames"},
+        "roofline": restore_roofline(int(counts[0]), t1),
+        "cpu_baseline": cpu_line,
+        "clocks": clk.summary(),
+    })
+    line["gpu_launches"] = args.steps * (total + 1)
+    return line

@@ -154,10 +154,7 @@ AmfFn<BATCH> pick(int wmax) {
 }
 
 int grid_for(int device, const void* fn, long long tiles) {
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kTW * kTH, 0) != cudaSuccess)
-    per_sm = 4;
-  const long long slots = (long long)device_sms(device) * (per_sm > 0 ? per_sm : 1);
+  const long long slots = (long long)device_sms(device) * occupancy(fn, kTW * kTH);
   return (int)(slots < tiles ? slots : tiles);
 }
 

@@ -231,8 +231,7 @@ int setup_t(sk_run* r) {
     set_error("helmholtz: unsupported delta/reduce combination");
     return SK_ERR_UNSUPPORTED;
   }
-  int per_sm = 0;
-  SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kBlock, 0));
+  const int per_sm = occupancy(reinterpret_cast<const void*>(fn), kBlock);
   const int sms = device_sms(r->device);
   const long long cells = (long long)p.rows * p.cols;
   r->block = kBlock;
@@ -241,6 +240,8 @@ int setup_t(sk_run* r) {
   // noise (>= 64 rows when the grid is large), short enough that every SM
   // gets several chunks (dynamic balance) on small grids.
   const long long slots = (long long)sms * per_sm;
+  // ~4 chunks per resident CTA; small (L2-resident, latency-bound) grids
+  // get short chunks so every SM has several warps in flight.
   long long want_chunks = slots * 4;
   long long ch = (p.rows * (long long)r->colblocks + want_chunks - 1) / want_chunks;
   if (cells >= (1ll << 24)) ch = ch < 64 ? 64 : ch;
@@ -301,9 +302,7 @@ int launch_t(sk_run* r, const LoopCtl& L, cudaStream_t s) {
   if (persist) {
     // the persistent variant has its own register budget: size the grid to
     // what is co-resident
-    int per_sm = 0;
-    SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, r->block, 0));
-    const int slots = device_sms(r->device) * (per_sm > 0 ? per_sm : 1);
+    const int slots = device_sms(r->device) * occupancy(reinterpret_cast<const void*>(fn), r->block);
     SK_CUDA(launch_kernel(fn, r->grid < slots ? r->grid : slots, r->block, a, s, true));
   } else {
     SK_CUDA(launch_kernel(fn, r->grid, r->block, a, s, false));

@@ -37,6 +37,10 @@ const KernelOps* amf_ops();  // adaptive-median detection (sk_amf.cu)
 
 int device_sms(int device);
 
+// Resident CTAs per SM for a kernel at a block size (cached per process: the
+// driver query costs tens of microseconds and runs are created per frame).
+int occupancy(const void* fn, int block);
+
 // Plain launch, or a cooperative launch for persistent (whole-loop) kernels,
 // which guarantees every CTA is co-resident for the in-kernel grid barrier.
 template <typename A>

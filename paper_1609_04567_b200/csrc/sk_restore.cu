@@ -344,9 +344,8 @@ int setup(sk_run* r) {
   r->flagged_dev = seg + nseg;
   // partial slots for the largest possible chunk count
   r->nchunks = (int)((npix + kCh - 1) / kCh) + r->nparts;
-  int per_sm = 0;
-  SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, restore_sweep, kRB, 0));
-  const long long slots = (long long)device_sms(r->device) * (per_sm > 0 ? per_sm : 1);
+  const long long slots = (long long)device_sms(r->device) *
+                          occupancy(reinterpret_cast<const void*>(restore_sweep), kRB);
   const long long most = r->nchunks;
   r->grid = (int)(slots < most ? slots : most);
   if (r->grid < 1) r->grid = 1;

@@ -4,6 +4,7 @@
 // Maps the reference's Executor protocol (loop.py:124-137) and _drive
 // (loop.py:198-224) onto device state.  See include/stencilkit_b200.h.
 #include <cstdlib>
+#include <map>
 #include <mutex>
 #include <string>
 
@@ -32,6 +33,22 @@ int device_sms(int device) {
     cache[device] = n;
   }
   return cache[device];
+}
+
+int occupancy(const void* fn, int block) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto key = std::make_pair(fn, block);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, block, 0) != cudaSuccess || n < 1) {
+    cudaGetLastError();
+    n = 1;
+  }
+  cache[key] = n;
+  return n;
 }
 
 // Pinned, device-mapped arena for the per-run value rings (cudaHostAlloc is
@@ -186,6 +203,22 @@ int sk_run_begin(const sk_plan* plan, const void* d_src, int64_t src_pitch, cons
     default:
       set_error("sk_run_begin: unknown kernel id");
       return SK_ERR_ARG;
+  }
+  // Keep stream-ordered allocations resident between runs: with the default
+  // release threshold (0) the pool unmaps freed memory at every synchronise
+  // and the next run's setup pays for re-mapping it.
+  {
+    static std::once_flag once[64];
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess && dev >= 0 && dev < 64)
+      std::call_once(once[dev], [dev] {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+          unsigned long long thr = ~0ull;
+          cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        cudaGetLastError();
+      });
   }
   sk_run* r = new sk_run();
   r->plan = *plan;

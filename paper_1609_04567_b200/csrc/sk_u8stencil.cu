@@ -510,9 +510,8 @@ U8Fn pick(int op, int reduce, bool batch) {
 int geometry(int device, U8Fn fn, long long rows, long long cols, int nparts, const int* part_row,
              long long frames, int* colblocks, int* chunk_rows, int* part_chunk, int* nchunks,
              int* grid) {
-  int per_sm = 0;
-  SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kBlock, 0));
-  const long long slots = (long long)device_sms(device) * (per_sm > 0 ? per_sm : 1);
+  const long long slots =
+      (long long)device_sms(device) * occupancy(reinterpret_cast<const void*>(fn), kBlock);
   *colblocks = (int)((cols + 32 * kVec - 1) / (32 * kVec));  // one warp per chunk
   const long long want = slots * (kBlock / 32) * 4;
   long long ch = (rows * (long long)*colblocks * frames + want - 1) / want;
