@@ -82,6 +82,25 @@ def amf_detect(img: Grid, wmax: int = 7, *, partitions: int = 1,
     return out
 
 
+def _detect_frame(img: Grid, wmax: int, stream) -> Grid:
+    """amf_detect of one frame through the batched detector, on `stream`.
+    Same kernel and bit-exact result as amf_detect; the mask comes back as a
+    device Grid tagged with its (0, 1) range."""
+    import torch
+
+    from ..partition import _u8_from
+
+    N.require_cuda()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    with torch.cuda.stream(stream):
+        t = _u8_from(img, "amf", 0, 255, dev).reshape(1, *img.dims)
+        masks, _ = amf_frames(t, wmax, stream=stream)
+    stream.synchronize()
+    g = Grid.from_tensor(masks[0], logical_dtype=np.int64)
+    g.value_range = (0, 1)
+    return g
+
+
 def amf_frames(frames, wmax: int = 7, out=None, stream=None):
     """Batched detection over a [F, H, W] uint8 CUDA tensor (one launch).
     Returns (masks [F, H, W] uint8 0/1, flagged counts [F] int64)."""
@@ -213,7 +232,12 @@ def video_restore_pipeline(frames: Iterable, *, width: int = 1, partitions: int 
     detect_group = WorkerGroup(1)
 
     def detect_fn(img: Grid):
-        mask = amf_detect(img, wmax=cfg.amf_wmax, group=detect_group)
+        # one batched-detector launch on the stage's stream (no run object:
+        # detection is a single stencil pass), then hand the frame and its
+        # mask to the restore farm
+        if img.ndim != 2:
+            raise GridError("detection expects a 2D image")
+        mask = _detect_frame(img, cfg.amf_wmax, detect_group.stream)
         if mask_writer is not None:
             mask_writer(mask)
         return img, mask
