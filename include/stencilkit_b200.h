@@ -89,6 +89,8 @@ typedef struct sk_plan {
 } sk_plan;
 
 #define SK_FLAG_TIMING 1 /* record CUDA events around every sweep launch */
+#define SK_FLAG_FRAMES 2 /* restore: the `partitions` row blocks are independent
+                            frames, each with its own loop (video farm batch) */
 
 typedef struct sk_cond {
   int32_t kind; /* SK_COND_* */
@@ -154,6 +156,11 @@ int sk_run_combine(sk_run* run, const double* d_partials, int32_t n, const sk_co
  * whether the loop stopped and whether the cap was hit. */
 int sk_run_status(sk_run* run, int64_t* iterations, double* value, int32_t* stopped,
                   int32_t* exhausted);
+
+/* Frame-batch restore runs (SK_FLAG_FRAMES): per-frame loop outcome after
+ * sk_run_loop -- completed iterations (the frame's result is in buffer
+ * iters[f] & 1), last reduce value, cap hit.  Arrays of `partitions`. */
+int sk_run_frame_status(sk_run* run, int64_t* iterations, double* values, int32_t* exhausted);
 
 /* Sum of CUDA-event durations of all timed sweep launches (SK_FLAG_TIMING). */
 int sk_run_kernel_time(sk_run* run, double* total_ms, int64_t* launches);

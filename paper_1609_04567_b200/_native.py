@@ -20,11 +20,13 @@ SK_DELTA_NONE, SK_DELTA_ABS, SK_DELTA_SQUARE = 0, 1, 2
 SK_COND_HOST, SK_COND_LT, SK_COND_RMS_LT, SK_COND_MEAN_LT, SK_COND_ITER_GE = 0, 1, 2, 3, 4
 SK_COND_MEAN_FLAGGED_LT = 5
 SK_FLAG_TIMING = 1
+SK_FLAG_FRAMES = 2
 
 # every symbol include/stencilkit_b200.h declares
 EXPORTS = (
     "sk_last_error", "sk_abi_version", "sk_run_begin", "sk_run_launch", "sk_run_value",
     "sk_run_loop", "sk_run_result", "sk_run_value_ptr", "sk_run_combine", "sk_run_status",
+    "sk_run_frame_status",
     "sk_run_kernel_time",
     "sk_run_launches", "sk_run_destroy", "sk_verify_div_f32", "sk_sobel_frames",
     "sk_amf_frames",
@@ -99,6 +101,7 @@ def _declare(lib):
         "sk_run_value_ptr": [P, C.POINTER(P)],
         "sk_run_combine": [P, P, I32, C.POINTER(sk_cond)],
         "sk_run_status": [P, C.POINTER(I64), C.POINTER(D), C.POINTER(I32), C.POINTER(I32)],
+        "sk_run_frame_status": [P, C.POINTER(I64), C.POINTER(D), C.POINTER(I32)],
         "sk_run_kernel_time": [P, C.POINTER(D), C.POINTER(I64)],
         "sk_run_launches": [P, C.POINTER(I64)],
         "sk_run_destroy": [P],

@@ -199,6 +199,66 @@ def restore_regularize(img: Grid, noise: Grid, cfg: Optional[RestoreConfig] = No
                          env=noise, delta=abs_change(), indexed=True, group=group)
 
 
+def restore_frames(frames, masks, cfg: Optional[RestoreConfig] = None, stream=None):
+    """restore_regularize over a batch of up to 64 frames in ONE persistent
+    launch: a device-side farm of loops.  Every frame keeps its own stopping
+    test, iteration count and final value (bit-identical to restoring it
+    alone); the grid barrier of the loop ends when the last frame stops.
+
+    frames: [F, H, W] CUDA tensor (uint8 or float64); masks: [F, H, W] uint8
+    0/1 CUDA tensor (e.g. from amf_frames).  Returns (outputs, reports): F
+    float64 [H, W] device views and F LoopReports.
+    """
+    import torch
+
+    from ..loop import LoopReport
+    from ..partition import model_ledger
+
+    lib = N.require_cuda()
+    cfg = cfg or RestoreConfig()
+    if frames.dim() != 3 or masks.shape != frames.shape or not frames.is_cuda:
+        raise GridError("restore_frames expects [F, H, W] CUDA frames and masks of that shape")
+    F, H, W = frames.shape
+    if not 1 <= F <= 64:
+        raise GridError("restore_frames takes 1..64 frames per batch")
+    st = stream if stream is not None else torch.cuda.current_stream()
+    with torch.cuda.stream(st):
+        src = frames.reshape(F * H, W).to(torch.float64).contiguous()
+        env = masks.reshape(F * H, W).to(torch.uint8).contiguous()
+        bufs = [torch.empty((F * H, W), dtype=torch.float64, device=frames.device)
+                for _ in range(2)]
+        p = N.sk_plan()
+        p.kernel, p.dtype = N.SK_KERNEL_RESTORE, N.SK_F64
+        p.rows, p.cols, p.partitions = F * H, W, F
+        p.reduce_op, p.delta_op = N.SK_REDUCE_SUM, N.SK_DELTA_ABS
+        p.flags = N.SK_FLAG_FRAMES
+        p.identity = 0.0
+        p.params[0], p.params[1] = cfg.beta, cfg.phi_eps
+        h = C.c_void_p()
+        N.check(lib.sk_run_begin(C.byref(p), C.c_void_p(src.data_ptr()), W,
+                                 C.c_void_p(env.data_ptr()), W, C.c_void_p(bufs[0].data_ptr()),
+                                 C.c_void_p(bufs[1].data_ptr()), W, N.stream_handle(st),
+                                 C.byref(h)))
+        try:
+            c = N.sk_cond()
+            c.kind, c.a, c.max_iterations = N.SK_COND_MEAN_FLAGGED_LT, cfg.tol, cfg.max_iterations
+            it, val, ex = C.c_int64(), C.c_double(), C.c_int32()
+            N.check(lib.sk_run_loop(h, C.byref(c), C.byref(it), C.byref(val), C.byref(ex)))
+            its = (C.c_int64 * F)()
+            vals = (C.c_double * F)()
+            exh = (C.c_int32 * F)()
+            N.check(lib.sk_run_frame_status(h, its, vals, exh))
+        finally:
+            N.check(lib.sk_run_destroy(h))
+    outs, reps = [], []
+    for f in range(F):
+        k = int(its[f])
+        outs.append(bufs[k & 1][f * H:(f + 1) * H])
+        reps.append(LoopReport(iterations=k, final_reduce=float(vals[f]),
+                               copies=model_ledger((H, W), 1, 1, k), exhausted=bool(exh[f])))
+    return outs, reps
+
+
 # ---------------------------------------------------------------- inputs, video
 
 

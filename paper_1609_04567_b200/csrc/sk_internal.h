@@ -32,6 +32,7 @@ struct KernelOps {
 const KernelOps* helmholtz_ops();
 const KernelOps* life_ops();
 const KernelOps* restore_ops();
+int restore_frame_status(sk_run* r, long long* iters, double* values, int* exhausted);
 const KernelOps* u8_ops();   // Sobel / Life (sk_u8stencil.cu)
 const KernelOps* amf_ops();  // adaptive-median detection (sk_amf.cu)
 
@@ -106,6 +107,6 @@ struct sk_run {
   cudaStream_t cap_stream = nullptr;
 
   // kernel-specific device state (restore: flagged list, change flags)
-  void* aux[8] = {};
+  void* aux[8] = {};  // kernel-specific device allocations
   long long aux_n[8] = {};
 };

@@ -46,6 +46,17 @@ struct RestoreArgs {
   const int* part_off;        // device: list offsets per partition [nparts + 1]
   double beta, eps;
   LoopCtl L;
+  // frame batches (SK_FLAG_FRAMES): partition p is an independent frame of
+  // frame_rows rows with its own loop (stop test, iteration count, value)
+  int frame_rows;             // 0: one image (partitions are row blocks of it)
+  struct FrameStat* fstat;    // [nparts]
+};
+
+struct FrameStat {
+  long long iter;   // iterations this frame completed
+  int stop;         // its loop is over
+  int exhausted;    // cap hit without the condition
+  double value;     // last reduce value
 };
 
 // F(u) = beta * sum over the 8 ring terms, in ring order, of w * sqrt((u-v)^2 + eps).
@@ -63,14 +74,14 @@ __device__ __forceinline__ double F_eval(double u, const double (&v)[8], const d
 }
 
 __device__ double restore_pixel(const RestoreArgs& a, const double* front, long long fp, int i,
-                                int j) {
+                                int j, int rlo, int rhi) {
   double v[8], w[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     const int di = k < 3 ? -1 : (k < 5 ? 0 : 1);               // _RING order
     const int dj = k < 3 ? k - 1 : (k < 5 ? (k == 3 ? -1 : 1) : k - 6);
     const int ni = i + di, nj = j + dj;
-    const bool in = ni >= 0 && ni < a.rows && nj >= 0 && nj < a.cols;
+    const bool in = ni >= rlo && ni < rhi && nj >= 0 && nj < a.cols;
     v[k] = in ? front[(long long)ni * fp + nj] : 0.0;
     w[k] = in ? (a.mask[(long long)ni * a.mask_pitch + nj] == 1 ? 1.0 : 2.0) : 0.0;
   }
@@ -87,13 +98,74 @@ __device__ double restore_pixel(const RestoreArgs& a, const double* front, long 
   return xmul(0.5, xadd(lo, hi));
 }
 
+// Cross-frame barrier for batched restores: the last CTA folds every active
+// frame's chunk partials (same fixed order as a single-frame run), applies
+// that frame's stop test, and releases the grid; the loop ends when every
+// frame has stopped.
+__device__ long long frames_barrier(const RestoreArgs& a, long long it, double* sh) {
+  __shared__ int s_last;
+  __shared__ unsigned s_gen;
+  __shared__ int s_all;
+  const LoopCtl& L = a.L;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* genp = &L.st->gen;
+    s_gen = *genp;
+    __threadfence();
+    const unsigned prev = atomicAdd(&L.st->ticket, 1u);
+    s_last = (prev == gridDim.x - 1);
+    s_all = 1;
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    const int* pch = L.part_chunk_dev;
+    for (int p = 0; p < L.nparts; ++p) {
+      FrameStat* fs = &a.fstat[p];
+      if (fs->stop) continue;  // uniform: every thread reads the same flag
+      double t = 0.0;
+      for (int c = pch[p] + (int)threadIdx.x; c < pch[p + 1]; c += kRB) t += __ldcg(&L.partials[c]);
+      const double v = L.identity + block_reduce<kRB>(SK_REDUCE_SUM, t, sh);
+      if (threadIdx.x == 0) {
+        const int n = a.part_off[p + 1] - a.part_off[p];
+        const int c = xdiv(v, (double)(n > 1 ? n : 1)) < L.cond.a;  // restore_regularize test
+        const int capped = it >= L.cond.max_it;
+        fs->iter = it;
+        fs->value = v;
+        fs->exhausted = !c && capped;
+        fs->stop = c || capped;
+        if (!(c || capped)) s_all = 0;
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      Status* st = L.st;
+      st->iter = it;
+      st->stop = s_all;
+      st->ticket = 0;
+      st->work = 0;
+      __threadfence();
+      atomicAdd(&L.st->gen, 1u);  // release
+    }
+  } else if (threadIdx.x == 0) {
+    volatile unsigned* genp = &L.st->gen;
+    while (*genp == s_gen) __nanosleep(64);
+  }
+  __syncthreads();
+  __threadfence();
+  volatile Status* st = L.st;
+  return st->stop ? 0 : it + 1;
+}
+
+template <bool FRAMES>
 __global__ void __launch_bounds__(kRB, 6) restore_sweep(const __grid_constant__ RestoreArgs a) {
   __shared__ double sh[kRB / 32];
   __shared__ double s_delta[kCh];
   __shared__ short s_queue[kCh];
   __shared__ int s_qlen;
   __shared__ int s_chunk;
-  for (long long it = loop_enter(a.L); it != 0; it = loop_next<kRB>(a.L, it, sh)) {
+  for (long long it = loop_enter(a.L); it != 0;
+       it = FRAMES ? frames_barrier(a, it, sh) : loop_next<kRB>(a.L, it, sh)) {
   const double* front = it == 1 ? a.src : a.buf[(it - 1) & 1];
   const long long fp = it == 1 ? a.src_pitch : a.pitch;
   double* back = a.buf[it & 1];
@@ -106,6 +178,10 @@ __global__ void __launch_bounds__(kRB, 6) restore_sweep(const __grid_constant__ 
   for (int c = next_chunk(a.L, &s_chunk); c < total; c = next_chunk(a.L, &s_chunk)) {
     int p = 0;
     while (p + 1 < a.L.nparts && c >= pch[p + 1]) ++p;
+    if (FRAMES && a.fstat[p].stop) continue;  // this frame's loop is over
+    // ring reads stay inside the image (one image) or inside the frame (batch)
+    const int rlo = FRAMES ? p * a.frame_rows : 0;
+    const int rhi = FRAMES ? rlo + a.frame_rows : a.rows;
     const int e0 = a.part_off[p] + (c - pch[p]) * kCh;
     const int e1 = min(e0 + kCh, a.part_off[p + 1]);
     if (threadIdx.x == 0) s_qlen = 0;
@@ -123,7 +199,7 @@ __global__ void __launch_bounds__(kRB, 6) restore_sweep(const __grid_constant__ 
         if (!active) {
           for (int di = -1; di <= 1 && !active; ++di) {
             const int ni = i + di;
-            if (ni < 0 || ni >= a.rows) continue;
+            if (ni < rlo || ni >= rhi) continue;
             for (int dj = -1; dj <= 1; ++dj) {
               const int nj = j + dj;
               if ((di | dj) == 0 || nj < 0 || nj >= a.cols) continue;
@@ -152,7 +228,7 @@ __global__ void __launch_bounds__(kRB, 6) restore_sweep(const __grid_constant__ 
       const int pix = a.list[e0 + pos];
       const int i = pix / a.cols, j = pix - i * a.cols;
       const double old = front[(long long)i * fp + j];
-      const double nv = restore_pixel(a, front, fp, i, j);
+      const double nv = restore_pixel(a, front, fp, i, j, rlo, rhi);
       back[(long long)i * a.pitch + j] = nv;
       ccur[pix] = nv != old;
       s_delta[pos] = fabs(xsub(nv, old));
@@ -290,7 +366,7 @@ __global__ void list_bounds(const int* list, const int* n_ptr, const int* part_r
 
 namespace {
 
-enum { AUX_LIST = 0, AUX_CHG = 1, AUX_SEG = 2, AUX_OFF = 3 };
+enum { AUX_LIST = 0, AUX_CHG = 1, AUX_SEG = 2, AUX_OFF = 3, AUX_FSTAT = 4 };
 
 int setup(sk_run* r) {
   const sk_plan& p = r->plan;
@@ -340,12 +416,22 @@ int setup(sk_run* r) {
     SK_CUDA(cudaMemcpy2DAsync(r->buf[b], r->pitch * 8, r->src, r->src_pitch * 8, p.cols * 8,
                               p.rows, cudaMemcpyDeviceToDevice, s));
   r->aux[AUX_OFF] = d_off;
+  if (p.flags & SK_FLAG_FRAMES) {
+    if (p.rows % r->nparts) {
+      set_error("restore: a frame batch must stack frames of equal height");
+      return SK_ERR_ARG;
+    }
+    void* fs = nullptr;
+    SK_CUDA(cudaMallocAsync(&fs, sizeof(FrameStat) * r->nparts, s));
+    SK_CUDA(cudaMemsetAsync(fs, 0, sizeof(FrameStat) * r->nparts, s));
+    r->aux[AUX_FSTAT] = fs;
+  }
   r->part_chunk_dev = d_pch;
   r->flagged_dev = seg + nseg;
   // partial slots for the largest possible chunk count
   r->nchunks = (int)((npix + kCh - 1) / kCh) + r->nparts;
   const long long slots = (long long)device_sms(r->device) *
-                          occupancy(reinterpret_cast<const void*>(restore_sweep), kRB);
+                          occupancy(reinterpret_cast<const void*>(restore_sweep<false>), kRB);
   const long long most = r->nchunks;
   r->grid = (int)(slots < most ? slots : most);
   if (r->grid < 1) r->grid = 1;
@@ -372,12 +458,23 @@ int launch(sk_run* r, const LoopCtl& L, cudaStream_t s) {
   a.beta = r->plan.params[0];
   a.eps = r->plan.params[1];
   a.L = L;
-  SK_CUDA(launch_kernel(restore_sweep, r->grid, kRB, a, s, L.persistent != 0));
+  if (r->plan.flags & SK_FLAG_FRAMES) {
+    // a batch of independent frames: always one persistent launch
+    if (!L.persistent) {
+      set_error("restore: frame batches run as one persistent loop");
+      return SK_ERR_UNSUPPORTED;
+    }
+    a.frame_rows = (int)(r->plan.rows / r->nparts);
+    a.fstat = static_cast<FrameStat*>(r->aux[AUX_FSTAT]);
+    SK_CUDA(launch_kernel(restore_sweep<true>, r->grid, kRB, a, s, true));
+    return SK_OK;
+  }
+  SK_CUDA(launch_kernel(restore_sweep<false>, r->grid, kRB, a, s, L.persistent != 0));
   return SK_OK;
 }
 
 void teardown(sk_run* r) {
-  for (int k : {AUX_LIST, AUX_CHG, AUX_SEG})
+  for (int k : {AUX_LIST, AUX_CHG, AUX_SEG, AUX_FSTAT})
     if (r->aux[k]) cudaFreeAsync(r->aux[k], r->stream);
   r->aux[AUX_OFF] = nullptr;  // lives inside the AUX_SEG block
 }
@@ -387,5 +484,22 @@ const KernelOps kOps = {setup, launch, teardown};
 }  // namespace
 
 const KernelOps* restore_ops() { return &kOps; }
+
+int restore_frame_status(sk_run* r, long long* iters, double* values, int* exhausted) {
+  if (!(r->plan.flags & SK_FLAG_FRAMES) || !r->aux[AUX_FSTAT]) {
+    set_error("sk_run_frame_status: not a frame-batch run");
+    return SK_ERR_STATE;
+  }
+  std::vector<FrameStat> fs(r->nparts);
+  SK_CUDA(cudaMemcpyAsync(fs.data(), r->aux[AUX_FSTAT], sizeof(FrameStat) * r->nparts,
+                          cudaMemcpyDeviceToHost, r->stream));
+  SK_CUDA(cudaStreamSynchronize(r->stream));
+  for (int i = 0; i < r->nparts; ++i) {
+    iters[i] = fs[i].iter;
+    values[i] = fs[i].value;
+    exhausted[i] = fs[i].exhausted;
+  }
+  return SK_OK;
+}
 
 }  // namespace sk

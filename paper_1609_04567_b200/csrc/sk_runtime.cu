@@ -479,6 +479,16 @@ int sk_run_status(sk_run* r, int64_t* iterations, double* value, int32_t* stoppe
   return SK_OK;
 }
 
+int sk_run_frame_status(sk_run* r, int64_t* iterations, double* values, int32_t* exhausted) {
+  if (!r || !iterations || !values || !exhausted) {
+    set_error("sk_run_frame_status: null argument");
+    return SK_ERR_ARG;
+  }
+  static_assert(sizeof(long long) == sizeof(int64_t), "");
+  return restore_frame_status(r, reinterpret_cast<long long*>(iterations), values,
+                              reinterpret_cast<int*>(exhausted));
+}
+
 int sk_run_launches(sk_run* r, int64_t* launches) {
   if (!r || !launches) {
     set_error("sk_run_launches: null argument");

@@ -237,7 +237,7 @@ class Grid:
             return np.asarray(self._list).reshape(self.dims)
         if self._arr is None:
             if self._t is not None:
-                a = self._t.detach().cpu().numpy().reshape(self.dims)
+                a = _to_host(self._t).reshape(self.dims)
                 if self._ldtype is not None and a.dtype != self._ldtype:
                     a = a.astype(self._ldtype)
                 self._arr = a
@@ -307,6 +307,37 @@ class Grid:
         self._ldtype = None
         self._src = "arr"
         self.value_range = None
+
+
+_PIN_LOCK = None
+_PIN_POOL: dict = {}
+
+
+def _to_host(t) -> np.ndarray:
+    """Device tensor -> fresh numpy array through a pooled pinned staging
+    buffer (pageable copies run at a fraction of PCIe bandwidth)."""
+    import threading
+
+    torch = _torch()
+    if not t.is_cuda or t.numel() * t.element_size() < (1 << 20):
+        return t.detach().cpu().numpy()
+    global _PIN_LOCK
+    if _PIN_LOCK is None:
+        _PIN_LOCK = threading.Lock()
+    key = (t.dtype, t.numel())
+    with _PIN_LOCK:
+        free = _PIN_POOL.setdefault(key, [])
+        buf = free.pop() if free else None
+    if buf is None:
+        buf = torch.empty(t.numel(), dtype=t.dtype, pin_memory=True)
+    try:
+        src = t.detach().reshape(-1) if t.is_contiguous() else t.detach().contiguous().reshape(-1)
+        buf.copy_(src, non_blocking=True)
+        torch.cuda.current_stream(t.device).synchronize()
+        return buf.numpy().copy()
+    finally:
+        with _PIN_LOCK:
+            _PIN_POOL[key].append(buf)
 
 
 def _numpy_dtype_of(tdtype):

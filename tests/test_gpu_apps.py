@@ -176,3 +176,38 @@ def test_sobel_iterated_twice():
     ref = O.sobel(O.sobel(img))
     assert np.array_equal(out.to_array().astype(np.uint8), ref)
     assert rep.final_reduce == int(ref.astype(np.int64).sum())
+
+
+def test_restore_frames_batch_matches_single_frame_runs(golden_large):
+    """A batch of frames in one persistent launch: every frame bit-identical to
+    its own restore_regularize run (and to the reference's C5 fixtures)."""
+    import hashlib
+
+    import torch
+
+    from oracle import stencil_oracle as O
+    from paper_1609_04567_b200.apps import amf_frames, restore_frames
+
+    frames = [O.salt_pepper(O.synthetic_frame(1080, 1920, i), 0.1, seed=42 + i)[0]
+              for i in range(4)]
+    ft = torch.from_numpy(np.stack(frames).astype(np.uint8)).cuda()
+    masks, _ = amf_frames(ft)
+    outs, reps = restore_frames(ft, masks)
+    for i in range(4):
+        m = golden_large.meta[f"C5_restore_frame{i}_P8"]
+        a = outs[i].cpu().numpy()
+        assert reps[i].iterations == m["iterations"], i
+        assert hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest() == m["sha"], i
+        single, rep1 = restore_regularize(sk.Grid.from_array(frames[i]),
+                                          sk.Grid.from_tensor(masks[i]))
+        assert rep1.final_reduce == reps[i].final_reduce
+    # a mixed batch: frames that stop early stay untouched while others run
+    small = [O.salt_pepper(O.gradient_image(40, 48), lvl, seed=s)[0]
+             for lvl, s in ((0.1, 1), (0.5, 2), (0.0, 3), (0.3, 4))]
+    st = torch.from_numpy(np.stack(small).astype(np.uint8)).cuda()
+    mk, _ = amf_frames(st)
+    outs, reps = restore_frames(st, mk)
+    for i in range(4):
+        ref, ri, rv, rex = O.restore_loop(small[i], mk[i].cpu().numpy())
+        assert reps[i].iterations == ri and reps[i].exhausted == rex, i
+        assert np.array_equal(outs[i].cpu().numpy(), ref), i
