@@ -170,7 +170,7 @@ def c2(args, ClockSampler, measured_peaks, local=0, world=1, rank=0):
 
     from paper_1609_04567_b200.apps import sobel_frames
 
-    F_all, B, H, W = 512, 64, 2048, 2048
+    F_all, B, H, W = 512, 512, 2048, 2048
     F = F_all // world
     gen = torch.Generator(device="cuda").manual_seed(rank)
     frames = torch.randint(0, 256, (F, H, W), dtype=torch.uint8, device="cuda", generator=gen)

@@ -35,7 +35,23 @@ struct U8Args {
   long long* sums;
   int frames;
   int chunks_per_frame;
+  const unsigned* magic;  // -> 0x4B000000 (Sobel lane extraction)
 };
+
+__device__ const unsigned kMagicWord = 0x4B000000u;
+
+// device address of kMagicWord on the current device (cached per device)
+inline const unsigned* magic_ptr() {
+  static const unsigned* cache[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!cache[dev]) {
+    void* p = nullptr;
+    if (cudaGetSymbolAddress(&p, kMagicWord) == cudaSuccess) cache[dev] = static_cast<const unsigned*>(p);
+  }
+  return cache[dev];
+}
 
 __device__ __forceinline__ int byte_of(unsigned w, int k) {
   return (int)__byte_perm(w, 0u, 0x4440u | (unsigned)k);
@@ -258,8 +274,21 @@ __global__ void __launch_bounds__(BLOCK) u8_sweep(const __grid_constant__ U8Args
 // Each lane becomes an exact fp32 (2^23 + v, magic), n = gx^2 + gy^2 is exact
 // in fp32 (< 2^24), and cvt.rni.sat.u8 rounds half-to-even and clips to 255
 // in one instruction -- the reference's min(255, rint(sqrt(n))).
-__device__ __forceinline__ unsigned lane_lo(unsigned p) { return __byte_perm(p, 0x4B000000u, 0x7610u); }
-__device__ __forceinline__ unsigned lane_hi(unsigned p) { return __byte_perm(p, 0x4B000000u, 0x7632u); }
+// K = 0x4B000000 (the exponent bits of 2^23).  A PRMT has one immediate
+// slot; with both K and the selector constant, ptxas keeps K immediate and
+// re-materialises the selector into a register before every use (2 extra
+// moves per pixel).  K is therefore loaded from memory once (a device
+// constant), which ptxas cannot fold: the selectors become immediates and K
+// stays in one register.
+__device__ __forceinline__ unsigned lane_lo(unsigned p, unsigned K) { return __byte_perm(p, K, 0x7610u); }
+__device__ __forceinline__ unsigned lane_hi(unsigned p, unsigned K) { return __byte_perm(p, K, 0x7632u); }
+
+#ifdef SK_SOBEL_MAGIC_ROUND
+// fminf + one magic add (1.5 * 2^23 forces round-half-even to an integer in
+// the low mantissa byte) instead of cvt.rni.sat.u8: keeps the conversion off
+// the XU pipe, which MUFU.SQRT already loads with one op per pixel.
+#define SK_SOBEL_ROUND(s) __float_as_uint(__fadd_rn(fminf((s), 255.0f), 12582912.0f))
+#endif
 
 __device__ __forceinline__ unsigned sobel_byte(unsigned gxm, unsigned gym) {
   const float gx = __fsub_rn(__uint_as_float(gxm), 8389632.0f);  // (2^23 + gx') - (2^23 + 1024)
@@ -267,9 +296,13 @@ __device__ __forceinline__ unsigned sobel_byte(unsigned gxm, unsigned gym) {
   const float n = __fmaf_rn(gy, gy, __fmul_rn(gx, gx));  // exact: every term < 2^24
   float s;
   asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(s) : "f"(n));
+#ifdef SK_SOBEL_ROUND
+  return SK_SOBEL_ROUND(s);  // result in the low byte
+#else
   unsigned b;
   asm("cvt.rni.sat.u8.f32 %0, %1;" : "=r"(b) : "f"(s));
   return b;
+#endif
 }
 
 // One border pixel with the reference's rule (off-image reads = centre),
@@ -293,6 +326,8 @@ __global__ void __launch_bounds__(BLOCK) sobel_sweep(const __grid_constant__ U8A
   constexpr int U = 6;  // multiple of the 3-row feature rotation: no register moves
   constexpr unsigned FULL = 0xffffffffu;
   __shared__ double sh[BLOCK / 32];
+  unsigned K;  // 0x4B000000, opaque to the compiler (see lane_lo)
+  asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(K) : "l"(a.magic));
   const Sweep2D& g = a.g;
   for (long long it = BATCH ? 1 : loop_enter(a.L); it != 0;
        it = BATCH ? 0 : loop_next<BLOCK>(a.L, it, sh)) {
@@ -326,20 +361,23 @@ __global__ void __launch_bounds__(BLOCK) sobel_sweep(const __grid_constant__ U8A
     const int col = cb * (32 * VEC) + lane * VEC;
     const int nvalid = cols - col;
     const bool active = nvalid > 0;
-    const int lsh = (lane == 0 && col > 0 && active) ? -1 : 0;        // edge-lane scalar loads
+    // Loads are never predicated: lanes past the image width read column 0
+    // (their bytes are masked), and the rows above/below the image read row
+    // 0 / rows-1 (those output rows are recomputed by the border pass).
+    const int lcol = active ? col : 0;
+    const int lsh = (lane == 0 && lcol > 0) ? -1 : 0;  // edge-lane scalar loads
     const int rsh = (lane == 31 && nvalid > VEC) ? VEC : 0;
     const bool ledge = lane == 0, redge = lane == 31;
+    // bytes of this lane's 8 that lie inside the image (the rest store 0)
+    const unsigned mlo = nvalid >= 4 ? 0xffffffffu : (nvalid <= 0 ? 0u : 0xffffffffu >> (32 - 8 * nvalid));
+    const unsigned mhi = nvalid >= 8 ? 0xffffffffu : (nvalid <= 4 ? 0u : 0xffffffffu >> (64 - 8 * nvalid));
+    const unsigned char* pbase = front + lcol;
+    const unsigned char* plast = pbase + (long long)(rows - 1) * fp;
 
-    // Row r (may be -1 or rows: zeros; never read past the image).
-    auto fetch = [&](int r, uint2& w, unsigned& xl, unsigned& xr) {
-      w = make_uint2(0u, 0u);
-      xl = xr = 0u;
-      if (active && r >= 0 && r < rows) {
-        const unsigned char* p = front + (long long)r * fp + col;
-        w = __ldg(reinterpret_cast<const uint2*>(p));
-        xl = __ldg(p + lsh);  // lanes without a left neighbour load their own byte (unused)
-        xr = __ldg(p + rsh);
-      }
+    auto fetch = [&](const unsigned char* p, uint2& w, unsigned& xl, unsigned& xr) {
+      w = __ldg(reinterpret_cast<const uint2*>(p));
+      xl = __ldg(p + lsh);  // lanes without a left neighbour load their own byte (unused)
+      xr = __ldg(p + rsh);
     };
     auto features = [&](uint2 w, unsigned exl, unsigned exr, unsigned* S, unsigned* D) {
       const unsigned lo_prev = __shfl_up_sync(FULL, w.y, 1);
@@ -369,11 +407,11 @@ __global__ void __launch_bounds__(BLOCK) sobel_sweep(const __grid_constant__ U8A
       for (int i = 0; i < 4; ++i) {
         const unsigned gxp = Dm[i] + (Dc[i] << 1) + Dp[i];
         const unsigned gyp = Sp[i] - Sm[i] + 0x04000400u;
-        ob[2 * i] = sobel_byte(lane_lo(gxp), lane_lo(gyp));
-        ob[2 * i + 1] = sobel_byte(lane_hi(gxp), lane_hi(gyp));
+        ob[2 * i] = sobel_byte(lane_lo(gxp, K), lane_lo(gyp, K));
+        ob[2 * i + 1] = sobel_byte(lane_hi(gxp, K), lane_hi(gyp, K));
       }
-      const unsigned lo = pack4((int)ob[0], (int)ob[1], (int)ob[2], (int)ob[3]);
-      const unsigned hi = pack4((int)ob[4], (int)ob[5], (int)ob[6], (int)ob[7]);
+      const unsigned lo = pack4((int)ob[0], (int)ob[1], (int)ob[2], (int)ob[3]) & mlo;
+      const unsigned hi = pack4((int)ob[4], (int)ob[5], (int)ob[6], (int)ob[7]) & mhi;
       if (REDUCE == SK_REDUCE_MAX) {
         const unsigned m = __vmaxu4(lo, hi);
         const unsigned m2 = __vmaxu4(m, m >> 16);
@@ -391,18 +429,25 @@ __global__ void __launch_bounds__(BLOCK) sobel_sweep(const __grid_constant__ U8A
     {
       uint2 w;
       unsigned xl, xr;
-      fetch(r0 - 1, w, xl, xr);
+      fetch(r0 > 0 ? pbase + (long long)(r0 - 1) * fp : pbase, w, xl, xr);
       features(w, xl, xr, S0, D0);
-      fetch(r0, w, xl, xr);
+      fetch(pbase + (long long)r0 * fp, w, xl, xr);
       features(w, xl, xr, S1, D1);
     }
+    // next row to fetch is r0 + 1; only row r1 == rows (the chunk's last
+    // fetch) can leave the image: clamped to rows - 1
+    const unsigned char* pf = pbase + (long long)(r0 + 1) * fp;
     unsigned char* po = back + (long long)r0 * op + col;
     int r = r0;
     for (; r + U <= r1; r += U) {  // full groups: no per-row checks
       uint2 w[U];
       unsigned xl[U], xr[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) fetch(r + u + 1, w[u], xl[u], xr[u]);
+      for (int u = 0; u < U; ++u) {
+        const unsigned char* p = pf + u * fp;
+        fetch(p > plast ? plast : p, w[u], xl[u], xr[u]);
+      }
+      pf += U * fp;
       // rows r..r+5 rotate the feature sets S0/S1/S2 by renaming
       features(w[0], xl[0], xr[0], S2, D2);
       emit(S0, D0, D1, S2, D2, po, acc, accm);
@@ -427,7 +472,8 @@ __global__ void __launch_bounds__(BLOCK) sobel_sweep(const __grid_constant__ U8A
     for (; r < r1; ++r) {  // tail rows
       uint2 w;
       unsigned xl, xr;
-      fetch(r + 1, w, xl, xr);
+      fetch(pf > plast ? plast : pf, w, xl, xr);
+      pf += fp;
       features(w, xl, xr, S2, D2);
       emit(S0, D0, D1, S2, D2, po, acc, accm);
       po += op;
@@ -439,34 +485,42 @@ __global__ void __launch_bounds__(BLOCK) sobel_sweep(const __grid_constant__ U8A
         D1[i] = D2[i];
       }
     }
-    // Fix-up pass: border pixels (image rows 0 / rows-1, columns 0 / cols-1)
-    // follow the centre-substitution rule, and bytes past the image width are
-    // zero.  Each lane rewrites its own bytes, reading what it just stored.
+    // Border pass: pixels of image rows 0 / rows-1 and columns 0 / cols-1
+    // follow the centre-substitution rule.  Border rows: each lane redoes its
+    // own 8 pixels.  Border columns: the warp's lanes split the chunk's rows
+    // (the column is owned by one lane, the work is spread over all 32).
+    // Each redo corrects the lane's running sum by (new - old).
     const bool top = r0 == 0, bottom = r1 == rows;
-    const bool lcol = active && col == 0, rcol = active && nvalid <= VEC;
-    if (active && (top || bottom || lcol || rcol)) {
-      auto redo = [&](int rr, int k) {
-        unsigned char* q = back + (long long)rr * op + col + k;
+    const int c_first = cb * (32 * VEC);
+    const bool has_c0 = cb == 0;                                        // column 0 here
+    const bool has_cl = cols - 1 >= c_first && cols - 1 < c_first + 32 * VEC;  // column cols-1
+    if (top || bottom || has_c0 || has_cl) {
+      __syncwarp();  // the owners' stores are visible to the lanes that redo them
+      auto redo = [&](int rr, int cc2) {
+        unsigned char* q = back + (long long)rr * op + cc2;
         const unsigned old = *q;
-        const unsigned nv = k < nvalid ? sobel_border_px(front, fp, rr, col + k, rows, cols) : 0u;
+        const unsigned nv = sobel_border_px(front, fp, rr, cc2, rows, cols);
         *q = (unsigned char)nv;
         acc += nv - old;
       };
-      for (int rr = r0; rr < r1; ++rr) {
-        if ((top && rr == 0) || (bottom && rr == rows - 1)) {
-          for (int k = 0; k < VEC; ++k) redo(rr, k);
-        } else {
-          if (lcol) redo(rr, 0);
-          if (rcol) {
-            for (int k = nvalid - 1; k < VEC; ++k) redo(rr, k);
-          }
-        }
+      if (active) {
+        const int kmax = nvalid < VEC ? nvalid : VEC;
+        if (top) for (int k = 0; k < kmax; ++k) redo(0, col + k);
+        if (bottom && !(top && rows == 1)) for (int k = 0; k < kmax; ++k) redo(rows - 1, col + k);
       }
-      if (REDUCE == SK_REDUCE_MAX) {  // rare: recompute this lane's max from what it stored
+      const int ra = top ? 1 : r0, rb = bottom ? rows - 1 : r1;  // rows not yet redone
+      for (int rr = ra + lane; rr < rb; rr += 32) {
+        if (has_c0) redo(rr, 0);
+        if (has_cl && cols > 1) redo(rr, cols - 1);
+      }
+      __syncwarp();
+      if (REDUCE == SK_REDUCE_MAX) {  // rare: recompute this lane's max from what was stored
+        __syncwarp();
         accm = -1;
-        for (int rr = r0; rr < r1; ++rr)
-          for (int k = 0; k < VEC && k < nvalid; ++k)
-            accm = max(accm, (int)back[(long long)rr * op + col + k]);
+        if (active)
+          for (int rr = r0; rr < r1; ++rr)
+            for (int k = 0; k < VEC && k < nvalid; ++k)
+              accm = max(accm, (int)back[(long long)rr * op + col + k]);
       }
     }
     double v;
@@ -476,7 +530,7 @@ __global__ void __launch_bounds__(BLOCK) sobel_sweep(const __grid_constant__ U8A
       for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(FULL, m, o));
       v = m < 0 ? -INFINITY : (double)m;
     } else {
-      v = (double)__reduce_add_sync(FULL, active ? acc : 0u);
+      v = (double)__reduce_add_sync(FULL, acc);  // border redos may sit on any lane
     }
     if (lane == 0) {
       if (BATCH) atomicAdd(reinterpret_cast<unsigned long long*>(&a.sums[frame]),
@@ -513,7 +567,10 @@ int geometry(int device, U8Fn fn, long long rows, long long cols, int nparts, co
   const long long slots =
       (long long)device_sms(device) * occupancy(reinterpret_cast<const void*>(fn), kBlock);
   *colblocks = (int)((cols + 32 * kVec - 1) / (32 * kVec));  // one warp per chunk
-  const long long want = slots * (kBlock / 32) * 4;
+#ifndef SK_U8_CHUNKS_PER_WARP
+#define SK_U8_CHUNKS_PER_WARP 8
+#endif
+  const long long want = slots * (kBlock / 32) * SK_U8_CHUNKS_PER_WARP;
   long long ch = (rows * (long long)*colblocks * frames + want - 1) / want;
   ch = ch < 8 ? 8 : (ch > 256 ? 256 : ch);
   ch = (ch + 11) / 12 * 12;  // whole prefetch groups (Life: 4 rows, Sobel: 6)
@@ -566,6 +623,7 @@ void fill_geom(const sk_run* r, Sweep2D& g) {
 
 int launch(sk_run* r, const LoopCtl& L, cudaStream_t s) {
   U8Args a{};
+  a.magic = magic_ptr();
   fill_geom(r, a.g);
   a.L = L;
   U8Fn fn = pick(op_of(r), r->plan.reduce_op, false);
@@ -596,6 +654,7 @@ int sobel_frames(const uint8_t* in, long long in_pitch, long long in_fs, uint8_t
   SK_CUDA(cudaGetDevice(&dev));
   U8Fn fn = pick(U8_SOBEL, SK_REDUCE_SUM, true);
   U8Args a{};
+  a.magic = magic_ptr();
   int part_row[2] = {0, (int)rows};
   int nch = 0, grid = 0;
   int rc = geometry(dev, fn, rows, cols, 1, part_row, frames, &a.g.colblocks, &a.g.chunk_rows,
