@@ -19,7 +19,16 @@
 #ifndef STENCILKIT_B200_H
 #define STENCILKIT_B200_H
 
+#ifndef __CUDACC_RTC__
 #include <stdint.h>
+#else /* NVRTC (user elemental kernels, sk_jit_*) */
+typedef signed char int8_t;
+typedef int int32_t;
+typedef long long int64_t;
+typedef unsigned char uint8_t;
+typedef unsigned int uint32_t;
+typedef unsigned long long uint64_t;
+#endif
 
 #ifdef __cplusplus
 extern "C" {
@@ -47,11 +56,13 @@ extern "C" {
 #define SK_KERNEL_AMF 3       /* params: wmax; u8 in, u8 0/1 out          */
 #define SK_KERNEL_RESTORE 4   /* params: beta, phi_eps; f64 work, u8 mask */
 #define SK_KERNEL_LIFE 5      /* u8 0/1 board                             */
+#define SK_KERNEL_JIT 6       /* user elemental function (sk_jit_compile)  */
 
 /* Combinator kinds (patterns.py:195-211) and Delta kinds
  * (apps/helmholtz.py:98-100, apps/denoise.py:252-254) */
 #define SK_REDUCE_SUM 1
 #define SK_REDUCE_MAX 2
+#define SK_REDUCE_CUSTOM 3 /* JIT kernels: the combinator compiled into the program */
 #define SK_DELTA_NONE 0
 #define SK_DELTA_ABS 1
 #define SK_DELTA_SQUARE 2
@@ -102,6 +113,7 @@ typedef struct sk_cond {
 
 typedef struct sk_run sk_run;
 
+#ifndef __CUDACC_RTC__ /* device programs (NVRTC) need only the constants and types above */
 const char* sk_last_error(void);
 int sk_abi_version(void);
 
@@ -191,6 +203,43 @@ int sk_sobel_frames(const uint8_t* d_in, int64_t in_pitch, int64_t in_frame_stri
 int sk_amf_frames(const uint8_t* d_in, int64_t in_pitch, int64_t in_frame_stride, uint8_t* d_mask,
                   int64_t mask_pitch, int64_t mask_frame_stride, int32_t frames, int64_t rows,
                   int64_t cols, int32_t wmax, int64_t* d_counts, void* stream);
+
+/* ---- user elemental functions (run-time compiled) -----------------------
+ * The paper's API passes the elemental function, combinator and delta as
+ * kernel source; the reference package passes Python
+ * callables (ElementalFn.point, patterns.py:41-68; Combinator/Delta
+ * patterns.py:85-122).  paper_1609_04567_b200/jit.py renders either as one
+ * CUDA program against csrc/sk_jit_prelude.cuh; sk_jit_compile builds it
+ * with NVRTC for sm_100a (no GPU needed) and keeps the cubin; the kernel is
+ * loaded per device when a run starts. */
+typedef struct sk_jit sk_jit;
+
+int sk_jit_compile(const char* source, const char* name, sk_jit** out);
+/* NVRTC log of the compile (owned by the program; may be empty) */
+const char* sk_jit_log(const sk_jit* program);
+int64_t sk_jit_cubin_size(const sk_jit* program);
+int sk_jit_destroy(sk_jit* program);
+
+/* Executor.begin for a compiled elemental (plan->kernel = SK_KERNEL_JIT,
+ * reduce_op SUM / MAX / CUSTOM).  d_src is the input grid (element type of
+ * the program's sk_in_t), d_buf0/1 the iteration buffers (sk_val_t); d_env
+ * holds n_env (0..4) read-only grids aligned with the loop grid, each with
+ * its own pitch in elements.  Other calls as for sk_run_begin. */
+int sk_run_begin_jit(const sk_plan* plan, const sk_jit* program, const void* d_src,
+                     int64_t src_pitch, const void* const* d_env, const int64_t* env_pitch,
+                     int32_t n_env, void* d_buf0, void* d_buf1, int64_t pitch, void* stream,
+                     sk_run** out);
+
+/* First elemental failure of a JIT run (the reference raises StencilError,
+ * patterns.py:29-38): code 0 = none, 1 = ABSENT used as a number
+ * (TypeError), 2 = division by zero, 3 = math domain error, 4 = int() of
+ * inf/nan, 5 = returned None, 6 = env index off the grid (GridError),
+ * 7 = window offset beyond the radius (IndexError), 8 = int ** negative int;
+ * index = row-major element index (lowest failing); iteration = the failing
+ * iteration.  A failed iteration's ring value (sk_run_value) is NaN and the
+ * loop stops there. */
+int sk_run_error(sk_run* run, int32_t* code, int64_t* index, int64_t* iteration);
+#endif /* __CUDACC_RTC__ */
 
 #ifdef __cplusplus
 }

@@ -28,7 +28,19 @@ SOURCES = [
     "sk_amf.cu",
     "sk_restore.cu",
     "sk_dispatch.cu",
+    "sk_jit.cu",
 ]
+
+# Headers NVRTC compiles user elemental programs against (embedded in the
+# library, see sk_jit.cu), with the include names the sources use.
+JIT_HEADERS = [
+    ("../../include/stencilkit_b200.h", os.path.join(ROOT, "include", "stencilkit_b200.h")),
+    ("sk_common.cuh", os.path.join(CSRC, "sk_common.cuh")),
+    ("sk_sweep.cuh", os.path.join(CSRC, "sk_sweep.cuh")),
+    ("sk_jit_prelude.cuh", os.path.join(CSRC, "sk_jit_prelude.cuh")),
+    ("sk_jit_kernel.cuh", os.path.join(CSRC, "sk_jit_kernel.cuh")),
+]
+GEN = os.path.join(LIBDIR, "gen")
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -38,7 +50,31 @@ NVCC_FLAGS = [
     "-fmad=false",
     "-Xcompiler", "-fPIC,-O2",
     "-Xptxas", "-v",
+    "-ldl",
 ]
+
+
+def write_jit_headers() -> str:
+    """Render JIT_HEADERS as C string tables (sk_jit_headers.inc)."""
+    os.makedirs(GEN, exist_ok=True)
+    names, srcs = [], []
+    for name, path in JIT_HEADERS:
+        with open(path) as fh:
+            text = fh.read()
+        delim = "SKJIT"
+        assert f"){delim}\"" not in text
+        names.append(f'"{name}"')
+        # split into <= 8 KB raw-string pieces (compiler literal limits)
+        parts = [text[i:i + 8000] for i in range(0, len(text), 8000)] or [""]
+        srcs.append("\n".join(f'R"{delim}({p}){delim}"' for p in parts))
+    out = os.path.join(GEN, "sk_jit_headers.inc")
+    body = (f"static const int kJitHeaderCount = {len(names)};\n"
+            f"static const char* const kJitHeaderNames[] = {{{', '.join(names)}}};\n"
+            f"static const char* const kJitHeaderSrcs[] = {{\n" + ",\n".join(srcs) + "};\n")
+    if not os.path.exists(out) or open(out).read() != body:
+        with open(out, "w") as fh:
+            fh.write(body)
+    return out
 
 
 def nvcc() -> str:
@@ -67,8 +103,9 @@ def build(verbose: bool = False, force: bool = False) -> str:
     if not force and not needs_build():
         return out
     os.makedirs(LIBDIR, exist_ok=True)
+    write_jit_headers()
     tmp = out + ".tmp"
-    cmd = [nvcc(), *NVCC_FLAGS, "-shared", "-o", tmp,
+    cmd = [nvcc(), *NVCC_FLAGS, "-I", GEN, "-shared", "-o", tmp,
            *[os.path.join(CSRC, s) for s in SOURCES]]
     res = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
     if res.returncode != 0:

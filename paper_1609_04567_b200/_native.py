@@ -15,7 +15,8 @@ from . import _build
 SK_OK, SK_ERR_ARG, SK_ERR_CUDA, SK_ERR_STATE, SK_ERR_UNSUPPORTED = 0, 1, 2, 3, 4
 SK_U8, SK_F32, SK_F64 = 1, 3, 4
 SK_KERNEL_HELMHOLTZ, SK_KERNEL_SOBEL, SK_KERNEL_AMF, SK_KERNEL_RESTORE, SK_KERNEL_LIFE = 1, 2, 3, 4, 5
-SK_REDUCE_SUM, SK_REDUCE_MAX = 1, 2
+SK_KERNEL_JIT = 6
+SK_REDUCE_SUM, SK_REDUCE_MAX, SK_REDUCE_CUSTOM = 1, 2, 3
 SK_DELTA_NONE, SK_DELTA_ABS, SK_DELTA_SQUARE = 0, 1, 2
 SK_COND_HOST, SK_COND_LT, SK_COND_RMS_LT, SK_COND_MEAN_LT, SK_COND_ITER_GE = 0, 1, 2, 3, 4
 SK_COND_MEAN_FLAGGED_LT = 5
@@ -29,7 +30,8 @@ EXPORTS = (
     "sk_run_frame_status",
     "sk_run_kernel_time",
     "sk_run_launches", "sk_run_destroy", "sk_verify_div_f32", "sk_sobel_frames",
-    "sk_amf_frames",
+    "sk_amf_frames", "sk_jit_compile", "sk_jit_log", "sk_jit_cubin_size", "sk_jit_destroy",
+    "sk_run_begin_jit", "sk_run_error",
 )
 
 
@@ -107,7 +109,16 @@ def _declare(lib):
         "sk_run_destroy": [P],
         "sk_sobel_frames": [P, I64, I64, P, I64, I64, I32, I64, I64, P, P],
         "sk_amf_frames": [P, I64, I64, P, I64, I64, I32, I64, I64, I32, P, P],
+        "sk_jit_compile": [C.c_char_p, C.c_char_p, C.POINTER(P)],
+        "sk_jit_destroy": [P],
+        "sk_run_begin_jit": [C.POINTER(sk_plan), P, P, I64, C.POINTER(P), C.POINTER(I64), I32, P, P,
+                             I64, P, C.POINTER(P)],
+        "sk_run_error": [P, C.POINTER(I32), C.POINTER(I64), C.POINTER(I64)],
     }
+    lib.sk_jit_log.argtypes = [P]
+    lib.sk_jit_log.restype = C.c_char_p
+    lib.sk_jit_cubin_size.argtypes = [P]
+    lib.sk_jit_cubin_size.restype = C.c_int64
     lib.sk_verify_div_f32.argtypes = [C.c_float, P]
     lib.sk_verify_div_f32.restype = C.c_longlong
     for name, args in sig.items():

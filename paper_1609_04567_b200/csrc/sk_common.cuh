@@ -10,9 +10,18 @@
 // per iteration, or one CUDA-graph launch for the whole loop).
 #pragma once
 
+#ifndef __CUDACC_RTC__
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <math.h>
+#else
+// Compiled by NVRTC as part of a user elemental kernel (sk_jit.cu): no host
+// headers.  Device graphs are never used by JIT kernels.
+typedef unsigned long long cudaGraphConditionalHandle;
+#ifndef INFINITY
+#define INFINITY __int_as_float(0x7f800000)
+#endif
+#endif
 
 #include "../../include/stencilkit_b200.h"
 
@@ -35,6 +44,10 @@ struct Status {
   long long gdecided;   // iterations the cross-rank combine has evaluated
   unsigned int gen;     // grid-barrier generation (persistent loops)
   unsigned int pad3;
+  // first elemental failure of the run (JIT kernels): ~((index << 8) | code),
+  // 0 = none; atomicMax keeps the lowest row-major index
+  unsigned long long err;
+  long long err_iter;   // iteration whose fold first saw `err` (0 = none)
 };
 
 constexpr int kMaxParts = 64;
@@ -103,11 +116,13 @@ __device__ __forceinline__ bool div_safe(double x) {
   const double a = fabs(x);
   return a >= 0x1p-500 && a < 0x1p500;
 }
+#ifndef __CUDACC_RTC__
 // host: is b inside the range where div_const is valid for div_safe(x)?
 inline bool div_b_ok(double b, bool f32) {
   const double a = b < 0 ? -b : b;
   return f32 ? (a >= 0x1p-30 && a <= 0x1p30) : (a >= 0x1p-200 && a <= 0x1p200);
 }
+#endif
 
 __device__ __forceinline__ float tabs(float x) { return fabsf(x); }
 __device__ __forceinline__ double tabs(double x) { return fabs(x); }
@@ -179,7 +194,9 @@ __device__ __forceinline__ long long loop_enter(const LoopCtl& L) {
   if (st->stop) {
     // a graph WHILE body entered after the loop ended must still clear the
     // condition, or the graph would spin
+#ifndef __CUDACC_RTC__
     if (L.use_graph && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(L.gh, 0u);
+#endif
     return 0;
   }
   return st->iter + 1;
@@ -195,57 +212,90 @@ __device__ __forceinline__ int next_chunk(const LoopCtl& L, int* s_chunk) {
   return *s_chunk;
 }
 
+// The engine's own reduce ops (SUM / MAX, patterns.py:195-211).  JIT
+// kernels pass their user combinator instead (same interface).
+struct OpCombine {
+  int op;
+  __device__ __forceinline__ double operator()(double a, double b) const { return rcombine(op, a, b); }
+  // fold of the partition values from the identity (the reference's host
+  // combine: `acc + v` / `a if b < a else b`, partition.py:642-646)
+  __device__ __forceinline__ double fold(double acc, double v) const {
+    return op == SK_REDUCE_SUM ? acc + v : ((v < acc) ? acc : v);
+  }
+  __device__ __forceinline__ double neutral(double) const { return rneutral(op); }
+};
+
+template <int BLOCK, class Comb>
+__device__ __forceinline__ double block_reduce_c(const Comb& comb, double neutral, double v, double* sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = comb(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  double r = neutral;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int w = 0; w < BLOCK / 32; ++w) r = comb(r, sh[w]);
+  }
+  __syncthreads();
+  return r;  // valid in thread 0
+}
+
 // Fold + decide, run by all threads of the last CTA to finish an iteration:
 // chunk partials per partition (fixed strided split + fixed tree), then
 // partitions in ascending order from the identity (partition.py:642-646),
 // then the loop condition (loop.py:209-218).  Publishes the iteration;
-// returns the stop decision (valid in every thread).
-template <int BLOCK>
-__device__ __noinline__ int fold_and_decide(const LoopCtl& L, long long it, double* sh) {
+// returns the stop decision (valid in every thread).  A recorded elemental
+// failure (Status::err) stops the loop as well.
+template <int BLOCK, class Comb>
+__device__ __noinline__ int fold_and_decide(const LoopCtl& L, long long it, double* sh, const Comb comb) {
   __shared__ int s_stop;
-  const int op = L.reduce;
   double acc = L.identity;
+  const double neutral = comb.neutral(L.identity);
   for (int p = 0; p < L.nparts; ++p) {
     const int c0 = L.part_chunk_dev ? L.part_chunk_dev[p] : L.part_chunk[p];
     const int c1 = L.part_chunk_dev ? L.part_chunk_dev[p + 1] : L.part_chunk[p + 1];
-    double v;
-    if (op == SK_REDUCE_SUM) {
-      double t = 0.0;
-      for (int c = c0 + (int)threadIdx.x; c < c1; c += BLOCK) t += __ldcg(&L.partials[c]);
-      v = block_reduce<BLOCK>(op, t, sh);
-    } else {
-      double t = -INFINITY;
-      for (int c = c0 + (int)threadIdx.x; c < c1; c += BLOCK) t = rmax(t, __ldcg(&L.partials[c]));
-      v = block_reduce<BLOCK>(op, t, sh);
-    }
-    if (threadIdx.x == 0) {
-      if (op == SK_REDUCE_SUM) acc = acc + v;
-      else acc = (v < acc) ? acc : v;  // max_combinator fold (patterns.py:205-211)
-    }
+    double t = neutral;
+    for (int c = c0 + (int)threadIdx.x; c < c1; c += BLOCK) t = comb(t, __ldcg(&L.partials[c]));
+    const double v = block_reduce_c<BLOCK>(comb, neutral, t, sh);
+    if (threadIdx.x == 0) acc = comb.fold(acc, v);
   }
   if (threadIdx.x == 0) {
     Status* st = L.st;
-    const int c = eval_cond(L.cond, acc, it, L.flagged_dev);
+    const int failed = *(volatile unsigned long long*)&st->err != 0ull;
+    const int c = failed ? 0 : eval_cond(L.cond, acc, it, L.flagged_dev);
     const int capped = (it >= L.cond.max_it);
     st->value = acc;
     st->cond_true = c;
-    st->exhausted = (!c && capped);
-    st->stop = c || capped;
+    st->exhausted = (!c && capped && !failed);
+    st->stop = c || capped || failed;
     st->iter = it;
     st->ticket = 0;
     st->work = 0;
-    if (L.ring) L.ring[it % kRing] = acc;
-    s_stop = c || capped;
+    if (failed && st->err_iter == 0) st->err_iter = it;
+    // a failed iteration publishes NaN: the host then asks sk_run_error
+    if (L.ring) L.ring[it % kRing] = failed ? __longlong_as_double(0x7ff8000000000000ll) : acc;
+    s_stop = c || capped || failed;
   }
   __syncthreads();
   return s_stop;
 }
 
+template <int BLOCK>
+__device__ __forceinline__ int fold_and_decide(const LoopCtl& L, long long it, double* sh) {
+  return fold_and_decide<BLOCK>(L, it, sh, OpCombine{L.reduce});
+}
+
+// OpCombine defaults carry no op: take the run's reduce op from the LoopCtl.
+__device__ __forceinline__ OpCombine pick_comb(const LoopCtl& L, const OpCombine&) { return OpCombine{L.reduce}; }
+template <class Comb>
+__device__ __forceinline__ const Comb& pick_comb(const LoopCtl&, const Comb& c) { return c; }
+
 // End of a launched iteration (one launch per iteration, or a graph WHILE
 // body): every CTA arrives; the last one folds, decides and -- in graph
 // mode -- clears the WHILE condition.
-template <int BLOCK>
-__device__ void loop_finalize(const LoopCtl& L, long long it, double* sh) {
+template <int BLOCK, class Comb = OpCombine>
+__device__ void loop_finalize(const LoopCtl& L, long long it, double* sh, const Comb comb = Comb{0}) {
   __shared__ int s_last;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -256,10 +306,12 @@ __device__ void loop_finalize(const LoopCtl& L, long long it, double* sh) {
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  const int stop = fold_and_decide<BLOCK>(L, it, sh);
+  const int stop = fold_and_decide<BLOCK>(L, it, sh, pick_comb(L, comb));
   if (threadIdx.x == 0) {
     __threadfence_system();
+#ifndef __CUDACC_RTC__
     if (L.use_graph) cudaGraphSetConditional(L.gh, stop ? 0u : 1u);
+#endif
   }
 }
 
@@ -269,8 +321,8 @@ __device__ void loop_finalize(const LoopCtl& L, long long it, double* sh) {
 // next sweep reads what every CTA just wrote) and the loop test.  The
 // gpu-scope fences on both sides also invalidate L1, so the next sweep's
 // read-only loads see the fresh buffer.  Returns the next iteration or 0.
-template <int BLOCK>
-__device__ long long loop_barrier(const LoopCtl& L, long long it, double* sh) {
+template <int BLOCK, class Comb = OpCombine>
+__device__ long long loop_barrier(const LoopCtl& L, long long it, double* sh, const Comb comb = Comb{0}) {
   __shared__ int s_last;
   __shared__ unsigned s_gen;
   __syncthreads();
@@ -284,7 +336,7 @@ __device__ long long loop_barrier(const LoopCtl& L, long long it, double* sh) {
   __syncthreads();
   if (s_last) {
     __threadfence();
-    fold_and_decide<BLOCK>(L, it, sh);
+    fold_and_decide<BLOCK>(L, it, sh, pick_comb(L, comb));
     if (threadIdx.x == 0) {
       __threadfence();
       atomicAdd(&L.st->gen, 1u);  // release

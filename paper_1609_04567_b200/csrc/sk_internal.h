@@ -8,6 +8,7 @@
 #include "sk_common.cuh"
 
 struct sk_run;
+struct sk_jit;
 
 namespace sk {
 
@@ -35,6 +36,13 @@ const KernelOps* restore_ops();
 int restore_frame_status(sk_run* r, long long* iters, double* values, int* exhausted);
 const KernelOps* u8_ops();   // Sobel / Life (sk_u8stencil.cu)
 const KernelOps* amf_ops();  // adaptive-median detection (sk_amf.cu)
+const KernelOps* jit_ops();  // user elemental functions (sk_jit.cu)
+
+// shared body of sk_run_begin / sk_run_begin_jit
+int begin_impl(const sk_plan* plan, const sk_jit* jit, const void* d_src, int64_t src_pitch,
+               const void* d_env, int64_t env_pitch, const void* const* jit_env,
+               const int64_t* jit_env_pitch, int n_env, void* d_buf0, void* d_buf1, int64_t pitch,
+               void* stream, sk_run** out);
 
 int device_sms(int device);
 
@@ -105,6 +113,13 @@ struct sk_run {
   // device-loop graph
   cudaGraphExec_t gexec = nullptr;
   cudaStream_t cap_stream = nullptr;
+
+  // user elemental kernel (SK_KERNEL_JIT)
+  const sk_jit* jit = nullptr;
+  const void* jit_env[4] = {};
+  long long jit_env_pitch[4] = {};
+  int jit_nenv = 0;
+  bool no_graph = false;  // the kernel cannot drive a graph WHILE node
 
   // kernel-specific device state (restore: flagged list, change flags)
   void* aux[8] = {};  // kernel-specific device allocations

@@ -176,6 +176,18 @@ int sk_abi_version(void) { return SK_ABI_VERSION; }
 int sk_run_begin(const sk_plan* plan, const void* d_src, int64_t src_pitch, const void* d_env,
                  int64_t env_pitch, void* d_buf0, void* d_buf1, int64_t pitch, void* stream,
                  sk_run** out) {
+  return sk::begin_impl(plan, nullptr, d_src, src_pitch, d_env, env_pitch, nullptr, nullptr, 0, d_buf0,
+                        d_buf1, pitch, stream, out);
+}
+
+}  // extern "C"
+
+namespace sk {
+
+int begin_impl(const sk_plan* plan, const sk_jit* jit, const void* d_src, int64_t src_pitch,
+               const void* d_env, int64_t env_pitch, const void* const* jit_env,
+               const int64_t* jit_env_pitch, int n_env, void* d_buf0, void* d_buf1, int64_t pitch,
+               void* stream, sk_run** out) {
   if (!plan || !out || !d_buf0 || !d_buf1 || !d_src) {
     set_error("sk_run_begin: null argument");
     return SK_ERR_ARG;
@@ -189,12 +201,22 @@ int sk_run_begin(const sk_plan* plan, const void* d_src, int64_t src_pitch, cons
     set_error("sk_run_begin: partitions must be in [1, min(rows, 64)]");
     return SK_ERR_ARG;
   }
-  if (plan->reduce_op != SK_REDUCE_SUM && plan->reduce_op != SK_REDUCE_MAX) {
+  if (plan->reduce_op != SK_REDUCE_SUM && plan->reduce_op != SK_REDUCE_MAX &&
+      !(jit && plan->reduce_op == SK_REDUCE_CUSTOM)) {
     set_error("sk_run_begin: unknown reduce op");
+    return SK_ERR_ARG;
+  }
+  if ((plan->kernel == SK_KERNEL_JIT) != (jit != nullptr)) {
+    set_error("sk_run_begin: user elemental kernels start with sk_run_begin_jit");
+    return SK_ERR_ARG;
+  }
+  if (n_env < 0 || n_env > 4 || (n_env > 0 && (!jit_env || !jit_env_pitch))) {
+    set_error("sk_run_begin_jit: 0..4 env grids");
     return SK_ERR_ARG;
   }
   const KernelOps* ops = nullptr;
   switch (plan->kernel) {
+    case SK_KERNEL_JIT: ops = jit_ops(); break;
     case SK_KERNEL_HELMHOLTZ: ops = helmholtz_ops(); break;
     case SK_KERNEL_LIFE: ops = life_ops(); break;
     case SK_KERNEL_RESTORE: ops = restore_ops(); break;
@@ -232,6 +254,13 @@ int sk_run_begin(const sk_plan* plan, const void* d_src, int64_t src_pitch, cons
   r->buf[1] = d_buf1;
   r->pitch = pitch;
   r->timing = (plan->flags & SK_FLAG_TIMING) != 0;
+  r->jit = jit;
+  r->jit_nenv = n_env;
+  for (int i = 0; i < n_env; ++i) {
+    r->jit_env[i] = jit_env[i];
+    r->jit_env_pitch[i] = jit_env_pitch[i];
+  }
+  r->no_graph = jit != nullptr;  // JIT kernels never set a graph condition
   int rc = SK_OK;
   cudaError_t ce = cudaGetDevice(&r->device);
   if (ce != cudaSuccess) {
@@ -275,6 +304,10 @@ int sk_run_begin(const sk_plan* plan, const void* d_src, int64_t src_pitch, cons
   return SK_OK;
 }
 
+}  // namespace sk
+
+extern "C" {
+
 int sk_run_launch(sk_run* r, int32_t n) {
   if (!r || n < 0) {
     set_error("sk_run_launch: bad argument");
@@ -313,7 +346,7 @@ int sk_run_loop(sk_run* r, const sk_cond* c, int64_t* iterations, double* final_
   // conditional graph nodes)
   const char* ng = getenv("SK_NO_GRAPH");
   const char* np = getenv("SK_NO_PERSIST");
-  bool use_graph = !r->timing && !(ng && ng[0] == '1');
+  bool use_graph = !r->timing && !r->no_graph && !(ng && ng[0] == '1');
   bool persistent = !r->timing && !(np && np[0] == '1');
   if (persistent) {
     // One cooperative launch runs every iteration (in-kernel grid barrier

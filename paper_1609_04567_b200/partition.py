@@ -37,7 +37,9 @@ from . import _native as N
 from .grid import Grid, GridError
 from .ledger import CopyLedger
 from .loop import Executor, LoopPlan, LoopState, _as_plan, _drive
-from .patterns import (Combinator, DeviceUnsupported, _check_env, combinator_kind, delta_kind)
+from .jit import JitKernel, build_program
+from .patterns import (Combinator, DeviceUnsupported, StencilError, _check_env, combinator_kind,
+                       delta_kind)
 
 
 class DeploymentMode(Enum):
@@ -175,6 +177,21 @@ def _torch():
     return torch
 
 
+class _TorchDtypes(dict):
+    def __missing__(self, key):
+        torch = _torch()
+        table = {np.dtype(np.bool_): torch.bool, np.dtype(np.int8): torch.int8,
+                 np.dtype(np.uint8): torch.uint8, np.dtype(np.int16): torch.int16,
+                 np.dtype(np.uint16): torch.uint16, np.dtype(np.int32): torch.int32,
+                 np.dtype(np.uint32): torch.uint32, np.dtype(np.int64): torch.int64,
+                 np.dtype(np.float32): torch.float32, np.dtype(np.float64): torch.float64}
+        self.update(table)
+        return table[np.dtype(key)]
+
+
+_TORCH_DT = _TorchDtypes()
+
+
 @dataclass
 class _DevRun:
     plan: LoopPlan
@@ -195,6 +212,7 @@ class _DevRun:
     launched: int = 0     # iterations enqueued on the device
     committed: Optional[int] = None
     released: bool = False
+    jit: Any = None       # jit.Program of a user elemental
 
 
 def _u8_from(grid: Grid, what: str, lo: int, hi: int, dev):
@@ -272,17 +290,20 @@ class DeviceExecutor(Executor):
         plan, grid = _adapt(plan, grid)
         _check_env(plan.env, grid.dims)
         dk = plan.fn.device if hasattr(plan.fn, "device") else None
-        if dk is None:
-            raise DeviceUnsupported(
-                "elemental function has no device kernel; the engine runs only its "
-                "sm_100a kernels (helmholtz, sobel, amf, restore, life)")
         if grid.ndim != 2:
             raise DeviceUnsupported("device kernels run on 2D grids")
         rows, cols = grid.dims
         P = self.partitions
         _check_partitioning(rows, P, plan.k)
-        reduce = combinator_kind(plan.op)
-        delta = delta_kind(plan.delta)
+        prog = None
+        if dk is None or isinstance(dk, JitKernel):
+            # a user elemental: compiled for the device at run time (jit.py);
+            # raises DeviceUnsupported if it cannot be translated
+            prog = build_program(plan, grid)
+            reduce = delta = None
+        else:
+            reduce = combinator_kind(plan.op)
+            delta = delta_kind(plan.delta)
         group = self._group
         owns = group is None
         stream = group.stream if group is not None else torch.cuda.current_stream()
@@ -290,12 +311,76 @@ class DeviceExecutor(Executor):
             group.start_run()
         try:
             with torch.cuda.stream(stream):
+                if prog is not None:
+                    return self._begin_jit(lib, plan, grid, prog, rows, cols, P, stream, group, owns)
                 return self._begin_on(lib, plan, grid, dk, rows, cols, P, reduce, delta,
                                       stream, group, owns)
         except BaseException:
             if group is not None:
                 group.end_run()
             raise
+
+    def _begin_jit(self, lib, plan, grid, prog, rows, cols, P, stream, group, owns):
+        torch = _torch()
+        dev = torch.device("cuda", torch.cuda.current_device())
+        tin = _TORCH_DT[prog.in_dtype]
+        src = grid.tensor(device=dev)
+        if src.dtype != tin:
+            src = src.to(tin)
+        src = src.reshape(rows, cols).contiguous()
+        env_grids = plan.env if isinstance(plan.env, tuple) else (
+            (plan.env,) if isinstance(plan.env, Grid) else ())
+        envs = []
+        for g, edt in zip(env_grids, prog.env_dtypes):
+            t = g.tensor(device=dev)
+            if t.dtype != _TORCH_DT[edt]:
+                t = t.to(_TORCH_DT[edt])
+            envs.append(t.reshape(rows, cols).contiguous())
+        tout = _TORCH_DT[prog.out_dtype]
+        bufs = [torch.empty((rows, cols), dtype=tout, device=dev) for _ in range(2)]
+        p = N.sk_plan()
+        p.kernel = N.SK_KERNEL_JIT
+        p.dtype = 0
+        p.rows, p.cols = rows, cols
+        p.partitions = P
+        p.reduce_op = prog.reduce
+        p.delta_op = N.SK_DELTA_NONE
+        p.halo_top = p.halo_bottom = 0
+        p.flags = N.SK_FLAG_TIMING if self.timing else 0
+        ident = plan.op.identity
+        p.identity = float(ident) if isinstance(ident, (int, float, bool, np.number)) else 0.0
+        n = len(envs)
+        eptr = (C.c_void_p * 4)(*[C.c_void_p(t.data_ptr()) for t in envs])
+        epitch = (C.c_int64 * 4)(*[t.stride(0) for t in envs])
+        h = C.c_void_p()
+        N.check(lib.sk_run_begin_jit(C.byref(p), prog.handle, C.c_void_p(src.data_ptr()),
+                                     src.stride(0), eptr, epitch, n,
+                                     C.c_void_p(bufs[0].data_ptr()), C.c_void_p(bufs[1].data_ptr()),
+                                     cols, N.stream_handle(stream), C.byref(h)))
+        return _DevRun(plan=plan, dims=(rows, cols), P=P, handle=h, bufs=bufs, src=src,
+                       env=envs, pitch=cols, cols=cols, out_dtype=prog.out_dtype,
+                       int_value=prog.int_value, stream=stream, group=group, owns_group=owns,
+                       jit=prog)
+
+    def _raise_if_failed(self, run: "_DevRun", upto: Optional[int] = None) -> None:
+        """A recorded elemental failure becomes the reference's StencilError
+        (partition.py:357-360, 638-641) for the lowest failing index."""
+        if run.jit is None:
+            return
+        lib = N.load()
+        code, index, it = C.c_int32(), C.c_int64(), C.c_int64()
+        N.check(lib.sk_run_error(run.handle, C.byref(code), C.byref(index), C.byref(it)))
+        if code.value == 0 or (upto is not None and it.value > upto):
+            return
+        from .jit import error_cause
+
+        i, j = divmod(index.value, run.cols)
+        part = None
+        if run.P > 1:
+            for pi, (lo, hi) in enumerate(_split_ranges(run.dims[0], run.P)):
+                if lo <= i < hi:
+                    part = pi
+        raise StencilError((i, j), error_cause(code.value), partition=part)
 
     def _begin_on(self, lib, plan, grid, dk, rows, cols, P, reduce, delta, stream, group, owns):
         torch = _torch()
@@ -401,6 +486,8 @@ class DeviceExecutor(Executor):
             run.launched += 1
         v = C.c_double()
         N.check(lib.sk_run_value(run.handle, t, C.byref(v)))
+        if run.jit is not None and v.value != v.value:  # NaN: maybe a failed iteration
+            self._raise_if_failed(run, upto=t)
         run.steps = t
         return self._value(run, v.value)
 
@@ -420,6 +507,7 @@ class DeviceExecutor(Executor):
         c.max_iterations = cond.max_iterations
         it, val, ex = C.c_int64(), C.c_double(), C.c_int32()
         N.check(lib.sk_run_loop(run.handle, C.byref(c), C.byref(it), C.byref(val), C.byref(ex)))
+        self._raise_if_failed(run)
         run.steps = run.launched = it.value
         return it.value, self._value(run, val.value), bool(ex.value)
 
@@ -444,7 +532,7 @@ class DeviceExecutor(Executor):
             out = out.contiguous()
         led = model_ledger(run.dims, run.P, run.plan.k, it)
         g = Grid.from_tensor(out, logical_dtype=run.out_dtype)
-        g.value_range = _OUT_RANGE.get(run.plan.fn.device.name)
+        g.value_range = _OUT_RANGE.get(getattr(run.plan.fn.device, "name", None))
         return g, led
 
     def abort(self, run: _DevRun) -> None:
