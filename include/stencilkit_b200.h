@@ -218,6 +218,8 @@ int sk_jit_compile(const char* source, const char* name, sk_jit** out);
 /* NVRTC log of the compile (owned by the program; may be empty) */
 const char* sk_jit_log(const sk_jit* program);
 int64_t sk_jit_cubin_size(const sk_jit* program);
+/* copy the sm_100a cubin (sk_jit_cubin_size bytes) -- for cuobjdump / caching */
+int sk_jit_cubin(const sk_jit* program, void* dst);
 int sk_jit_destroy(sk_jit* program);
 
 /* Executor.begin for a compiled elemental (plan->kernel = SK_KERNEL_JIT,

@@ -20,6 +20,7 @@ from .patterns import (Combinator, Delta, DeviceKernel, DeviceUnsupported, Eleme
                        reduce_all, reduce_pattern, sq_change, stencil_apply,
                        stencil_apply_indexed, sum_combinator)
 
+from .jit import CudaCombine, CudaDelta, cuda_elemental
 from .streams import (OrderedFarm, Pipeline, Stage, StreamError, StreamReport, ordered_farm,
                       pipeline, run_stream)
 

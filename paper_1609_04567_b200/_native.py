@@ -30,7 +30,7 @@ EXPORTS = (
     "sk_run_frame_status",
     "sk_run_kernel_time",
     "sk_run_launches", "sk_run_destroy", "sk_verify_div_f32", "sk_sobel_frames",
-    "sk_amf_frames", "sk_jit_compile", "sk_jit_log", "sk_jit_cubin_size", "sk_jit_destroy",
+    "sk_amf_frames", "sk_jit_compile", "sk_jit_log", "sk_jit_cubin_size", "sk_jit_cubin", "sk_jit_destroy",
     "sk_run_begin_jit", "sk_run_error",
 )
 
@@ -111,6 +111,7 @@ def _declare(lib):
         "sk_amf_frames": [P, I64, I64, P, I64, I64, I32, I64, I64, I32, P, P],
         "sk_jit_compile": [C.c_char_p, C.c_char_p, C.POINTER(P)],
         "sk_jit_destroy": [P],
+        "sk_jit_cubin": [P, P],
         "sk_run_begin_jit": [C.POINTER(sk_plan), P, P, I64, C.POINTER(P), C.POINTER(I64), I32, P, P,
                              I64, P, C.POINTER(P)],
         "sk_run_error": [P, C.POINTER(I32), C.POINTER(I64), C.POINTER(I64)],

@@ -156,7 +156,7 @@ int jit_function(sk_jit* j, int dev, CUfunction* fn) {
   return SK_OK;
 }
 
-constexpr int kTW = 128, kTH = 16;  // sk_jit_kernel.cuh tile
+constexpr int kTW = 128;  // sk_jit_kernel.cuh tile width; rows per tile = plan.params[0]
 
 int jit_setup(sk_run* r) {
   sk_jit* j = const_cast<sk_jit*>(r->jit);
@@ -169,12 +169,21 @@ int jit_setup(sk_run* r) {
   if (rc) return rc;
   r->block = j->block;
   r->colblocks = (int)((r->plan.cols + kTW - 1) / kTW);
-  r->chunk_rows = kTH;
+  const int kTH = r->plan.params[0] >= 1 ? (int)r->plan.params[0] : 16;  // the program's SK_TH
+  // chunk = a run of tiles: as tall as possible (<= 8 tiles) while leaving
+  // ~4 chunks per resident CTA for balance
+  {
+    const long long slots = (long long)device_sms(r->device) * j->occ[r->device];
+    const long long tiles = ((r->plan.rows + kTH - 1) / kTH) * r->colblocks;
+    long long m = tiles / (4 * slots);
+    m = m < 1 ? 1 : (m > 8 ? 8 : m);
+    r->chunk_rows = (int)(kTH * m);
+  }
   int n = 0;
   r->part_chunk[0] = 0;
   for (int i = 0; i < r->nparts; ++i) {
     const int pr = r->part_row[i + 1] - r->part_row[i];
-    n += ((pr + kTH - 1) / kTH) * r->colblocks;
+    n += ((pr + r->chunk_rows - 1) / r->chunk_rows) * r->colblocks;
     r->part_chunk[i + 1] = n;
   }
   r->nchunks = n;
@@ -292,6 +301,15 @@ int sk_jit_compile(const char* source, const char* name, sk_jit** out) {
 const char* sk_jit_log(const sk_jit* j) { return j ? j->log.c_str() : ""; }
 
 int64_t sk_jit_cubin_size(const sk_jit* j) { return j ? (int64_t)j->cubin.size() : 0; }
+
+int sk_jit_cubin(const sk_jit* j, void* dst) {
+  if (!j || !dst) {
+    set_error("sk_jit_cubin: null argument");
+    return SK_ERR_ARG;
+  }
+  memcpy(dst, j->cubin.data(), j->cubin.size());
+  return SK_OK;
+}
 
 int sk_jit_destroy(sk_jit* j) {
   if (!j) return SK_OK;

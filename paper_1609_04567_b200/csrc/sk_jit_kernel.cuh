@@ -11,22 +11,34 @@
 // wide the stencil.  Tiles never span a partition, and each tile writes its
 // own reduce partial (deterministic fold, independent of scheduling).
 //
-// Required from the generated part: sk_in_t, sk_val_t, SK_K, SK_PAD_EDGE,
-// SK_PAD_VALUE, sk_elemental_1/_n, sk_delta_1/_n, struct SkComb.
+// Required from the generated part: sk_in_t, sk_val_t, sk_delta_t, SK_K,
+// SK_PAD_EDGE, SK_PAD_VALUE, sk_elemental_1/_n, sk_delta_1/_n, struct SkComb;
+// optional SK_LOCAL_MAX (the combinator is the engine's max: each thread
+// keeps its running max in sk_delta_t and converts it once).
 #pragma once
 
 
 #ifndef SK_BLOCK
 #define SK_BLOCK 256
 #endif
+#ifndef SK_MINB
+#define SK_MINB 1
+#endif
 #define SK_TW 128
-#define SK_TH 16
+#ifndef SK_TH
+#define SK_TH 16  // rows per tile (jit.py may pick 8 for wide windows)
+#endif
 
 namespace sk {
 
 constexpr int kJitTWP = SK_TW + 2 * SK_K;
 constexpr int kJitTileElems = (SK_TH + 2 * SK_K) * kJitTWP;
 constexpr int kJitElemMax = sizeof(sk_in_t) > sizeof(sk_val_t) ? sizeof(sk_in_t) : sizeof(sk_val_t);
+
+template <class T>
+__device__ __forceinline__ T jit_lmax(T a, T b) {  // NaN-propagating, as rmax
+  return (a != a) ? a : ((b != b) ? b : (b > a ? b : a));
+}
 
 __device__ __forceinline__ void jit_fail(Status* st, long long index, int code) {
   atomicMax(&st->err, ~(((unsigned long long)index << 8) | (unsigned)code));
@@ -36,29 +48,76 @@ __device__ __forceinline__ void jit_fail(Status* st, long long index, int code) 
 // front into the tile: off-grid slots take the pad value ("constant") or the
 // nearest border element ("edge"), like the reference's context assembly
 // (partition.py:278-288, 551-581).
+// one element global -> shared: 4/8-byte elements with cp.async (no register
+// round trip, every load of the tile in flight at once), others by value
 template <class V>
-__device__ __forceinline__ void jit_stage(V* tile, const V* front, long long fp, int r0, int nr,
-                                          int c0, int rows, int cols) {
-  const int n = (nr + 2 * SK_K) * kJitTWP;
-  for (int idx = threadIdx.x; idx < n; idx += SK_BLOCK) {
-    const int tr = idx / kJitTWP, tc = idx - tr * kJitTWP;
-    int gi = r0 - SK_K + tr, gj = c0 - SK_K + tc;
-    V v;
-#if SK_PAD_EDGE
-    gi = gi < 0 ? 0 : (gi >= rows ? rows - 1 : gi);
-    gj = gj < 0 ? 0 : (gj >= cols ? cols - 1 : gj);
-    v = front[(long long)gi * fp + gj];
-#else
-    const bool in = (unsigned)gi < (unsigned)rows && (unsigned)gj < (unsigned)cols;
-    v = in ? front[(long long)gi * fp + gj] : (V)(SK_PAD_VALUE);
-#endif
-    tile[idx] = v;
+__device__ __forceinline__ void stage_one(V* dst, const V* src) {
+  if constexpr (sizeof(V) == 4 || sizeof(V) == 8) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(d), "l"(src), "n"((int)sizeof(V)));
+  } else {
+    *dst = *src;
   }
 }
 
+template <class V>
+__device__ __forceinline__ void jit_stage(V* tile, const V* front, long long fp, int r0, int nr,
+                                          int c0, int rows, int cols) {
+  const int tx = threadIdx.x % SK_TW, ty = threadIdx.x / SK_TW;
+  const int nrow = nr + 2 * SK_K;
+  const bool inner = r0 - SK_K >= 0 && r0 + nr + SK_K <= rows && c0 - SK_K >= 0 &&
+                     c0 + SK_TW + SK_K <= cols;
+  if (inner) {  // the whole window frame lies on the grid: plain copies
+    const V* p = front + (long long)(r0 - SK_K) * fp + (c0 - SK_K);
+#pragma unroll 4
+    for (int tr = ty; tr < nrow; tr += SK_BLOCK / SK_TW) {
+      const V* rp = p + (long long)tr * fp;
+      V* tp = tile + tr * kJitTWP;
+#pragma unroll
+      for (int tc = tx; tc < kJitTWP; tc += SK_TW) stage_one(tp + tc, rp + tc);
+    }
+  } else {
+    for (int tr = ty; tr < nrow; tr += SK_BLOCK / SK_TW) {
+      int gi = r0 - SK_K + tr;
+      const bool rin = (unsigned)gi < (unsigned)rows;
+#if SK_PAD_EDGE
+      gi = gi < 0 ? 0 : (gi >= rows ? rows - 1 : gi);
+#endif
+      const V* rp = front + (long long)gi * fp;
+      V* tp = tile + tr * kJitTWP;
+#pragma unroll
+      for (int tc = tx; tc < kJitTWP; tc += SK_TW) {
+        int gj = c0 - SK_K + tc;
+#if SK_PAD_EDGE
+        gj = gj < 0 ? 0 : (gj >= cols ? cols - 1 : gj);
+        stage_one(tp + tc, rp + gj);
+#else
+        if (rin && (unsigned)gj < (unsigned)cols) stage_one(tp + tc, rp + gj);
+        else tp[tc] = (V)(SK_PAD_VALUE);
+#endif
+      }
+    }
+  }
+  if constexpr (sizeof(V) == 4 || sizeof(V) == 8)
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+
+// wait until at most `pending` staged tiles are still in flight
+template <class V>
+__device__ __forceinline__ void stage_wait_upto(int pending) {
+  if constexpr (sizeof(V) == 4 || sizeof(V) == 8) {
+    if (pending) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    else asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  }
+}
+
+// A work chunk = one column block x chunk_rows rows = a run of SK_TH-row
+// tiles.  Tiles are double-buffered: while tile t is computed, tile t+1 is
+// already on its way into the other buffer (cp.async), so each CTA keeps
+// its loads in flight.  One reduce partial per chunk.
 template <class V, bool FIRST>
-__device__ __forceinline__ double jit_sweep(const JitArgs& a, long long it, V* tile, int* s_chunk,
-                                            double* sh, const SkComb& comb) {
+__device__ __forceinline__ void jit_sweep(const JitArgs& a, long long it, V* tiles, int* s_chunk,
+                                          double* sh, const SkComb& comb) {
   const Sweep2D& g = a.g;
   const V* front = static_cast<const V*>(FIRST ? g.src : g.buf[(it - 1) & 1]);
   const long long fp = FIRST ? g.src_pitch : g.pitch;
@@ -70,50 +129,73 @@ __device__ __forceinline__ double jit_sweep(const JitArgs& a, long long it, V* t
   for (int c = next_chunk(a.L, s_chunk); c < total; c = next_chunk(a.L, s_chunk)) {
     int cb, r0, r1;
     chunk_geom(a.L, g, c, &cb, &r0, &r1);
-    const int c0 = cb * SK_TW, nr = r1 - r0;
-    jit_stage<V>(tile, front, fp, r0, nr, c0, rows, cols);
-    __syncthreads();
+    const int c0 = cb * SK_TW;
     double acc = neutral;
+#ifdef SK_LOCAL_MAX
+    sk_delta_t lmax = 0;
+    bool lany = false;
+#endif
     const int gj = c0 + tx;
-    if (gj < cols) {
-      for (int lr = ty; lr < nr; lr += SK_BLOCK / SK_TW) {
-        const int gi = r0 + lr;
-        SkNb<V> nb;
-        nb.c = tile + (lr + SK_K) * kJitTWP + tx + SK_K;
-        nb.stride = kJitTWP;
-        nb.i = gi;
-        nb.j = gj;
-        nb.rows = rows;
-        nb.cols = cols;
-        nb.k = SK_K;
-        SkErr err;
-        sk_val_t nw;
-        double d;
-        if (FIRST) {
-          nw = sk_elemental_1(nb, a.env, err);
-          d = sk_delta_1(nw, nb.center(), err);
-        } else {
-          nw = sk_elemental_n(nb, a.env, err);
-          d = sk_delta_n(nw, nb.center(), err);
+    int buf = 0;
+    jit_stage<V>(tiles, front, fp, r0, min(SK_TH, r1 - r0), c0, rows, cols);
+    for (int t0 = r0; t0 < r1; t0 += SK_TH) {
+      const int nr = min(SK_TH, r1 - t0);
+      const bool more = t0 + SK_TH < r1;
+      if (more)
+        jit_stage<V>(tiles + (buf ^ 1) * kJitTileElems, front, fp, t0 + SK_TH,
+                     min(SK_TH, r1 - t0 - SK_TH), c0, rows, cols);
+      stage_wait_upto<V>(more ? 1 : 0);
+      __syncthreads();
+      const V* tile = tiles + buf * kJitTileElems;
+      if (gj < cols) {
+        for (int lr = ty; lr < nr; lr += SK_BLOCK / SK_TW) {
+          const int gi = t0 + lr;
+          SkNb<V> nb;
+          nb.c = tile + (lr + SK_K) * kJitTWP + tx + SK_K;
+          nb.stride = kJitTWP;
+          nb.i = gi;
+          nb.j = gj;
+          nb.rows = rows;
+          nb.cols = cols;
+          nb.k = SK_K;
+          SkErr err;
+          sk_val_t nw;
+          sk_delta_t d;
+          if (FIRST) {
+            nw = sk_elemental_1(nb, a.env, err);
+            d = sk_delta_1(nw, nb.center(), err);
+          } else {
+            nw = sk_elemental_n(nb, a.env, err);
+            d = sk_delta_n(nw, nb.center(), err);
+          }
+          back[(long long)gi * g.pitch + gj] = nw;
+          if (err.code) jit_fail(a.L.st, (long long)gi * cols + gj, err.code);
+#ifdef SK_LOCAL_MAX
+          lmax = lany ? jit_lmax(lmax, d) : d;
+          lany = true;
+#else
+          acc = comb(acc, (double)d);
+#endif
         }
-        back[(long long)gi * g.pitch + gj] = nw;
-        if (err.code) jit_fail(a.L.st, (long long)gi * cols + gj, err.code);
-        acc = comb(acc, d);
       }
+      __syncthreads();  // tile `buf` is free for the tile after next
+      buf ^= 1;
     }
+#ifdef SK_LOCAL_MAX
+    if (lany) acc = comb(acc, (double)lmax);
+#endif
     const double v = block_reduce_c<SK_BLOCK>(comb, neutral, acc, sh);
     if (threadIdx.x == 0) a.L.partials[c] = v;
   }
-  return 0.0;
 }
 
 }  // namespace sk
 
-extern "C" __global__ void __launch_bounds__(SK_BLOCK) sk_jit_sweep(const __grid_constant__ sk::JitArgs a) {
+extern "C" __global__ void __launch_bounds__(SK_BLOCK, SK_MINB) sk_jit_sweep(const __grid_constant__ sk::JitArgs a) {
   using namespace sk;
   __shared__ double sh[SK_BLOCK / 32];
   __shared__ int s_chunk;
-  __shared__ __align__(16) unsigned char s_tile[kJitTileElems * kJitElemMax];
+  __shared__ __align__(16) unsigned char s_tile[2 * kJitTileElems * kJitElemMax];  // 2 tile buffers
   const SkComb comb{};
   long long it = loop_enter(a.L);
   if (it == 0) return;

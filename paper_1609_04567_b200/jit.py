@@ -40,6 +40,7 @@ import ctypes as C
 import inspect
 import linecache
 import math
+import os
 import threading
 from dataclasses import dataclass, field
 from typing import Any, Optional
@@ -52,7 +53,10 @@ from .patterns import DeviceUnsupported
 # ----------------------------------------------------------------------------- types
 
 BOOL, INT, F32, F64 = "bool", "int", "f32", "f64"
-_RANK = {BOOL: 0, INT: 1, F32: 2, F64: 3}
+# join order: a numpy float32 value meeting a Python float (F64 here is always
+# a Python float: f64 grids hold Python floats, as in the reference's list
+# Grid) stays float32 (NEP 50), so F32 ranks above F64
+_RANK = {BOOL: 0, INT: 1, F64: 2, F32: 3}
 CTYPE = {BOOL: "bool", INT: "long long", F32: "float", F64: "double"}
 NP_OF = {BOOL: np.dtype(np.bool_), INT: np.dtype(np.int64), F32: np.dtype(np.float32),
          F64: np.dtype(np.float64)}
@@ -272,10 +276,12 @@ class Translator:
     Types are inferred by re-running the translation until every local's type
     is stable (a join over its assignments); the final pass emits code."""
 
-    def __init__(self, fn, params: list, role: str, win: Optional[WindowSpec] = None):
+    def __init__(self, fn, params: list, role: str, win: Optional[WindowSpec] = None,
+                 ctx: Optional["HelperCtx"] = None):
         self.fn = fn
-        self.role = role  # 'elemental' | 'delta' | 'combine'
+        self.role = role  # 'elemental' | 'delta' | 'combine' | 'helper'
         self.win = win
+        self.ctx = ctx if ctx is not None else HelperCtx()
         self.node = _func_node(fn)
         self.params = params  # list of (name -> Val) in order, for non-window roles
         try:
@@ -328,6 +334,9 @@ class Translator:
         node = self.node
         args = [a.arg for a in node.args.args]
         self.local_vals = {}
+        if node.args.vararg or node.args.kwarg or node.args.kwonlyargs or node.args.defaults:
+            raise TranslateError(f"{getattr(self.fn, '__qualname__', self.fn)}: only plain "
+                                 "positional parameters are supported")
         if self.role == "elemental":
             if len(args) != 2:
                 raise TranslateError("an elemental function takes (nb, env)")
@@ -977,7 +986,48 @@ class Translator:
                 return num(self.truth(args[0], e), BOOL) if args else const_val(False)
             nums = [self.present(a, e) for a in args]
             return self._numeric_call(fo, name, mod, nums, e)
+        if inspect.isfunction(fo):
+            if self.role in ("delta", "combine"):
+                self.fail(e, "deltas and combinators cannot call other Python functions")
+            return self._helper_call(fo, args, e)
         self.fail(e, f"call of {getattr(fo, '__qualname__', fo)!r} is not supported on the device")
+
+    def _helper_call(self, fo, args, e):
+        """A call of another plain Python function: translated once per
+        argument signature into its own __device__ function (which receives
+        the window, env and error state too, so it may use them)."""
+        sig, cparams, cargs, pvals = [], [], [], []
+        for i, a in enumerate(args):
+            if a.kind == "num":
+                sig.append(("num", a.t, a.ok is not None))
+                cparams.append(f"{CTYPE[a.t]} p{i}")
+                cargs.append(a.c)
+                ok = None
+                if a.ok is not None:
+                    cparams.append(f"bool p{i}_ok")
+                    cargs.append(a.ok)
+                    ok = f"p{i}_ok"
+                pvals.append(num(f"p{i}", a.t, ok=ok))
+            elif a.kind in ("nb", "env", "envgrid", "absent", "none"):
+                sig.append((a.kind, a.slot))
+                pvals.append(a)
+            elif a.kind == "obj":
+                sig.append(("obj", id(a.obj)))
+                pvals.append(a)
+            elif a.kind == "tuple" and all(x.kind == "num" and x.ok is None for x in a.items) \
+                    and a.ok is None:
+                sig.append(("tuple", tuple(x.t for x in a.items)))
+                items = []
+                for j, x in enumerate(a.items):
+                    cparams.append(f"{CTYPE[x.t]} p{i}_{j}")
+                    cargs.append(x.c)
+                    items.append(num(f"p{i}_{j}", x.t))
+                pvals.append(Val("tuple", items=tuple(items)))
+            else:
+                self.fail(e, f"cannot pass a {a.kind} to {fo.__qualname__}")
+        win_t = (self.win.in_c, self.win.in_t) if self.win is not None else None
+        name, ret_t = self.ctx.helper(fo, tuple(sig), win_t, cparams, pvals, self.win)
+        return num(f"{name}(nb, env, err{''.join(', ' + c for c in cargs)})", ret_t)
 
     def _numeric_call(self, fo, name, mod, a, e):
         def f64(v):
@@ -1226,6 +1276,40 @@ _PYOPS = {ast.Add: _op.add, ast.Sub: _op.sub, ast.Mult: _op.mul, ast.BitAnd: _op
           ast.BitOr: _op.or_, ast.BitXor: _op.xor, ast.LShift: _op.lshift, ast.RShift: _op.rshift}
 
 
+class HelperCtx:
+    """Helper functions called by the translated code, shared by every
+    translation of one program (emitted before their callers)."""
+
+    def __init__(self):
+        self.funcs = {}      # key -> (name, ret type)
+        self.sources = []    # C definitions in dependency order
+        self.active = set()
+
+    def helper(self, fo, sig, win_t, cparams, pvals, win):
+        key = (fo.__code__, sig, win_t)
+        if key in self.funcs:
+            return self.funcs[key]
+        if key in self.active:
+            raise TranslateError(f"recursive call of {fo.__qualname__} is not supported")
+        self.active.add(key)
+        try:
+            tr = Translator(fo, pvals, "helper", win, ctx=self)
+            body, ret_t = tr.translate()
+        finally:
+            self.active.discard(key)
+        import re
+
+        name = f"sk_h{len(self.funcs)}_" + re.sub(r"\W", "_", fo.__name__)
+        rt = CTYPE[ret_t]
+        head = ", ".join(["const NBT& nb", "const SkEnv& env", "SkErr& err"] + cparams)
+        src = [f"template <class NBT>", f"__device__ {rt} {name}({head}) {{"]
+        src += [ln.replace("RET_T", rt) for ln in body]
+        src.append("}")
+        self.sources.append("\n".join(src))
+        self.funcs[key] = (name, ret_t)
+        return name, ret_t
+
+
 @dataclass(frozen=True)
 class _NbMethod:
     name: str
@@ -1297,6 +1381,7 @@ class Program:
     env_dtypes: tuple
     reduce: int
     int_value: bool
+    tile_rows: int = 16
 
 
 _prog_lock = threading.Lock()
@@ -1319,6 +1404,15 @@ def compile_source(source: str) -> C.c_void_p:
         return h
 
 
+def cubin_of(prog: "Program") -> bytes:
+    """The program's sm_100a cubin (inspect with cuobjdump -sass)."""
+    lib = N.load()
+    n = lib.sk_jit_cubin_size(prog.handle)
+    buf = C.create_string_buffer(n)
+    N.check(lib.sk_jit_cubin(prog.handle, buf))
+    return buf.raw
+
+
 def _reduce_parts(op, delta, val_t: str, in_t: str, val_c: str, in_c: str):
     """C definitions of sk_delta_1/_n and SkComb, the reduce id, int-ness."""
     from .patterns import combinator_kind
@@ -1326,24 +1420,28 @@ def _reduce_parts(op, delta, val_t: str, in_t: str, val_c: str, in_c: str):
     lines = []
     dt = None
     if delta is None:
-        for suffix, ot in (("1", in_c), ("n", val_c)):
-            lines.append(f"__device__ __forceinline__ double sk_delta_{suffix}(sk_val_t nw, {ot} old, SkErr& err) "
-                         f"{{ return (double)nw; }}")
         dt = val_t
+        for suffix, ot in (("1", in_c), ("n", val_c)):
+            lines.append(f"__device__ __forceinline__ sk_delta_t sk_delta_{suffix}(sk_val_t nw, {ot} old, SkErr& err) "
+                         f"{{ return (sk_delta_t)nw; }}")
     elif isinstance(getattr(delta, "fn", None), CudaDelta) or isinstance(delta, CudaDelta):
         body = (delta if isinstance(delta, CudaDelta) else delta.fn).body
-        for suffix, ot in (("1", in_c), ("n", val_c)):
-            lines.append(f"__device__ __forceinline__ double sk_delta_{suffix}(sk_val_t nw, {ot} old, SkErr& err) "
-                         f"{{ {body} }}")
         dt = F64
+        for suffix, ot in (("1", in_c), ("n", val_c)):
+            lines.append(f"__device__ __forceinline__ sk_delta_t sk_delta_{suffix}(sk_val_t nw, {ot} old, SkErr& err) "
+                         f"{{ {body} }}")
     else:
+        bodies = []
         for suffix, ot, os_ in (("1", in_t, in_c), ("n", val_t, val_c)):
             tr = Translator(delta.fn, [num("nw", val_t), num(f"(({CTYPE[ot]})old)", ot)], "delta")
             body, rt = tr.translate()
-            dt = rt
-            lines.append(f"__device__ __forceinline__ double sk_delta_{suffix}(sk_val_t nw, {os_} old, SkErr& err) {{")
-            lines += [ln.replace("RET_T", "double") for ln in body]
+            dt = _join(dt, rt)
+            bodies.append((suffix, os_, body))
+        for suffix, os_, body in bodies:
+            lines.append(f"__device__ __forceinline__ sk_delta_t sk_delta_{suffix}(sk_val_t nw, {os_} old, SkErr& err) {{")
+            lines += [ln.replace("RET_T", "sk_delta_t") for ln in body]
             lines.append("}")
+    lines.insert(0, f"typedef {CTYPE[dt]} sk_delta_t;")
     kind = None
     if isinstance(getattr(op, "fn", None), CudaCombine):
         comb_body = op.fn.body
@@ -1358,6 +1456,9 @@ def _reduce_parts(op, delta, val_t: str, in_t: str, val_c: str, in_c: str):
         reduce = N.SK_REDUCE_SUM
     elif kind == "max":
         lines.append("typedef SkMax SkComb;")
+        # per-thread max in the delta's own type, converted once (exact:
+        # conversion to double is monotonic)
+        lines.append("#define SK_LOCAL_MAX 1")
         reduce = N.SK_REDUCE_MAX
     else:
         if comb_body is None:
@@ -1417,6 +1518,7 @@ def build_program(plan, grid) -> Program:
     pad_edge = 1 if fn.pad_mode == "edge" else 0
     pad = fn.pad_value
     parts = []
+    ctx = HelperCtx()
     if isinstance(dk, JitKernel):
         out_dtype = dk.out_dtype if dk.out_dtype is not None else in_dtype
         val_c, val_t = storage_of(out_dtype)
@@ -1429,13 +1531,13 @@ def build_program(plan, grid) -> Program:
         parts.append("__device__ __forceinline__ sk_val_t sk_elemental_n(const SkNb<sk_val_t>& nb, const SkEnv& env, SkErr& err) { return sk_user(nb, env, err); }")
     else:
         point = fn.point
-        tr1 = Translator(point, [], "elemental", win)
+        tr1 = Translator(point, [], "elemental", win, ctx=ctx)
         body1, t1 = tr1.translate()
         # later iterations see the first iteration's output type
         val_c, val_t = CTYPE[t1], t1
         win_n = WindowSpec(k=k, in_c=val_c, in_t=val_t, indexed=win.indexed, env=env_types,
                            env_kind=env_kind, env_obj=env_obj)
-        trn = Translator(point, [], "elemental", win_n)
+        trn = Translator(point, [], "elemental", win_n, ctx=ctx)
         bodyn, tn = trn.translate()
         if tn != t1:
             raise DeviceUnsupported(
@@ -1451,17 +1553,27 @@ def build_program(plan, grid) -> Program:
     else:
         pad_lit = _lit(pad, val_t if isinstance(pad, float) or val_t == F32 else INT) \
             if val_t != BOOL else _lit(bool(pad), BOOL)
+    th = tile_rows(k, max(np.dtype(in_dtype).itemsize, np.dtype(out_dtype).itemsize))
     head = [
         '#include "sk_jit_prelude.cuh"',
         "namespace sk {",
         f"typedef {in_c} sk_in_t;",
         f"typedef {val_c} sk_val_t;",
         f"#define SK_K {k}",
+        f"#define SK_TH {th}",
+        f"#define SK_MINB {int(os.environ.get('SK_JIT_MINB', '0')) or 6}",
         f"#define SK_PAD_EDGE {pad_edge}",
         f"#define SK_PAD_VALUE {pad_lit}",
     ]
-    src = "\n".join(head + parts + red + ["}  // namespace sk", '#include "sk_jit_kernel.cuh"', ""])
+    src = "\n".join(head + ctx.sources + parts + red +
+                    ["}  // namespace sk", '#include "sk_jit_kernel.cuh"', ""])
     handle = compile_source(src)
     return Program(handle=handle, source=src, in_dtype=in_dtype, out_dtype=np.dtype(out_dtype),
                    env_dtypes=tuple(grid_dtype(g) for g in env_grids), reduce=reduce,
-                   int_value=int_value)
+                   int_value=int_value, tile_rows=th)
+
+
+def tile_rows(k: int, esize: int) -> int:
+    """Rows per staged tile: 16, or 8 when two 16-row buffers of the window
+    (+ radius frame, 128 columns wide) would pass 40 KB of shared memory."""
+    return 16 if 2 * (16 + 2 * k) * (128 + 2 * k) * esize <= 40 * 1024 else 8

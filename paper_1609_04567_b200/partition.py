@@ -349,6 +349,7 @@ class DeviceExecutor(Executor):
         p.flags = N.SK_FLAG_TIMING if self.timing else 0
         ident = plan.op.identity
         p.identity = float(ident) if isinstance(ident, (int, float, bool, np.number)) else 0.0
+        p.params[0] = float(prog.tile_rows)  # the program's SK_TH (rows per work tile)
         n = len(envs)
         eptr = (C.c_void_p * 4)(*[C.c_void_p(t.data_ptr()) for t in envs])
         epitch = (C.c_int64 * 4)(*[t.stride(0) for t in envs])

@@ -6,13 +6,14 @@ reduce_pattern, stencil_apply(_indexed), sum_combinator, max_combinator.
 
 What changes is what a descriptor carries.  In the reference an
 ElementalFn is a Python callable (+ an optional numpy block form) that the
-runtime calls per element or per block.  Here an ElementalFn additionally
-carries a `device` descriptor naming one of the engine's sm_100a kernels and
-its dtype-rounded constants; that is what the DeviceExecutor runs.
-Combinators and Deltas map onto the engine's reduce/delta enums, either
-declared (`kind`) or recognised by probing the Python callable on a fixed set
-of values.  A Python callable with no device form is rejected with
-DeviceUnsupported -- there is no per-element host path.
+runtime calls per element or per block.  Here an ElementalFn may carry a
+`device` descriptor naming one of the engine's hand-written sm_100a kernels
+and its dtype-rounded constants; without one, its Python `point` function
+(and the plan's Combinator / Delta callables) are translated and compiled
+for the device at run time (jit.py).  Sum / max combinators and abs /
+square deltas are recognised (declared `kind`, or by probing the callable)
+and map onto the engine's reduce / delta enums.  Anything that cannot be
+compiled is rejected with DeviceUnsupported -- there is no host path.
 """
 
 from __future__ import annotations
@@ -192,27 +193,44 @@ def stencil_apply(f, k: Optional[int], a: Grid, env: Any = None) -> Grid:
 
 
 def stencil_apply_indexed(f, k: Optional[int], a: Grid, env: Any = None) -> Grid:
-    """Indexed stencil application (patterns.py:180-192); device kernels see
-    global indices natively, so this equals stencil_apply."""
-    return stencil_apply(f, k, a, env)
+    """Indexed stencil application (patterns.py:180-192): window entries are
+    (value, index) pairs."""
+    from .loop import stop_after, loop_stencil_reduce_i
+
+    k = _radius(f, k)
+    _check_env(env, a.dims)
+    out, _ = loop_stencil_reduce_i(k, f, sum_combinator(0), stop_after(1), a, env=env)
+    return out
 
 
 def apply_to_all(f: Callable[[Any], Any], a: Grid) -> Grid:
-    """Elementwise map (patterns.py:138-140).  Only device kernels are
-    accepted (a radius-0 ElementalFn with a device form)."""
-    if isinstance(f, ElementalFn) and f.device is not None:
+    """Elementwise map (patterns.py:138-140) on the device: a radius-0
+    stencil.  A plain Python `f(x)` is compiled for the device (jit.py); a
+    radius-0 ElementalFn is applied as is."""
+    if isinstance(f, ElementalFn):
         return stencil_apply(f, f.k, a)
-    raise DeviceUnsupported("apply_to_all needs a device kernel (ElementalFn with .device)")
+    return stencil_apply(ElementalFn(point=lambda nb, env: f(nb.center), k=0), 0, a)
 
 
 def reduce_all(op: Combinator, a: Grid) -> Any:
-    """Reduce of a numeric grid on the device (patterns.py:143-147)."""
+    """Left fold of all elements from the identity (patterns.py:143-147) on
+    the device: SUM / MAX directly; any other combinator as a one-iteration
+    loop of the identity stencil whose reduce is the compiled combinator."""
     from . import _native
 
     _native.require_cuda()
     import torch
 
-    kind = combinator_kind(op)
+    try:
+        kind = combinator_kind(op)
+    except DeviceUnsupported:
+        kind = None
+    if kind is None:
+        from .loop import loop_stencil_reduce, stop_after
+
+        _, rep = loop_stencil_reduce(0, ElementalFn(point=lambda nb, env: nb.center, k=0), op,
+                                     stop_after(1), a)
+        return rep.final_reduce
     t = a.tensor(device="cuda")
     if t.numel() == 0:
         return op.identity

@@ -221,3 +221,31 @@ ERROR_CASES = {
 def cond_fn(spec):
     kind, x = spec["cond"]
     return _lt(x) if kind == "below" else _after(x)
+
+
+def _clip(x, lo, hi):
+    if x < lo:
+        return lo
+    return hi if x > hi else x
+
+
+def _weight(v, c):
+    d = v - c
+    return 1.0 / (1.0 + d * d)
+
+
+def bilateral(nb, env):
+    """Helper functions (plain Python, called per window slot)."""
+    c = nb.center
+    acc = 0.0
+    ws = 0.0
+    for v in nb.values():
+        w = _weight(v, c)
+        acc += w * v
+        ws += w
+    return _clip(acc / ws, -1.0, 1.0)
+
+
+CASES["bilateral_helpers"] = dict(point=bilateral, k=1, op=("sum", None), identity=0.0,
+                                  delta=lambda new, old: abs(new - old), cond=("after", 4),
+                                  grid=lambda: _rng_f64(14, (23, 135), -2, 2), env=None)

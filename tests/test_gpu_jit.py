@@ -147,3 +147,36 @@ def test_reference_executor_protocol_drop_in():
     out, rep = sk.loop_stencil_reduce(1, J.sobel, sk.sum_combinator(0), sk.stop_after(1),
                                       as_grid(g), executor=ex)
     _check("sobel_int", out, rep)
+
+
+def test_map_and_reduce_patterns_compile_python_functions():
+    """apply_to_all / reduce_all / stencil_apply_indexed with plain Python
+    callables (patterns.py:138-192) run as compiled device programs."""
+    a = np.random.default_rng(30).integers(-50, 50, (40, 200)).astype(np.int64)
+    g = as_grid(a)
+    out = sk.apply_to_all(lambda x: x * x - 3 * x if x > 0 else -x, g)
+    want = np.where(a > 0, a * a - 3 * a, -a)
+    assert np.array_equal(out.to_array(), want)
+    mn = sk.reduce_all(sk.Combinator(lambda p, q: p if p < q else q, 10 ** 6), g)
+    assert mn == int(a.min()) and isinstance(mn, int)
+    assert sk.reduce_all(sk.sum_combinator(0), g) == int(a.sum())
+
+    def idx_pt(nb, env):
+        v, (i, j) = nb.center
+        return v + 1000 * i + j
+
+    out = sk.stencil_apply_indexed(idx_pt, 0, g)
+    ii, jj = np.indices(a.shape)
+    assert np.array_equal(out.to_array(), a + 1000 * ii + jj)
+
+
+def test_cuda_source_delta_and_combinator():
+    spec = J.CASES["box_mean_r2"]
+    g, _ = inputs(spec)
+    d = sk.Delta(sk.CudaDelta("const double t = nw - old; return t * t;"))
+    op = sk.Combinator(sk.CudaCombine("return a + b;"), 0.0)
+    out, rep = sk.loop_stencil_reduce_d(2, sk.ElementalFn(J.box_mean, 2), d, op, sk.stop_after(4),
+                                        as_grid(g))
+    meta, arrays = golden()
+    assert np.array_equal(out.to_array(), arrays["box_mean_r2"])
+    assert math.isclose(rep.final_reduce, meta["box_mean_r2"]["final_reduce"], rel_tol=1e-12)

@@ -146,3 +146,18 @@ def test_compile_error_reports_log():
     with pytest.raises(sk.DeviceUnsupported) as ei:
         jit.build_program(LoopPlan(fn=f, k=1, op=sk.sum_combinator(0.0)), g)
     assert "undefined_symbol" in str(ei.value)
+
+
+def test_pattern_wrappers_compile():
+    """apply_to_all's wrapper (a lambda calling the user's lambda) and an
+    indexed identity stencil compile."""
+    g = sk.Grid((6, 9), np.arange(54, dtype=np.int64).reshape(6, 9))
+    f = lambda x: x * x - 3 * x if x > 0 else -x  # noqa: E731
+    wrap = sk.ElementalFn(point=lambda nb, env: f(nb.center), k=0)
+    prog = jit.build_program(LoopPlan(fn=wrap, k=0, op=sk.sum_combinator(0)), g)
+    assert prog.out_dtype == np.int64
+    idx = sk.ElementalFn(point=lambda nb, env: nb.center[0] + nb.center[1][0], k=0)
+    jit.build_program(LoopPlan(fn=idx, k=0, op=sk.sum_combinator(0), indexed=True), g)
+    mn = sk.Combinator(lambda p, q: p if p < q else q, 10 ** 6)
+    jit.build_program(LoopPlan(fn=sk.ElementalFn(point=lambda nb, env: nb.center, k=0), k=0,
+                               op=mn), g)
