@@ -47,6 +47,15 @@ def restore_roofline(flagged, t_iter1_ms):
             "avg_kernel_ms": t_iter1_ms, "peak_source": src}
 
 
+def _traffic(key, units=1):
+    """DRAM bytes per launch from the committed ncu capture (profiles/traffic.json)."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return None
+    v = json.load(open(p)).get(key)
+    return None if v is None else v * units
+
+
 def _events():
     import torch
 
@@ -242,9 +251,10 @@ def c2(args, ClockSampler, measured_peaks, local=0, world=1, rank=0):
                 "h2d_bytes_per_step": F * H * W, "d2h_bytes_per_step": F * H * W,
                 "mode": "pinned host frames, H2D/kernel/D2H overlapped on 3 streams"},
         "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-                     "frac": ach / peak, "traffic": None, "avg_kernel_ms": kms,
+                     "frac": ach / peak, "traffic": _traffic("sobel_2048_per_frame", B),
+                     "avg_kernel_ms": kms,
                      "kernel": f"sobel_sweep batched ({B} frames/launch), 2 B/pixel",
-                     "note": "instruction-issue-bound: exact per-pixel sqrt/round path",
+                     "note": "instruction-issue-bound (70% issue-active): exact per-pixel sqrt/round path",
                      "peak_source": pk},
         "cpu_baseline": None if cpu is None else
         {"value": cpu, "unit": "frames/s", "cores": cores, "kind": "port", "sample": sample},
