@@ -143,7 +143,7 @@ def c1(args, ClockSampler, measured_peaks, local=0):
                 "d2h_bytes_per_step": 4 * n * n * per_step, "ms_per_solve": e2e_s * 1e3},
         "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
                      "frac": ach / peak, "traffic": None, "avg_kernel_ms": sweep_ms,
-                     "kernel": "helmholtz_sweep<float, persistent> per sweep incl. grid barrier",
+                     "kernel": "helm_resident<float> (grid held in registers/smem for the whole loop; one cooperative launch per solve): time per sweep incl. grid barrier",
                      "note": "latency-bound (L2-resident); one cooperative launch per solve",
                      "peak_source": pk},
         "cpu_baseline": {"value": cpu, "unit": "cell-updates/s", "cores": os.cpu_count(),

@@ -21,6 +21,8 @@
 // division): keep*c + ((relax*((f + ax*(l+r)) + ay*(u+d))) / b), constants
 // rounded to the grid dtype first (numpy NEP 50).  Results are bit-identical
 // to the reference block route in fp32 and fp64.
+#include <cstdlib>
+
 #include "sk_internal.h"
 #include "sk_sweep.cuh"
 
@@ -42,6 +44,7 @@ struct HelmArgs {
   LoopCtl L;
   T ax, ay, b, keep, relax;
   int fast_div;  // b inside div_b_ok and verified: use div_const for safe numerators
+  long long xpitch;  // resident loop: row stride of the edge-row exchange buffer
 };
 
 __device__ __forceinline__ float rcp_rn(float b) { return __frcp_rn(b); }
@@ -191,6 +194,289 @@ __global__ void __launch_bounds__(BLOCK, (sizeof(T) == 8 ? (PERSIST ? 4 : SK_F64
   }  // iterations
 }
 
+// ---------------------------------------------------------------- resident loop
+// Small grids (BASELINE C1: 1024^2, 36 sweeps) are latency-bound: a sweep
+// moves 12.6 MB that sit in L2, so what costs is the per-iteration round
+// trip, not bandwidth.  This variant keeps the whole grid ON CHIP for the
+// whole loop: one cooperative launch, one CTA per row band (<= RMAX rows x
+// the full width; 4 columns per thread), u in registers, f in shared memory.
+// Per iteration a CTA reads nothing from memory but its two halo rows (the
+// neighbouring bands' edge rows, exchanged through a small global buffer),
+// and writes only its two edge rows and its reduce partial; the grid barrier
+// that follows also folds the partials and decides the loop (sk_common.cuh).
+// The final iteration's values are written to buf[it & 1] once, at the end.
+// Bands are the chunks of chunk_geom with one column block, so they never
+// span a partition and the reduce tree is the engine's usual one.
+// Arithmetic is helmholtz_sweep's, op for op (bit-identical results).
+template <typename T>
+__device__ __forceinline__ T helm_update(T c, T l, T rt, T up, T dn, T fv, const HelmArgs<T>& a,
+                                         T rb, bool fast) {
+  const T t3 = xadd(fv, xmul(a.ax, xadd(l, rt)));
+  const T num = xmul(a.relax, xadd(t3, xmul(a.ay, xadd(up, dn))));
+  T q;
+  if (fast && div_safe(num)) {
+    q = div_const(num, a.b, rb);
+  } else {
+    q = xdiv(num, a.b);
+  }
+  return xadd(xmul(a.keep, c), q);
+}
+
+// Grid-wide step of the resident loop: every CTA publishes its partial
+// (double-buffered by iteration parity), arrives on a monotonic counter with
+// release semantics and waits for all nb arrivals with acquire semantics;
+// then EVERY CTA folds the nb partials itself -- per partition in the
+// engine's fixed tree, partitions ascending from the identity, as
+// fold_and_decide -- and evaluates the loop test on identical data, so all
+// reach the same decision without a second round trip.  CTA 0 publishes the
+// status for the host at the end.  Returns the stop decision.
+template <int BLOCK, bool AMAX>
+__device__ int res_step(const LoopCtl& L, long long it, double mine, unsigned* cnt, double* parts,
+                        int nb, double* sh) {
+  __shared__ int s_stop;
+  const double v = block_reduce<BLOCK>(L.reduce, mine, sh);
+  double* slot = parts + (it & 1) * nb;
+  // AMAX (one partition, MAX of a non-negative delta): the partials meet in
+  // one atomicMax on the value bits (order-free; non-negative doubles and
+  // NaN order like their bit patterns), three slots by iteration mod 3
+  unsigned long long* amax = reinterpret_cast<unsigned long long*>(parts + 2 * nb);
+  if (threadIdx.x == 0) {
+    if (AMAX) {
+      atomicMax(&amax[it % 3], (unsigned long long)__double_as_longlong(v));
+      if (blockIdx.x == 0) amax[(it + 1) % 3] = 0ull;  // next iteration's slot
+    } else {
+      slot[blockIdx.x] = v;
+    }
+    __threadfence();
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
+    const unsigned want = (unsigned)(nb * it);
+    unsigned seen;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(cnt) : "memory");
+    } while ((int)(seen - want) < 0);
+  }
+  __syncthreads();
+  const OpCombine comb{L.reduce};
+  double acc = L.identity;
+  if (AMAX) {
+    if (threadIdx.x == 0)
+      acc = comb.fold(acc, __longlong_as_double((long long)__ldcg(&amax[it % 3])));
+  } else {
+    const double neutral = comb.neutral(L.identity);
+    for (int p = 0; p < L.nparts; ++p) {
+      double t = neutral;
+      for (int c = L.part_chunk[p] + (int)threadIdx.x; c < L.part_chunk[p + 1]; c += BLOCK)
+        t = comb(t, __ldcg(&slot[c]));
+      const double pv = block_reduce_c<BLOCK>(comb, neutral, t, sh);
+      if (threadIdx.x == 0) acc = comb.fold(acc, pv);
+    }
+  }
+
+  if (threadIdx.x == 0) {
+    const int c = eval_cond(L.cond, acc, it, L.flagged_dev);
+    const int capped = it >= L.cond.max_it;
+    const int stop = c || capped;
+    if (stop && blockIdx.x == 0) {
+      Status* st = L.st;
+      st->value = acc;
+      st->cond_true = c;
+      st->exhausted = !c && capped;
+      st->iter = it;
+      st->stop = 1;
+      __threadfence();
+    }
+    s_stop = stop;
+  }
+  __syncthreads();
+  return s_stop;
+}
+
+// VEC contiguous elements per thread for the resident loop (VEC = 4: one
+// 16-byte vector for float, two for double; 1 or 2: scalar accesses)
+template <typename T, int V>
+struct VecN {
+  T v[V];
+};
+template <typename T, int V>
+__device__ __forceinline__ VecN<T, V> ldgN(const T* p) {
+  VecN<T, V> r;
+  if constexpr (V == 4) {
+    const Vec4<T> q = ldg4(p);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) r.v[e] = q.v[e];
+  } else {
+#pragma unroll
+    for (int e = 0; e < V; ++e) r.v[e] = __ldg(p + e);
+  }
+  return r;
+}
+template <typename T, int V>
+__device__ __forceinline__ void stN(T* p, const VecN<T, V>& x) {
+  if constexpr (V == 4) {
+    Vec4<T> q;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) q.v[e] = x.v[e];
+    st4(p, q);
+  } else {
+#pragma unroll
+    for (int e = 0; e < V; ++e) p[e] = x.v[e];
+  }
+}
+template <typename T, int V>
+__device__ __forceinline__ VecN<T, V> zeroN() {
+  VecN<T, V> r;
+#pragma unroll
+  for (int e = 0; e < V; ++e) r.v[e] = T(0);
+  return r;
+}
+template <typename T, int V>
+__device__ __forceinline__ T sumN(const T* d) {  // helmholtz_sweep's order for V = 4
+  if constexpr (V == 4) return xadd(xadd(d[0], d[1]), xadd(d[2], d[3]));
+  else if constexpr (V == 2) return xadd(d[0], d[1]);
+  else return d[0];
+}
+
+template <typename T, int BLOCK, int VEC, int RMAX, int DELTA, int REDUCE>
+__global__ void __launch_bounds__(BLOCK, 1) helm_resident(const __grid_constant__ HelmArgs<T> a,
+                                                          T* xbuf, unsigned* cnt, double* parts) {
+  constexpr unsigned FULL = 0xffffffffu;
+  constexpr int NW = BLOCK / 32;
+  __shared__ double sh[NW];
+  __shared__ T s_edge[RMAX][2][NW];
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  T* s_f = reinterpret_cast<T*>(s_dyn);  // f of this band, RMAX rows x cols
+  const Sweep2D& g = a.g;
+  long long it = loop_enter(a.L);
+  if (it == 0) return;
+  const int cols = g.cols, rows = g.rows;
+  int cb, r0, r1;
+  chunk_geom(a.L, g, blockIdx.x, &cb, &r0, &r1);
+  const int R = r1 - r0;
+  const int nb = gridDim.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int col = threadIdx.x * VEC;
+  const int nvalid = cols - col;
+  const bool active = nvalid > 0;
+  const T rb = rcp_rn(a.b);
+  const bool fast = a.fast_div != 0;
+  const bool top_zero = !g.halo_top, bot_zero = !g.halo_bottom;
+
+  // iteration-1 input and f, straight from memory (the only full reads)
+  VecN<T, VEC> u[RMAX];
+  const T* src = static_cast<const T*>(g.src) + (long long)g.halo_top * g.src_pitch;
+  const T* env = static_cast<const T*>(g.env) + (long long)g.halo_top * g.env_pitch;
+#pragma unroll
+  for (int r = 0; r < RMAX; ++r) {
+    u[r] = (active && r < R) ? ldgN<T, VEC>(src + (long long)(r0 + r) * g.src_pitch + col) : zeroN<T, VEC>();
+    if (active && r < R) {
+      const VecN<T, VEC> fv = ldgN<T, VEC>(env + (long long)(r0 + r) * g.env_pitch + col);
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) s_f[r * cols + col + e] = fv.v[e];
+    }
+  }
+  VecN<T, VEC> up = (active && !(r0 == 0 && top_zero)) ? ldgN<T, VEC>(src + (long long)(r0 - 1) * g.src_pitch + col)
+                                                   : zeroN<T, VEC>();
+  VecN<T, VEC> dn = (active && !(r1 == rows && bot_zero)) ? ldgN<T, VEC>(src + (long long)r1 * g.src_pitch + col)
+                                                      : zeroN<T, VEC>();
+  for (;;) {
+    // warp-edge columns for the horizontal neighbours of lanes 0 / 31
+#pragma unroll
+    for (int r = 0; r < RMAX; ++r) {
+      if (r < R) {
+        if (lane == 0) s_edge[r][0][warp] = u[r].v[0];
+        if (lane == 31) s_edge[r][1][warp] = u[r].v[VEC - 1];
+      }
+    }
+    __syncthreads();
+    T accm = -INFINITY;
+    double accs = 0.0;
+    VecN<T, VEC> prev = up;  // old value of the row above the current one
+#pragma unroll
+    for (int r = 0; r < RMAX; ++r) {
+      if (r < R) {
+        const VecN<T, VEC> cen = u[r];
+        const VecN<T, VEC> below = (r + 1 < R) ? u[r + 1 < RMAX ? r + 1 : r] : dn;
+        T lv = __shfl_up_sync(FULL, cen.v[VEC - 1], 1);
+        T rv = __shfl_down_sync(FULL, cen.v[0], 1);
+        if (lane == 0) lv = warp > 0 ? s_edge[r][1][warp - 1] : T(0);
+        if (lane == 31) rv = warp + 1 < NW ? s_edge[r][0][warp + 1] : T(0);
+        VecN<T, VEC> o;
+        T dd[VEC];
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) {
+          const T l = e == 0 ? lv : cen.v[e - 1];
+          T rt = e == VEC - 1 ? rv : cen.v[e + 1];
+          if (e + 1 >= nvalid) rt = T(0);  // Dirichlet-0 right border
+          const T fv = active && e < nvalid ? s_f[r * cols + col + e] : T(0);
+          const T out = helm_update(cen.v[e], l, rt, prev.v[e], below.v[e], fv, a, rb, fast);
+          const bool in = e < nvalid;
+          o.v[e] = in ? out : T(0);
+          T d;
+          if (DELTA == SK_DELTA_ABS) {
+            d = tabs(xsub(out, cen.v[e]));
+          } else if (DELTA == SK_DELTA_SQUARE) {
+            const T t = xsub(out, cen.v[e]);
+            d = xmul(t, t);
+          } else {
+            d = out;
+          }
+          if (REDUCE == SK_REDUCE_MAX) {
+            if (in) accm = max_nan(accm, d);
+          } else {
+            dd[e] = in ? d : T(0);
+          }
+        }
+        if (REDUCE == SK_REDUCE_SUM) accs += (double)sumN<T, VEC>(dd);
+        prev = cen;
+        u[r] = o;
+      }
+    }
+    // this band's edge rows for the neighbouring bands (iteration parity slot)
+    if (active) {
+      T* x = xbuf + ((long long)((it & 1) * nb + blockIdx.x) * 2) * a.xpitch;
+      stN<T, VEC>(x + col, u[0]);
+#pragma unroll
+      for (int r = 0; r < RMAX; ++r)
+        if (r == R - 1) stN<T, VEC>(x + a.xpitch + col, u[r]);
+    }
+    const double mine = REDUCE == SK_REDUCE_MAX ? (double)accm : accs;
+    constexpr bool kAmaxOk = REDUCE == SK_REDUCE_MAX && DELTA != SK_DELTA_NONE;
+    const long long nxt =
+        ((kAmaxOk && a.L.nparts == 1) ? res_step<BLOCK, kAmaxOk>(a.L, it, mine, cnt, parts, nb, sh)
+                                      : res_step<BLOCK, false>(a.L, it, mine, cnt, parts, nb, sh))
+            ? 0 : it + 1;
+    if (nxt == 0) {
+      // the loop is over: iteration `it` is the result
+      if (active) {
+        T* out = static_cast<T*>(g.buf[it & 1]) + (long long)g.halo_top * g.pitch;
+#pragma unroll
+        for (int r = 0; r < RMAX; ++r)
+          if (r < R) stN<T, VEC>(out + (long long)(r0 + r) * g.pitch + col, u[r]);
+      }
+      return;
+    }
+    // halo rows of the next iteration: the neighbours' edge rows
+    if (active) {
+      const T* xb = xbuf + (long long)((it & 1) * nb) * 2 * a.xpitch;
+      if (blockIdx.x > 0 && !(r0 == 0)) {
+        const T* p = xb + ((long long)(blockIdx.x - 1) * 2 + 1) * a.xpitch + col;
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) up.v[e] = __ldcg(p + e);
+      } else {
+        up = zeroN<T, VEC>();
+      }
+      if (r1 < rows) {
+        const T* p = xb + ((long long)(blockIdx.x + 1) * 2) * a.xpitch + col;
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) dn.v[e] = __ldcg(p + e);
+      } else {
+        dn = zeroN<T, VEC>();
+      }
+    }
+    it = nxt;
+  }
+}
+
 // ---------------------------------------------------------------- host side
 
 namespace {
@@ -266,6 +552,88 @@ int setup_t(sk_run* r) {
   return SK_OK;
 }
 
+constexpr int kResRows = 8;  // RMAX: rows per band (registers)
+
+template <typename T>
+using ResFn = void (*)(const HelmArgs<T>, T*, unsigned*, double*);
+
+template <typename T, int BLOCK, int VEC>
+ResFn<T> pick_res_b(int delta, int reduce) {
+#define SK_R(D, R) \
+  if (delta == D && reduce == R) return helm_resident<T, BLOCK, VEC, kResRows, D, R>;
+  SK_R(SK_DELTA_NONE, SK_REDUCE_SUM)
+  SK_R(SK_DELTA_NONE, SK_REDUCE_MAX)
+  SK_R(SK_DELTA_ABS, SK_REDUCE_SUM)
+  SK_R(SK_DELTA_ABS, SK_REDUCE_MAX)
+  SK_R(SK_DELTA_SQUARE, SK_REDUCE_SUM)
+  SK_R(SK_DELTA_SQUARE, SK_REDUCE_MAX)
+#undef SK_R
+  return nullptr;
+}
+
+// Register-resident whole-loop launch (see helm_resident) when the grid fits
+// on chip: one band of <= kResRows rows per co-resident CTA, f in shared
+// memory.  Returns SK_ERR_UNSUPPORTED (nothing launched) otherwise.
+template <typename T>
+int launch_resident(sk_run* r, const LoopCtl& L, cudaStream_t s, const HelmArgs<T>& base) {
+  const sk_plan& p = r->plan;
+  if (p.halo_top || p.halo_bottom) return SK_ERR_UNSUPPORTED;
+  const char* off = getenv("SK_NO_RESIDENT");
+  if (off && off[0] == '1') return SK_ERR_UNSUPPORTED;
+  // one column per thread up to 1024 columns (32 warps per SM hide the
+  // shuffle / shared-memory latencies), two up to 2048
+  const int block = 1024;
+  const int vec = p.cols <= 1024 ? 1 : (p.cols <= 2048 ? 2 : 0);
+  if (!vec) return SK_ERR_UNSUPPORTED;
+  ResFn<T> fn = vec == 1 ? pick_res_b<T, 1024, 1>(p.delta_op, p.reduce_op)
+                         : pick_res_b<T, 1024, 2>(p.delta_op, p.reduce_op);
+  if (!fn) return SK_ERR_UNSUPPORTED;
+  const int sms = device_sms(r->device);
+  // band height: the smallest that gives at most one band per SM
+  int band = (int)((p.rows + sms - 1) / sms);
+  if (band < 1) band = 1;
+  if (band > kResRows) return SK_ERR_UNSUPPORTED;
+  LoopCtl L2 = L;
+  int nb = 0;
+  L2.part_chunk[0] = 0;
+  for (int i = 0; i < r->nparts; ++i) {
+    const int pr = r->part_row[i + 1] - r->part_row[i];
+    nb += (pr + band - 1) / band;
+    L2.part_chunk[i + 1] = nb;
+  }
+  const size_t dyn = (size_t)band * p.cols * sizeof(T);
+  if (dyn > 200 * 1024) return SK_ERR_UNSUPPORTED;
+  SK_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+  int occ = 0;
+  SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, reinterpret_cast<const void*>(fn),
+                                                        block, dyn));
+  if (occ < 1 || nb > occ * sms) return SK_ERR_UNSUPPORTED;
+  // scratch: arrival counter | partials (2 x bands) | edge-row exchange
+  // buffer (2 iteration parities x bands x 2 rows x cols)
+  const size_t pbytes = (16 + (size_t)(2 * nb + 3) * sizeof(double) + 255) / 256 * 256;
+  const long long cpad = (p.cols + 3) / 4 * 4;  // aligned rows
+  const size_t xbytes = pbytes + (size_t)2 * nb * 2 * cpad * sizeof(T);
+  if (!r->aux[7] || (size_t)r->aux_n[7] < xbytes) {
+    if (r->aux[7]) SK_CUDA(cudaFreeAsync(r->aux[7], s));
+    SK_CUDA(cudaMallocAsync(&r->aux[7], xbytes, s));
+    r->aux_n[7] = (long long)xbytes;
+  }
+  SK_CUDA(cudaMemsetAsync(r->aux[7], 0, pbytes, s));
+  HelmArgs<T> a = base;
+  a.g.colblocks = 1;
+  a.g.chunk_rows = band;
+  a.xpitch = cpad;
+  a.L = L2;
+  a.L.ring = nullptr;
+  unsigned* cnt = static_cast<unsigned*>(r->aux[7]);
+  double* parts = reinterpret_cast<double*>(static_cast<char*>(r->aux[7]) + 16);
+  T* xbuf = reinterpret_cast<T*>(static_cast<char*>(r->aux[7]) + pbytes);
+  void* params[] = {&a, &xbuf, &cnt, &parts};
+  SK_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(fn), nb, block, params, dyn, s));
+  return SK_OK;
+}
+
 template <typename T>
 int launch_t(sk_run* r, const LoopCtl& L, cudaStream_t s) {
   const sk_plan& p = r->plan;
@@ -298,6 +666,11 @@ int launch_t(sk_run* r, const LoopCtl& L, cudaStream_t s) {
     set_error("helmholtz: persistent loop reserved for small grids");
     return SK_ERR_UNSUPPORTED;  // caller falls back to the graph loop
   }
+  if (persist) {
+    const int rc = launch_resident<T>(r, L, s, a);
+    if (rc == SK_OK) return SK_OK;
+    if (rc != SK_ERR_UNSUPPORTED) return rc;
+  }
   KernelFn<T> fn = pick<T>(p.delta_op, p.reduce_op, persist);
   if (persist) {
     // the persistent variant has its own register budget: size the grid to
@@ -322,7 +695,12 @@ int launch(sk_run* r, const LoopCtl& L, cudaStream_t s) {
   return launch_t<double>(r, L, s);
 }
 
-void teardown(sk_run*) {}
+void teardown(sk_run* r) {
+  if (r->aux[7]) {
+    cudaFreeAsync(r->aux[7], r->stream);
+    r->aux[7] = nullptr;
+  }
+}
 
 const KernelOps kOps = {setup, launch, teardown};
 

@@ -90,6 +90,8 @@ struct RingArena {
 RingArena g_ring;
 }  // namespace
 
+// `c` set: a device loop (sk_run_loop), whose values the host never reads
+// per iteration -- no writes to the host-mapped value ring.
 static LoopCtl make_ctl(sk_run* r, const sk_cond* c, bool graph, cudaGraphConditionalHandle gh) {
   LoopCtl L;
   L.st = r->d_status;
@@ -100,7 +102,7 @@ static LoopCtl make_ctl(sk_run* r, const sk_cond* c, bool graph, cudaGraphCondit
   L.flagged_dev = r->flagged_dev;
   L.reduce = r->plan.reduce_op;
   L.identity = r->plan.identity;
-  L.ring = r->d_ring;
+  L.ring = c ? nullptr : r->d_ring;
   if (c) {
     L.cond.kind = c->kind;
     L.cond.a = c->a;
