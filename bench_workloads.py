@@ -369,7 +369,7 @@ def _c5_frames(k=32):
             for i in range(k)]
 
 
-def c5(args, ClockSampler, measured_peaks, local=0, world=1, rank=0, width=8):
+def c5(args, ClockSampler, measured_peaks, local=0, world=1, rank=0, width=32):
     """Streaming video denoise: 1000 synthetic 1920x1080 frames (10% noise), a
     farm of stencil-reduce loops.
     value: frames resident in HBM; per batch of 32 frames one batched AMF

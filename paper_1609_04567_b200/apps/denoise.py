@@ -15,6 +15,9 @@ W restoration loops are in flight on the GPU at once.
 
 from __future__ import annotations
 
+import threading
+import time
+
 import ctypes as C
 import math
 from dataclasses import dataclass
@@ -276,12 +279,110 @@ def salt_pepper(img: Grid, level: float, seed: int = 42):
     return Grid.from_array(noisy), Grid.from_array(hit.astype(np.int64))
 
 
+class _RestoreBatcher:
+    """Coalesces the restore farm's frames into device batches.
+
+    Every farm replica still handles one frame at a time (the reference's
+    ordered farm, apps/denoise.py:338-356); what the replicas hand in
+    concurrently is restored together by `restore_frames` -- one persistent
+    launch in which every frame runs its own loop to its own stop, each
+    bit-identical to restoring it alone.  A batch is closed when it is full,
+    or when no further frame arrives within `linger_s`."""
+
+    def __init__(self, cfg: RestoreConfig, max_batch: int, linger_s: float = 2e-4,
+                 detect: bool = False):
+        import torch
+
+        self.cfg = cfg
+        self.max_batch = max(1, min(64, max_batch))
+        self.linger_s = linger_s
+        self.cv = threading.Condition()
+        self.pending = []
+        self.closed = False
+        self.detect = detect  # run the detector on each batch first (masks not given)
+        self.stream = torch.cuda.Stream()
+        self.thread = threading.Thread(target=self._run, daemon=True)
+        self.thread.start()
+
+    def submit(self, frame, mask):
+        """frame / mask: [H, W] uint8 CUDA tensors; returns (out, report)."""
+        slot = {"done": threading.Event()}
+        with self.cv:
+            if self.closed:
+                raise RuntimeError("restore batcher is closed")
+            self.pending.append((frame, mask, slot))
+            self.cv.notify_all()
+        slot["done"].wait()
+        if "error" in slot:
+            raise slot["error"]
+        return slot["result"]
+
+    def _take(self):
+        with self.cv:
+            while not self.pending and not self.closed:
+                self.cv.wait()
+            if not self.pending:
+                return None
+            deadline = time.perf_counter() + self.linger_s
+            while len(self.pending) < self.max_batch:
+                left = deadline - time.perf_counter()
+                if left <= 0 or self.closed:
+                    break
+                self.cv.wait(left)
+            shape = self.pending[0][0].shape
+            batch = [x for x in self.pending if x[0].shape == shape][:self.max_batch]
+            for x in batch:
+                self.pending.remove(x)
+            return batch
+
+    def _run(self):
+        import torch
+
+        while True:
+            batch = self._take()
+            if batch is None:
+                return
+            try:
+                with torch.cuda.stream(self.stream):
+                    frames = torch.stack([b[0] for b in batch])
+                    if self.detect:
+                        masks, _ = amf_frames(frames, self.cfg.amf_wmax, stream=self.stream)
+                    else:
+                        masks = torch.stack([b[1] for b in batch])
+                    outs, reps = restore_frames(frames, masks, self.cfg, stream=self.stream)
+                for (_f, _m, slot), o, r in zip(batch, outs, reps):
+                    g = Grid.from_tensor(o, logical_dtype=np.float64)
+                    slot["result"] = (g, r)
+                    slot["done"].set()
+            except Exception as e:  # the batch's frames all fail with it
+                for _f, _m, slot in batch:
+                    slot["error"] = e
+                    slot["done"].set()
+
+    def close(self):
+        with self.cv:
+            self.closed = True
+            self.cv.notify_all()
+        self.thread.join(timeout=30)
+
+
 def video_restore_pipeline(frames: Iterable, *, width: int = 1, partitions: int = 1,
                            mode=DeploymentMode.ONE_TO_ONE, cfg: Optional[RestoreConfig] = None,
                            writer: Optional[Callable] = None, loader: Optional[Callable] = None,
                            mask_writer: Optional[Callable] = None) -> StreamReport:
     """read -> detect -> ordered_farm(restore, width) -> write
-    (apps/denoise.py:307-368)."""
+    (apps/denoise.py:307-368).
+
+    1:1 deployment: the detect stage uploads each frame once (uint8) and
+    runs the detector on the device; the `width` restore replicas hand their
+    frames to one batcher that restores whatever is in flight together in a
+    single persistent launch (a device-side farm of loops, restore_frames).
+    1:n deployment: each replica runs restore_regularize over `partitions`
+    row blocks of its frame."""
+    import torch
+
+    from ..partition import _u8_from
+
     mode = DeploymentMode.parse(mode)
     if mode is DeploymentMode.ONE_TO_N and partitions < 2:
         raise GridError("1:n deployment needs at least 2 partitions")
@@ -290,6 +391,12 @@ def video_restore_pipeline(frames: Iterable, *, width: int = 1, partitions: int 
 
     read = Stage(loader or (lambda f: f), name="read")
     detect_group = WorkerGroup(1)
+    batched = eff == 1
+    # without a mask writer the detector runs inside the restore batches (one
+    # AMF launch per batch, on the batcher's stream); with one, per frame in
+    # the detect stage so the masks are written in stream order
+    fused_detect = batched and mask_writer is None
+    batcher = _RestoreBatcher(cfg, width, detect=fused_detect) if batched else None
 
     def detect_fn(img: Grid):
         # one batched-detector launch on the stage's stream (no run object:
@@ -297,26 +404,45 @@ def video_restore_pipeline(frames: Iterable, *, width: int = 1, partitions: int 
         # mask to the restore farm
         if img.ndim != 2:
             raise GridError("detection expects a 2D image")
-        mask = _detect_frame(img, cfg.amf_wmax, detect_group.stream)
+        if not batched:
+            mask = _detect_frame(img, cfg.amf_wmax, detect_group.stream)
+            if mask_writer is not None:
+                mask_writer(mask)
+            return img, mask
+        st = detect_group.stream
+        dev = torch.device("cuda", torch.cuda.current_device())
+        with torch.cuda.stream(st):
+            t = _u8_from(img, "amf", 0, 255, dev)
+            if fused_detect:
+                st.synchronize()
+                return t, None
+            masks, _ = amf_frames(t.reshape(1, *img.dims), cfg.amf_wmax, stream=st)
+        st.synchronize()
         if mask_writer is not None:
-            mask_writer(mask)
-        return img, mask
+            mg = Grid.from_tensor(masks[0], logical_dtype=np.int64)
+            mg.value_range = (0, 1)
+            mask_writer(mg)
+        return t, masks[0]
 
     detect = Stage(detect_fn, name="detect")
 
     def make_restorer():
-        grp = WorkerGroup(eff)
+        grp = None if batched else WorkerGroup(eff)
 
         class _Restorer:
             def __call__(self, pair):
                 img, mask = pair
+                if batched:
+                    out, _rep = batcher.submit(img, mask)
+                    return out
                 out, _rep = restore_regularize(
                     img, mask, cfg, partitions=eff,
                     mode=mode if eff > 1 else DeploymentMode.ONE_TO_ONE, group=grp)
                 return out
 
             def close(self):
-                grp.close()
+                if grp is not None:
+                    grp.close()
 
         return _Restorer()
 
@@ -334,3 +460,5 @@ def video_restore_pipeline(frames: Iterable, *, width: int = 1, partitions: int 
         return run_stream(frames, top, sink=lambda _item: None)
     finally:
         detect_group.close()
+        if batcher is not None:
+            batcher.close()

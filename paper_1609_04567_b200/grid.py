@@ -247,6 +247,13 @@ class Grid:
 
     def to_array(self, dtype=None) -> np.ndarray:
         """Fresh host numpy array of the elements (grid.py:158-162)."""
+        if self._src == "t" and self._arr is None and self._t is not None and self._t.is_cuda:
+            # read straight from the device into a fresh array (no cached
+            # copy to copy again)
+            a = _to_host(self._t).reshape(self.dims)
+            if self._ldtype is not None and a.dtype != self._ldtype:
+                return a.astype(self._ldtype if dtype is None else dtype)
+            return a.astype(dtype) if dtype is not None else a
         a = self._host()
         return a.astype(dtype) if dtype is not None else a.copy()
 
@@ -313,6 +320,30 @@ _PIN_LOCK = None
 _PIN_POOL: dict = {}
 
 
+_COPY_POOL = None
+
+
+def _par_copy(src: np.ndarray) -> np.ndarray:
+    """Fresh copy of a large host array with 8 threads: the cost is mostly
+    first-touch page faults of the new memory, which parallelise (numpy
+    releases the GIL in copyto)."""
+    global _COPY_POOL
+    out = np.empty_like(src)
+    if src.nbytes < (4 << 20):
+        np.copyto(out, src)
+        return out
+    if _COPY_POOL is None:
+        from concurrent.futures import ThreadPoolExecutor
+
+        _COPY_POOL = ThreadPoolExecutor(8, thread_name_prefix="sk-hostcopy")
+    n, k = src.size, 8
+    step = -(-n // k)
+    a, b = src.reshape(-1), out.reshape(-1)
+    list(_COPY_POOL.map(lambda i: np.copyto(b[i * step:(i + 1) * step], a[i * step:(i + 1) * step]),
+                        range(k)))
+    return out
+
+
 def _to_host(t) -> np.ndarray:
     """Device tensor -> fresh numpy array through a pooled pinned staging
     buffer (pageable copies run at a fraction of PCIe bandwidth)."""
@@ -334,7 +365,7 @@ def _to_host(t) -> np.ndarray:
         src = t.detach().reshape(-1) if t.is_contiguous() else t.detach().contiguous().reshape(-1)
         buf.copy_(src, non_blocking=True)
         torch.cuda.current_stream(t.device).synchronize()
-        return buf.numpy().copy()
+        return _par_copy(buf.numpy())
     finally:
         with _PIN_LOCK:
             _PIN_POOL[key].append(buf)
