@@ -41,11 +41,15 @@ class _Nb:
 
     @property
     def center(self):
+        if len(self.center_index) == 1:
+            return self.entries[self.k]
         w = 2 * self.k + 1
         return self.entries[self.k * w + self.k]
 
     def at(self, *delta):
         k, w = self.k, 2 * self.k + 1
+        if len(delta) == 1:
+            return self.entries[k + delta[0]]
         return self.entries[(k + delta[0]) * w + (k + delta[1])]
 
     def values(self):
@@ -77,6 +81,19 @@ class OracleError(RuntimeError):
         super().__init__(f"failed at {index}: {cause!r}")
 
 
+def _windows_1d(front, n, k, indexed, absent):
+    cls = _IndexedNb if indexed else _Nb
+    for i in range(n):
+        entries = []
+        for a in range(2 * k + 1):
+            gi = i - k + a
+            if 0 <= gi < n:
+                entries.append((front[gi], (gi,)) if indexed else front[gi])
+            else:
+                entries.append(absent)
+        yield (i,), cls(k, (i,), tuple(entries), absent)
+
+
 def _windows(front, rows, cols, k, indexed, absent):
     w = 2 * k + 1
     cls = _IndexedNb if indexed else _Nb
@@ -100,14 +117,18 @@ def sequential_loop(point: Callable, k: int, op: Callable, identity: Any,
                     indexed: bool = False, max_iterations: int = 10_000, absent=None,
                     partitions: int = 1, state=None):
     """Run the loop; returns (rows of values, iterations, final_reduce, exhausted).
+    A flat sequence is a rank-1 grid (the reference's 1D route,
+    partition.py:369-404).
 
     `grid` is a 2D sequence of Python values (numpy scalars keep their type,
     as in a reference Grid built from an array's elements); `cond(value, it,
     state)` as the reference's Condition.fn."""
     if absent is None:
         from paper_1609_04567_b200.grid import ABSENT as absent  # the product's marker
-    front = [list(r) for r in grid]
-    rows, cols = len(front), len(front[0])
+    one_d = not isinstance(grid[0], (list, tuple, np.ndarray))
+    front = list(grid) if one_d else [list(r) for r in grid]
+    rows = len(front)
+    cols = 1 if one_d else len(front[0])
     bounds = [(0, rows)]
     if partitions > 1:
         from oracle.stencil_oracle import split_ranges
@@ -119,16 +140,23 @@ def sequential_loop(point: Callable, k: int, op: Callable, identity: Any,
     value = None
     while True:
         it += 1
-        back = [[None] * cols for _ in range(rows)]
+        back = [None] * rows if one_d else [[None] * cols for _ in range(rows)]
         part_acc = [identity for _ in bounds]
-        for (i, j), nb in _windows(front, rows, cols, k, indexed, absent):
+        wins = _windows_1d(front, rows, k, indexed, absent) if one_d else \
+            _windows(front, rows, cols, k, indexed, absent)
+        for idx, nb in wins:
             try:
                 new = point(nb, env)
             except Exception as e:
-                raise OracleError((i, j), e) from e
-            back[i][j] = new
+                raise OracleError(idx, e) from e
+            i = idx[0]
+            old = front[i] if one_d else front[i][idx[1]]
+            if one_d:
+                back[i] = new
+            else:
+                back[i][idx[1]] = new
             p = next(q for q, (lo, hi) in enumerate(bounds) if lo <= i < hi)
-            part_acc[p] = op(part_acc[p], new if delta is None else delta(new, front[i][j]))
+            part_acc[p] = op(part_acc[p], new if delta is None else delta(new, old))
         value = identity  # host combine of the partials (partition.py:642-646)
         for a in part_acc:
             value = op(value, a)

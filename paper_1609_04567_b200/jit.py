@@ -268,6 +268,8 @@ class WindowSpec:
     env: list = field(default_factory=list)   # per slot (C storage type, semantic type)
     env_kind: str = "none"                    # 'none' | 'grid' | 'tuple' | 'obj'
     env_obj: Any = None
+    ndim: int = 2                             # 1: a rank-1 grid, run as an (n, 1) column
+    dims: tuple = ()                          # the grid's dims (env grids share them)
 
 
 class Translator:
@@ -695,14 +697,28 @@ class Translator:
         self.depth -= 1
         self.emit("} }")
 
-    def _window_loop(self, s, w: "_WindowIter"):
+    def _win_slots(self, i: str):
+        """(slot count, row-offset expr, column-offset expr) of a window walk
+        in row-major order (rank-1 grids: one offset, the column stays 0)."""
         k = self.win.k
         n = 2 * k + 1
+        if self.win.ndim == 1:
+            return n, f"({i} - {k})", "0"
+        return n * n, f"({i} / {n} - {k})", f"({i} % {n} - {k})"
+
+    def _idx_tuple(self, a: str, b: str) -> Val:
+        if self.win.ndim == 1:
+            return Val("tuple", items=(num(f"((long long)nb.i + {a})", INT),))
+        return Val("tuple", items=(num(f"((long long)nb.i + {a})", INT),
+                                   num(f"((long long)nb.j + {b})", INT)))
+
+    def _window_loop(self, s, w: "_WindowIter"):
         self.tmp += 1
         i = f"w{self.tmp}"
-        self.emit(f"for (int {i} = 0; {i} < {n * n}; ++{i}) {{")
+        cnt, ea, eb = self._win_slots(i)
+        self.emit(f"for (int {i} = 0; {i} < {cnt}; ++{i}) {{")
         self.depth += 1
-        self.emit(f"const int {i}a = {i} / {n} - {k}, {i}b = {i} % {n} - {k};")
+        self.emit(f"const int {i}a = {ea}, {i}b = {eb};")
         okc = f"nb.ok({i}a, {i}b)"
         val = self._win_value(f"{i}a", f"{i}b")
         if w.what == "entries":
@@ -712,8 +728,7 @@ class Translator:
             if w.what == "values":
                 item = val
             else:  # pairs
-                item = Val("tuple", items=(val, Val("tuple", items=(
-                    num(f"((long long)nb.i + {i}a)", INT), num(f"((long long)nb.j + {i}b)", INT)))))
+                item = Val("tuple", items=(val, self._idx_tuple(f"{i}a", f"{i}b")))
         self.assign(s.target, item)
         for b in s.body:
             self.stmt(b)
@@ -730,9 +745,7 @@ class Translator:
     def _win_entry(self, a, b, okc) -> Val:
         val = self._win_value(a, b)
         if self.win.indexed:
-            return Val("tuple", items=(val, Val("tuple", items=(
-                num(f"((long long)nb.i + {a})", INT), num(f"((long long)nb.j + {b})", INT)))),
-                ok=okc)
+            return Val("tuple", items=(val, self._idx_tuple(a, b)), ok=okc)
         val.ok = okc
         return val
 
@@ -777,11 +790,10 @@ class Translator:
             if a == "center":
                 v = self._win_value("0", "0")
                 if w.indexed:
-                    return Val("tuple", items=(v, Val("tuple", items=(num("((long long)nb.i)", INT),
-                                                                      num("((long long)nb.j)", INT)))))
+                    return Val("tuple", items=(v, self._idx_tuple("0", "0")))
                 return v
             if a == "center_index":
-                return Val("tuple", items=(num("((long long)nb.i)", INT), num("((long long)nb.j)", INT)))
+                return self._idx_tuple("0", "0")
             if a == "k":
                 return const_val(w.k)
             if a in ("at", "values", "pairs"):
@@ -791,9 +803,9 @@ class Translator:
             if a in ("at", "in_range"):
                 return Val("obj", obj=_EnvMethod(a, base))
             if a == "dims":
-                return Val("obj", obj=(int(self.win.env_obj_dims[0]), int(self.win.env_obj_dims[1])))
+                return Val("obj", obj=tuple(int(d) for d in self.win.dims))
             if a == "ndim":
-                return const_val(2)
+                return const_val(self.win.ndim)
             self.fail(e, f"env attribute {a!r} is not supported on the device")
         if base.kind == "obj":
             try:
@@ -844,6 +856,10 @@ class Translator:
         self.fail(e, f"subscript of a {base.kind}")
 
     def _env_at(self, g: Val, idx, node):
+        if self.win.ndim == 1:
+            if len(idx) != 1:
+                self.fail(node, "env.at takes (i) on a rank-1 grid")
+            idx = [idx[0], const_val(0)]
         if len(idx) != 2:
             self.fail(node, "env.at takes (i, j)")
         i, j = (self.present(x, node) for x in idx)
@@ -889,15 +905,19 @@ class Translator:
                 return self._env_at(fo.grid if fo.grid.kind == "envgrid" else Val("envgrid", slot=0),
                                     args, e)
             a = [self.present(x, e) for x in args]
-            return num(f"env.ok({a[0].c}, {a[1].c})", BOOL)
+            if self.win.ndim == 1:
+                return num(f"env.ok({a[0].c}, 0)", BOOL) if len(a) == 1 else const_val(False)
+            return num(f"env.ok({a[0].c}, {a[1].c})", BOOL) if len(a) == 2 else const_val(False)
         return self._builtin_call(fo, e)
 
     def _nb_call(self, name, e):
         w = self.win
         if name == "at":
             args = self._args(e)
+            if w.ndim == 1 and len(args) == 1:
+                args = [args[0], const_val(0)]
             if len(args) != 2:
-                self.fail(e, "nb.at takes two offsets on a 2D grid")
+                self.fail(e, f"nb.at takes {w.ndim} offset(s) on a rank-{w.ndim} grid")
             a, b = (self.present(x, e) for x in args)
             for v in (a, b):
                 if v.t not in (INT, BOOL):
@@ -932,8 +952,9 @@ class Translator:
         self.emit(f"{CTYPE[t] if how != 'len' else 'long long'} {acc} = {init}; long long {cnt} = 0;")
         if how == "sum" and t == F64:
             self.emit(f"double {acc}c = 0.0;")
-        self.emit(f"for (int {i} = 0; {i} < {n * n}; ++{i}) {{")
-        self.emit(f"  const int {i}a = {i} / {n} - {k}, {i}b = {i} % {n} - {k};")
+        cntw, ea, eb = self._win_slots(i)
+        self.emit(f"for (int {i} = 0; {i} < {cntw}; ++{i}) {{")
+        self.emit(f"  const int {i}a = {ea}, {i}b = {eb};")
         self.emit(f"  if (!nb.ok({i}a, {i}b)) continue;")
         v = self._win_value(f"{i}a", f"{i}b")
         vc = self.cast(v, t) if how != "len" else "0"
@@ -969,7 +990,7 @@ class Translator:
                 and isinstance(args[0].obj, _WindowIter) and args[0].obj.what == "values":
             return self._reduce_window(fo.__name__, args[0].obj, e)
         if fo is len and len(args) == 1 and args[0].kind == "nb":
-            return const_val((2 * self.win.k + 1) ** 2)
+            return const_val((2 * self.win.k + 1) ** self.win.ndim)
         if fo is len and len(args) == 1 and args[0].kind == "obj" and isinstance(args[0].obj, (tuple, list)):
             return const_val(len(args[0].obj))
         if fo is len and len(args) == 1 and args[0].kind == "tuple":
@@ -1513,7 +1534,7 @@ def build_program(plan, grid) -> Program:
     env_kind, env_grids, env_obj = _env_spec(plan.env)
     env_types = [storage_of(grid_dtype(g)) for g in env_grids]
     win = WindowSpec(k=k, in_c=in_c, in_t=in_t, indexed=bool(plan.indexed), env=env_types,
-                     env_kind=env_kind, env_obj=env_obj)
+                     env_kind=env_kind, env_obj=env_obj, ndim=grid.ndim, dims=tuple(grid.dims))
     dk = getattr(fn, "device", None)
     pad_edge = 1 if fn.pad_mode == "edge" else 0
     pad = fn.pad_value
@@ -1536,7 +1557,7 @@ def build_program(plan, grid) -> Program:
         # later iterations see the first iteration's output type
         val_c, val_t = CTYPE[t1], t1
         win_n = WindowSpec(k=k, in_c=val_c, in_t=val_t, indexed=win.indexed, env=env_types,
-                           env_kind=env_kind, env_obj=env_obj)
+                           env_kind=env_kind, env_obj=env_obj, ndim=win.ndim, dims=win.dims)
         trn = Translator(point, [], "elemental", win_n, ctx=ctx)
         bodyn, tn = trn.translate()
         if tn != t1:

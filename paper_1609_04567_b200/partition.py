@@ -290,13 +290,17 @@ class DeviceExecutor(Executor):
         plan, grid = _adapt(plan, grid)
         _check_env(plan.env, grid.dims)
         dk = plan.fn.device if hasattr(plan.fn, "device") else None
-        if grid.ndim != 2:
-            raise DeviceUnsupported("device kernels run on 2D grids")
-        rows, cols = grid.dims
+        jit_fn = dk is None or isinstance(dk, JitKernel)
+        if grid.ndim == 1 and jit_fn:
+            rows, cols = grid.dims[0], 1  # a rank-1 grid runs as an (n, 1) column
+        elif grid.ndim != 2:
+            raise DeviceUnsupported("the built-in device kernels run on 2D grids")
+        else:
+            rows, cols = grid.dims
         P = self.partitions
         _check_partitioning(rows, P, plan.k)
         prog = None
-        if dk is None or isinstance(dk, JitKernel):
+        if jit_fn:
             # a user elemental: compiled for the device at run time (jit.py);
             # raises DeviceUnsupported if it cannot be translated
             prog = build_program(plan, grid)
@@ -358,7 +362,7 @@ class DeviceExecutor(Executor):
                                      src.stride(0), eptr, epitch, n,
                                      C.c_void_p(bufs[0].data_ptr()), C.c_void_p(bufs[1].data_ptr()),
                                      cols, N.stream_handle(stream), C.byref(h)))
-        return _DevRun(plan=plan, dims=(rows, cols), P=P, handle=h, bufs=bufs, src=src,
+        return _DevRun(plan=plan, dims=tuple(grid.dims), P=P, handle=h, bufs=bufs, src=src,
                        env=envs, pitch=cols, cols=cols, out_dtype=prog.out_dtype,
                        int_value=prog.int_value, stream=stream, group=group, owns_group=owns,
                        jit=prog)
@@ -376,12 +380,13 @@ class DeviceExecutor(Executor):
         from .jit import error_cause
 
         i, j = divmod(index.value, run.cols)
+        where = (i,) if len(run.dims) == 1 else (i, j)
         part = None
         if run.P > 1:
             for pi, (lo, hi) in enumerate(_split_ranges(run.dims[0], run.P)):
                 if lo <= i < hi:
                     part = pi
-        raise StencilError((i, j), error_cause(code.value), partition=part)
+        raise StencilError(where, error_cause(code.value), partition=part)
 
     def _begin_on(self, lib, plan, grid, dk, rows, cols, P, reduce, delta, stream, group, owns):
         torch = _torch()
@@ -531,6 +536,8 @@ class DeviceExecutor(Executor):
         out = buf[:, :run.cols]
         if run.pitch != run.cols:
             out = out.contiguous()
+        if len(run.dims) == 1:
+            out = out.reshape(run.dims)
         led = model_ledger(run.dims, run.P, run.plan.k, it)
         g = Grid.from_tensor(out, logical_dtype=run.out_dtype)
         g.value_range = _OUT_RANGE.get(getattr(run.plan.fn.device, "name", None))

@@ -40,7 +40,7 @@ def main():
 
     J.ABSENT = ref.ABSENT  # the functions test against the reference's marker
     arrays, meta = {}, {}
-    for name, spec in {**J.CASES, **J.ERROR_CASES}.items():
+    for name, spec in {**J.CASES, **J.ERROR_CASES, **J.CASES_1D}.items():
         g = spec["grid"]()
         env = spec["env"]() if spec["env"] is not None else None
         if isinstance(env, tuple):

@@ -249,3 +249,21 @@ def bilateral(nb, env):
 CASES["bilateral_helpers"] = dict(point=bilateral, k=1, op=("sum", None), identity=0.0,
                                   delta=lambda new, old: abs(new - old), cond=("after", 4),
                                   grid=lambda: _rng_f64(14, (23, 135), -2, 2), env=None)
+
+
+def smooth1d(nb, env):
+    """Rank-1 grid: 3-point relaxation with one offset per slot."""
+    c = nb.center
+    l = nb.at(-1)
+    r = nb.at(1)
+    l = c if l is ABSENT else l
+    r = c if r is ABSENT else r
+    (i,) = nb.center_index
+    return 0.5 * c + 0.25 * (l + r) + 0.01 * env.at(i)
+
+
+CASES_1D = {
+    "smooth1d": dict(point=smooth1d, k=1, op=("max", None), identity=0.0,
+                     delta=lambda new, old: abs(new - old), cond=("after", 7),
+                     grid=lambda: _rng_f64(15, (517,)), env=lambda: _rng_f64(16, (517,))),
+}

@@ -36,7 +36,7 @@ def _check(name, out, rep):
     assert got.dtype == want.dtype, (got.dtype, want.dtype)
     assert np.array_equal(got.view(np.uint8), want.view(np.uint8)), \
         f"{name}: {np.count_nonzero(got != want)} elements differ"
-    kind = J.CASES[name]["op"][0]
+    kind = {**J.CASES, **J.CASES_1D}[name]["op"][0]
     fr = float(rep.final_reduce)
     if kind == "sum" and not m["final_is_int"]:
         assert math.isclose(fr, m["final_reduce"], rel_tol=SUM_RTOL, abs_tol=1e-300)
@@ -50,6 +50,16 @@ def _check(name, out, rep):
 def test_case_device_loop(name):
     out, rep = run_device(J.CASES[name])
     _check(name, out, rep)
+
+
+@pytest.mark.parametrize("name", sorted(J.CASES_1D))
+def test_rank1_grid(name):
+    """Rank-1 grids (the reference's 1D route, partition.py:369-404)."""
+    out, rep = run_device(J.CASES_1D[name])
+    assert out.dims == J.CASES_1D[name]["grid"]().shape
+    _check(name, out, rep)
+    out3, rep3 = run_device(J.CASES_1D[name], P=3)
+    _check(name, out3, rep3)
 
 
 @pytest.mark.parametrize("name", ["jacobi_f64", "life_glider", "int_mix", "f32_relax"])

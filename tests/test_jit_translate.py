@@ -28,13 +28,14 @@ class _HostGrid:
         self.a = np.asarray(a)
         self.dims = self.a.shape
 
-    def at(self, i, j):
-        if not (0 <= i < self.dims[0] and 0 <= j < self.dims[1]):
+    def at(self, *idx):
+        if len(idx) != len(self.dims) or not all(0 <= i < d for i, d in zip(idx, self.dims)):
             raise sk.GridError("out of range")
-        return py_rows(self.a)[i][j] if self.a.dtype == np.float32 else self.a[i, j].item()
+        v = self.a[idx]
+        return v if self.a.dtype == np.float32 else v.item()
 
-    def in_range(self, i, j):
-        return 0 <= i < self.dims[0] and 0 <= j < self.dims[1]
+    def in_range(self, *idx):
+        return len(idx) == len(self.dims) and all(0 <= i < d for i, d in zip(idx, self.dims))
 
 
 def _oracle(spec):
@@ -49,10 +50,10 @@ def _oracle(spec):
                            indexed=spec.get("indexed", False), max_iterations=spec.get("max_it", 10_000))
 
 
-@pytest.mark.parametrize("name", sorted(J.CASES))
+@pytest.mark.parametrize("name", sorted({**J.CASES, **J.CASES_1D}))
 def test_oracle_matches_reference(name):
     meta, arrays = golden()
-    rows, it, val, ex = _oracle(J.CASES[name])
+    rows, it, val, ex = _oracle({**J.CASES, **J.CASES_1D}[name])
     m = meta[name]
     assert it == m["iterations"] and ex == m["exhausted"]
     assert float(val) == m["final_reduce"]
@@ -71,9 +72,9 @@ def test_oracle_errors_match_reference(name):
     assert type(ei.value.cause).__name__ == meta[name]["error"]
 
 
-@pytest.mark.parametrize("name", sorted({**J.CASES, **J.ERROR_CASES}))
+@pytest.mark.parametrize("name", sorted({**J.CASES, **J.ERROR_CASES, **J.CASES_1D}))
 def test_case_compiles(name):
-    spec = {**J.CASES, **J.ERROR_CASES}[name]
+    spec = {**J.CASES, **J.ERROR_CASES, **J.CASES_1D}[name]
     g, env = inputs(spec)
     plan = LoopPlan(fn=sk.ElementalFn(point=spec["point"], k=spec["k"]), k=spec["k"],
                     op=op_of(spec), env=env_grids(env),
