@@ -13,14 +13,16 @@ from .ledger import CopyLedger
 from .loop import (Condition, DeviceCond, LoopReport, LoopState, loop_stencil_reduce,
                    loop_stencil_reduce_d, loop_stencil_reduce_i, loop_stencil_reduce_s,
                    stop_after)
-from .partition import (DeploymentMode, DeviceExecutor, WorkerGroup, model_ledger,
-                        parallel_loop)
+from .partition import (DeploymentMode, DeviceExecutor, DeviceRows, Partition, PartitionSet,
+                        WorkerGroup, halo_exchange, model_ledger, parallel_loop, parallel_step,
+                        partition)
 from .patterns import (Combinator, Delta, DeviceKernel, DeviceUnsupported, ElementalFn,
                        StencilError, abs_change, apply_to_all, map_pattern, max_combinator,
                        reduce_all, reduce_pattern, sq_change, stencil_apply,
                        stencil_apply_indexed, sum_combinator)
 
 from .jit import CudaCombine, CudaDelta, cuda_elemental
+from .pgm import PgmError, read_pgm, write_pgm
 from .streams import (OrderedFarm, Pipeline, Stage, StreamError, StreamReport, ordered_farm,
                       pipeline, run_stream)
 

@@ -98,6 +98,216 @@ def model_ledger(dims, P: int, k: int, iterations: int) -> CopyLedger:
     return led
 
 
+# ---------------------------------------------------------------- partition sets
+# The reference's host-side building blocks (partition.py:60-262, 415-432):
+# split a grid into row partitions with k-deep halos, exchange halos, run one
+# step per partition, gather.  Here every partition buffer lives in device
+# memory; rows read and write as Python lists like the reference's list
+# storage, so code poking at `part.front[i]` keeps working.
+
+
+class DeviceRows:
+    """A partition buffer (rows incl. halos) in device memory, indexed by
+    local row: `rows[i]` -> list (scalar for 1D), `rows[i] = list`."""
+
+    def __init__(self, t):
+        self.t = t
+
+    def __len__(self):
+        return int(self.t.shape[0])
+
+    def __getitem__(self, i):
+        v = self.t[i]
+        return v.tolist()
+
+    def __setitem__(self, i, value):
+        torch = _torch()
+        self.t[i] = torch.as_tensor(value, dtype=self.t.dtype, device=self.t.device)
+
+    def __iter__(self):
+        return iter(self.t.tolist())
+
+    def __eq__(self, other):
+        if isinstance(other, DeviceRows):
+            other = other.t.tolist()
+        return self.t.tolist() == list(other)
+
+    __hash__ = None
+
+    def __repr__(self):
+        return f"DeviceRows({tuple(self.t.shape)}, {self.t.dtype})"
+
+
+def _as_rows(buf, like) -> "DeviceRows":
+    """Whatever a caller stored in front/back (DeviceRows, tensor, lists) as
+    device rows shaped like `like`."""
+    if isinstance(buf, DeviceRows):
+        return buf
+    torch = _torch()
+    if torch.is_tensor(buf):
+        return DeviceRows(buf)
+    return DeviceRows(torch.as_tensor(buf, dtype=like.t.dtype, device=like.t.device))
+
+
+class Partition:
+    """One partition: owned rows [r_begin, r_end) plus k-deep halos, double
+    buffered in device memory (partition.py:76-148)."""
+
+    def __init__(self, index, r_begin, r_end, top_halo, bottom_halo, width):
+        self.index = index
+        self.r_begin, self.r_end = r_begin, r_end
+        self.top_halo, self.bottom_halo = top_halo, bottom_halo
+        self.width = width  # None for 1D grids
+        self.front = None
+        self.back = None
+
+    @property
+    def rows(self) -> int:
+        return self.r_end - self.r_begin
+
+    @property
+    def owned_elems(self) -> int:
+        return self.rows * (self.width or 1)
+
+    def _t(self, which):
+        b = _as_rows(self.front if which == "front" else self.back, self.front)
+        if which == "front":
+            self.front = b
+        else:
+            self.back = b
+        return b.t
+
+    def owned_view(self, which):
+        return self._t(which)[self.top_halo:self.top_halo + self.rows]
+
+    def owned_head(self, which, k):
+        lo = self.top_halo
+        return self._t(which)[lo:lo + k].clone()
+
+    def owned_tail(self, which, k):
+        hi = self.top_halo + self.rows
+        return self._t(which)[hi - k:hi].clone()
+
+    def set_top_halo(self, which, rows) -> None:
+        self._t(which)[0:self.top_halo] = rows
+
+    def set_bottom_halo(self, which, rows) -> None:
+        lo = self.top_halo + self.rows
+        self._t(which)[lo:lo + self.bottom_halo] = rows
+
+    def swap(self) -> None:
+        self.front, self.back = self.back, self.front
+
+
+class PartitionSet:
+    """All partitions of one grid plus the copy ledger (partition.py:151-184)."""
+
+    def __init__(self, dims, k, parts, storage):
+        self.dims = tuple(dims)
+        self.k = k
+        self.parts = parts
+        self.storage = storage
+        self.ledger = CopyLedger()
+
+    @property
+    def buffer_allocations(self) -> int:
+        return 2 * len(self.parts)  # front + back per partition (partition.py:160)
+
+    @property
+    def P(self) -> int:
+        return len(self.parts)
+
+    def swap_all(self) -> None:
+        for p in self.parts:
+            p.swap()
+
+    def gather(self, which: str = "back") -> Grid:
+        """The owned rows back as one (device) grid; one readback per partition."""
+        torch = _torch()
+        pieces = []
+        for p in self.parts:
+            pieces.append(p.owned_view(which))
+            self.ledger.record_readback(p.owned_elems)
+        return Grid.from_tensor(torch.cat(pieces).reshape(self.dims).contiguous())
+
+
+def partition(a: Grid, P: int, k: int, storage: str = "list") -> PartitionSet:
+    """Split into P row partitions with k-deep halos and load them into device
+    memory (one fill per partition; partition.py:198-244).  `storage` is kept
+    for the signature: the buffers are device tensors either way."""
+    torch = _torch()
+    N.require_cuda()
+    _check_partitioning(a.dims[0], P, k)
+    width = a.dims[1] if a.ndim == 2 else None
+    full = a.tensor(device=torch.device("cuda", torch.cuda.current_device()))
+    parts = []
+    ranges = _split_ranges(a.dims[0], P)
+    ps = PartitionSet(a.dims, k, parts, storage)
+    for i, (lo, hi) in enumerate(ranges):
+        p = Partition(i, lo, hi, k if i > 0 else 0, k if i < P - 1 else 0, width)
+        p.front = DeviceRows(full[lo - p.top_halo:hi + p.bottom_halo].clone())
+        p.back = DeviceRows(torch.empty_like(p.front.t))
+        parts.append(p)
+        ps.ledger.record_fill(p.owned_elems)
+    return ps
+
+
+def halo_exchange(ps: PartitionSet, which: str = "front") -> None:
+    """Refresh every halo from the neighbouring partition's owned rows, device
+    to device; 2*k*width elements and two events per boundary
+    (partition.py:247-262)."""
+    k = ps.k
+    if k == 0 or ps.P == 1:
+        return
+    per_row = ps.parts[0].width or 1
+    for a, b in zip(ps.parts, ps.parts[1:]):
+        b.set_top_halo(which, a.owned_tail(which, k))
+        a.set_bottom_halo(which, b.owned_head(which, k))
+        ps.ledger.record_halo(2 * k * per_row, 2)
+
+
+def parallel_step(ps: PartitionSet, f, k, op: Combinator, env: Any = None):
+    """One stencil step over every partition plus the combined reduce
+    (partition.py:415-432): each partition's buffer (owned rows + halos) is
+    swept on the device, its owned outputs land in the back buffer, its
+    partial is the device reduce of those outputs; the partials are folded
+    in ascending partition order from the identity, on the host as in the
+    reference."""
+    from .loop import loop_stencil_reduce, stop_after
+    from .patterns import _radius, reduce_all
+
+    kk = _radius(f, k)
+    if kk != ps.k:
+        raise GridError(f"stencil radius {kk} does not match halo depth {ps.k}")
+    _check_env(env, ps.dims)
+    partials = []
+    for p in ps.parts:
+        buf = _as_rows(p.front, p.front).t
+        lo, hi = p.r_begin - p.top_halo, p.r_end + p.bottom_halo
+        penv = _slice_env(env, lo, hi)
+        out, _ = loop_stencil_reduce(kk, f, op, stop_after(1), Grid.from_tensor(buf), env=penv)
+        owned = out.tensor()[p.top_halo:p.top_halo + p.rows]
+        if p.back is None or not isinstance(p.back, DeviceRows) or p.back.t.dtype != owned.dtype:
+            p.back = DeviceRows(_torch().empty((hi - lo,) + tuple(owned.shape[1:]),
+                                               dtype=owned.dtype, device=owned.device))
+        p.back.t[p.top_halo:p.top_halo + p.rows] = owned
+        partials.append(reduce_all(op, Grid.from_tensor(owned.contiguous())))
+    combined = op.identity
+    for v in partials:
+        combined = op.fn(combined, v)
+    return partials, combined
+
+
+def _slice_env(env, lo, hi):
+    if env is None:
+        return None
+    if isinstance(env, Grid):
+        return Grid.from_tensor(env.tensor(device="cuda")[lo:hi])
+    if isinstance(env, tuple):
+        return tuple(_slice_env(e, lo, hi) if isinstance(e, Grid) else e for e in env)
+    return env
+
+
 # ---------------------------------------------------------------- worker group
 
 
