@@ -417,9 +417,12 @@ def c5(args, ClockSampler, measured_peaks, local=0, world=1, rank=0, width=32):
         t = torch.tensor([sec], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         sec = float(t.item())
-    # roofline: iteration 1 of frame 0 (all flagged pixels active)
-    masks, counts = amf_frames(dev[:1])
-    t1 = _restore_iter1_ms(sk, dev[0], masks[0])
+    # roofline: restore iteration 1 (every flagged pixel active) at the farm's
+    # batch scale -- the batch's frames stacked into one grid, the work of one
+    # device-side batch of B loops
+    masks, counts = amf_frames(dev)
+    F, H, W = dev.shape
+    t1 = _restore_iter1_ms(sk, dev.reshape(F * H, W), masks.reshape(F * H, W))
     # e2e: the reference's pipeline shape, host frames in / host frames out
     frames = [sk.Grid.from_array(distinct[i % len(distinct)]) for i in range(min(total, 256))]
     video_restore_pipeline(frames[:16], width=width, writer=lambda g: g.to_array())  # warm
@@ -447,7 +450,7 @@ def c5(args, ClockSampler, measured_peaks, local=0, world=1, rank=0, width=32):
                 "h2d_bytes_per_step": len(frames) * 1080 * 1920,
                 "d2h_bytes_per_step": len(frames) * 1080 * 1920 * 8,
                 "mode": f"video_restore_pipeline(width={width}) over {len(frames)} host frames"},
-        "roofline": restore_roofline(int(counts[0]), t1),
+        "roofline": restore_roofline(int(counts.sum()), t1),
         "cpu_baseline": cpu_line,
         "clocks": clk.summary(),
     })
