@@ -92,8 +92,9 @@ typedef struct sk_plan {
   int32_t partitions;  /* row partitions for the reduce fold (partition.py:187-195) */
   int32_t reduce_op;   /* SK_REDUCE_* */
   int32_t delta_op;    /* SK_DELTA_* */
-  int32_t halo_top;    /* 1 if buffers carry a neighbour-owned row above row 0 */
-  int32_t halo_bottom; /* 1 if buffers carry a neighbour-owned row below row rows-1 */
+  int32_t halo_top;    /* neighbour-owned rows the buffers carry above row 0
+                          (Helmholtz: 0 or 1; user elementals: 0 or the radius k) */
+  int32_t halo_bottom; /* likewise below row rows-1 */
   int32_t flags;       /* SK_FLAG_* */
   double identity;     /* combinator identity */
   double params[8];    /* kernel parameters, see SK_KERNEL_* */
@@ -223,7 +224,11 @@ int sk_jit_cubin(const sk_jit* program, void* dst);
 int sk_jit_destroy(sk_jit* program);
 
 /* Executor.begin for a compiled elemental (plan->kernel = SK_KERNEL_JIT,
- * reduce_op SUM / MAX / CUSTOM).  d_src is the input grid (element type of
+ * reduce_op SUM / MAX / CUSTOM).  plan->params: [0] rows per staged tile
+ * (the program's SK_TH), [1] global row of owned row 0 and [2] global row
+ * count when this run is one rank's row block of a larger grid (0, 0 for a
+ * whole grid).  Each d_env[i] points at the env row of owned row 0; a row
+ * block's env carries the same halo rows as its grid, before and after.   d_src is the input grid (element type of
  * the program's sk_in_t), d_buf0/1 the iteration buffers (sk_val_t); d_env
  * holds n_env (0..4) read-only grids aligned with the loop grid, each with
  * its own pitch in elements.  Other calls as for sk_run_begin. */

@@ -160,9 +160,9 @@ constexpr int kTW = 128;  // sk_jit_kernel.cuh tile width; rows per tile = plan.
 
 int jit_setup(sk_run* r) {
   sk_jit* j = const_cast<sk_jit*>(r->jit);
-  if (r->plan.halo_top || r->plan.halo_bottom) {
-    set_error("user elemental kernels run on whole grids (no halo rows)");
-    return SK_ERR_UNSUPPORTED;
+  if (r->plan.halo_top < 0 || r->plan.halo_bottom < 0) {
+    set_error("negative halo rows");
+    return SK_ERR_ARG;
   }
   CUfunction f;
   int rc = jit_function(j, r->device, &f);
@@ -208,16 +208,24 @@ int jit_launch(sk_run* r, const LoopCtl& L, cudaStream_t s) {
   g.pitch = r->pitch;
   g.rows = (int)r->plan.rows;
   g.cols = (int)r->plan.cols;
+  g.halo_top = r->plan.halo_top;
+  g.halo_bottom = r->plan.halo_bottom;
   g.colblocks = r->colblocks;
   g.chunk_rows = r->chunk_rows;
   for (int i = 0; i <= r->nparts; ++i) g.part_row[i] = r->part_row[i];
   a.L = L;
+  // a row block of a larger grid: global row of owned row 0, global rows
+  const int row0 = (int)r->plan.params[1];
+  const int grows = r->plan.params[2] >= 1 ? (int)r->plan.params[2] : g.rows;
   for (int i = 0; i < r->jit_nenv; ++i) {
-    a.env.p[i] = r->jit_env[i];
+    a.env.p[i] = r->jit_env[i];  // -> owned row 0 (halo rows, if any, precede it)
     a.env.pitch[i] = r->jit_env_pitch[i];
   }
-  a.env.rows = g.rows;
+  a.env.rows = grows;
   a.env.cols = g.cols;
+  a.env.row0 = row0;
+  a.env.lo = row0 - g.halo_top;
+  a.env.hi = row0 + g.rows + g.halo_bottom;
   void* params[] = {&a};
   const Driver& d = driver();
   CUresult cr;
@@ -238,7 +246,7 @@ const KernelOps kJitOps = {jit_setup, jit_launch, jit_teardown};
 
 // JitArgs is built on the host and read by NVRTC-compiled code: both sides
 // compile the same headers, the size check below catches drift.
-static_assert(sizeof(SkEnv) == 4 * 8 + 4 * 8 + 8, "SkEnv layout");
+static_assert(sizeof(SkEnv) == 4 * 8 + 4 * 8 + 5 * 4 + 4, "SkEnv layout");
 
 }  // namespace
 

@@ -60,12 +60,14 @@ __device__ __forceinline__ void stage_one(V* dst, const V* src) {
   }
 }
 
+// Local rows [rlo, rhi) are readable: the owned rows plus the halo rows a
+// row block carries (multi-rank runs); beyond them is off the global grid.
 template <class V>
 __device__ __forceinline__ void jit_stage(V* tile, const V* front, long long fp, int r0, int nr,
-                                          int c0, int rows, int cols) {
+                                          int c0, int rlo, int rhi, int cols) {
   const int tx = threadIdx.x % SK_TW, ty = threadIdx.x / SK_TW;
   const int nrow = nr + 2 * SK_K;
-  const bool inner = r0 - SK_K >= 0 && r0 + nr + SK_K <= rows && c0 - SK_K >= 0 &&
+  const bool inner = r0 - SK_K >= rlo && r0 + nr + SK_K <= rhi && c0 - SK_K >= 0 &&
                      c0 + SK_TW + SK_K <= cols;
   if (inner) {  // the whole window frame lies on the grid: plain copies
     const V* p = front + (long long)(r0 - SK_K) * fp + (c0 - SK_K);
@@ -79,9 +81,9 @@ __device__ __forceinline__ void jit_stage(V* tile, const V* front, long long fp,
   } else {
     for (int tr = ty; tr < nrow; tr += SK_BLOCK / SK_TW) {
       int gi = r0 - SK_K + tr;
-      const bool rin = (unsigned)gi < (unsigned)rows;
+      const bool rin = gi >= rlo && gi < rhi;
 #if SK_PAD_EDGE
-      gi = gi < 0 ? 0 : (gi >= rows ? rows - 1 : gi);
+      gi = gi < rlo ? rlo : (gi >= rhi ? rhi - 1 : gi);
 #endif
       const V* rp = front + (long long)gi * fp;
       V* tp = tile + tr * kJitTWP;
@@ -119,10 +121,14 @@ template <class V, bool FIRST>
 __device__ __forceinline__ void jit_sweep(const JitArgs& a, long long it, V* tiles, int* s_chunk,
                                           double* sh, const SkComb& comb) {
   const Sweep2D& g = a.g;
-  const V* front = static_cast<const V*>(FIRST ? g.src : g.buf[(it - 1) & 1]);
   const long long fp = FIRST ? g.src_pitch : g.pitch;
-  sk_val_t* back = static_cast<sk_val_t*>(g.buf[it & 1]);
+  // owned row 0 of the front / back buffers (row blocks carry halo rows)
+  const V* front = static_cast<const V*>(FIRST ? g.src : g.buf[(it - 1) & 1]) +
+                   (long long)g.halo_top * fp;
+  sk_val_t* back = static_cast<sk_val_t*>(g.buf[it & 1]) + (long long)g.halo_top * g.pitch;
   const int rows = g.rows, cols = g.cols;
+  const int rlo = -g.halo_top, rhi = rows + g.halo_bottom;
+  const int row0 = a.env.row0, grows = a.env.rows;
   const int tx = threadIdx.x % SK_TW, ty = threadIdx.x / SK_TW;
   const double neutral = comb.neutral(a.L.identity);
   const int total = a.L.part_chunk[a.L.nparts];
@@ -137,13 +143,13 @@ __device__ __forceinline__ void jit_sweep(const JitArgs& a, long long it, V* til
 #endif
     const int gj = c0 + tx;
     int buf = 0;
-    jit_stage<V>(tiles, front, fp, r0, min(SK_TH, r1 - r0), c0, rows, cols);
+    jit_stage<V>(tiles, front, fp, r0, min(SK_TH, r1 - r0), c0, rlo, rhi, cols);
     for (int t0 = r0; t0 < r1; t0 += SK_TH) {
       const int nr = min(SK_TH, r1 - t0);
       const bool more = t0 + SK_TH < r1;
       if (more)
         jit_stage<V>(tiles + (buf ^ 1) * kJitTileElems, front, fp, t0 + SK_TH,
-                     min(SK_TH, r1 - t0 - SK_TH), c0, rows, cols);
+                     min(SK_TH, r1 - t0 - SK_TH), c0, rlo, rhi, cols);
       stage_wait_upto<V>(more ? 1 : 0);
       __syncthreads();
       const V* tile = tiles + buf * kJitTileElems;
@@ -153,9 +159,9 @@ __device__ __forceinline__ void jit_sweep(const JitArgs& a, long long it, V* til
           SkNb<V> nb;
           nb.c = tile + (lr + SK_K) * kJitTWP + tx + SK_K;
           nb.stride = kJitTWP;
-          nb.i = gi;
+          nb.i = gi + row0;  // global row
           nb.j = gj;
-          nb.rows = rows;
+          nb.rows = grows;
           nb.cols = cols;
           nb.k = SK_K;
           SkErr err;
@@ -169,7 +175,7 @@ __device__ __forceinline__ void jit_sweep(const JitArgs& a, long long it, V* til
             d = sk_delta_n(nw, nb.center(), err);
           }
           back[(long long)gi * g.pitch + gj] = nw;
-          if (err.code) jit_fail(a.L.st, (long long)gi * cols + gj, err.code);
+          if (err.code) jit_fail(a.L.st, (long long)(gi + row0) * cols + gj, err.code);
 #ifdef SK_LOCAL_MAX
           lmax = lany ? jit_lmax(lmax, d) : d;
           lany = true;

@@ -64,16 +64,21 @@ struct SkNb {
 // the loop grid.  get<T>(slot, i, j) reads an absolute element; ok(i, j) says
 // whether (i, j) is on the grid.
 struct SkEnv {
-  const void* p[4];
+  const void* p[4];      // -> owned row 0 of each env grid (halo rows above it)
   long long pitch[4];
-  int rows, cols;
+  int rows, cols;        // global grid dims
+  int row0;              // global row of local row 0 (row blocks of a multi-rank run)
+  int lo, hi;            // global rows [lo, hi) resident here (owned + halos)
   template <class T>
   __device__ __forceinline__ T get(int slot, long long i, long long j) const {
-    return __ldg(static_cast<const T*>(p[slot]) + i * pitch[slot] + j);
+    return __ldg(static_cast<const T*>(p[slot]) + (i - row0) * pitch[slot] + j);
   }
   __device__ __forceinline__ bool ok(long long i, long long j) const {
     return i >= 0 && i < rows && j >= 0 && j < cols;
   }
+  // on the grid but not resident on this rank (a row block's env rows end
+  // with its halo rows)
+  __device__ __forceinline__ bool resident(long long i) const { return i >= lo && i < hi; }
 };
 
 // Kernel parameters of sk_jit_sweep (built on the host in sk_jit.cu).

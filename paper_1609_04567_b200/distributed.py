@@ -46,19 +46,20 @@ def _direct(t) -> bool:
     return t.is_cuda and dist.get_backend() == "nccl"
 
 
-def exchange_halos(buf, rank: int, world: int, halo_top: int, rows: int, group=None) -> None:
+def exchange_halos(buf, rank: int, world: int, halo_top: int, rows: int, group=None,
+                   k: int = 1) -> None:
     """Refresh buf's halo rows from the neighbours' boundary rows.
 
     buf: [halo_top + rows + halo_bottom, pitch]; owned rows start at halo_top.
-    Sends the first owned row up and the last owned row down; receives the
-    neighbours' rows into the top/bottom halo rows (partition.py:247-262).
+    Sends the first k owned rows up and the last k down; receives the
+    neighbours' rows into the top/bottom k halo rows (partition.py:247-262).
     """
     import torch
 
     dist = _dist()
-    first, last = buf[halo_top], buf[halo_top + rows - 1]
-    top = buf[0] if halo_top else None
-    bot = buf[halo_top + rows] if rank < world - 1 else None
+    first, last = buf[halo_top:halo_top + k], buf[halo_top + rows - k:halo_top + rows]
+    top = buf[0:k] if halo_top else None
+    bot = buf[halo_top + rows:halo_top + rows + k] if rank < world - 1 else None
     direct = _direct(buf)
     stage = (lambda t: t) if direct else (lambda t: t.detach().cpu())
     ops, recvs = [], []
@@ -297,3 +298,152 @@ def bench_weak_scaling(args, world: int, rank: int, local: int, ClockSampler, me
         "cpu_baseline": None,
         "clocks": clk.summary(),
     }
+
+
+# ---------------------------------------------------------------- any elemental
+
+
+def _all_ints(vals, group=None):
+    """All-gather small ints on any backend (host round trip)."""
+    import torch
+
+    dist = _dist()
+    backend = dist.get_backend(group)
+    dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else "cpu"
+    mine = torch.tensor(vals, dtype=torch.int64, device=dev)
+    out = [torch.zeros_like(mine) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(out, mine, group=group)
+    return [t.tolist() for t in out]
+
+
+def block_loop(f, k, op, cond, block, *, env=None, delta=None, indexed: bool = False,
+               rank: int, world: int, group=None, max_iterations=None, batch: int = 4):
+    """parallel_loop over a grid split across ranks: this rank holds `block`,
+    its contiguous rows of the global grid (ranks in row order), and `env`,
+    the same rows of each env grid.  Any elemental function -- a built-in
+    Helmholtz kernel or a user function compiled for the device (jit.py) --
+    with a recognised sum / max combinator.  Per iteration: the sweep on the
+    block (k-deep halo rows in its buffers), the k boundary rows to each
+    neighbour (NCCL / gloo), the partials all-gathered and folded in rank
+    order on the device, the loop condition evaluated there (or, for a
+    Python condition, on the host from that same value on every rank).
+    Returns (this rank's owned rows as a device Grid, LoopReport)."""
+    import torch
+
+    from .grid import Grid
+    from .jit import JitKernel, build_program
+    from .loop import LoopReport, _as_plan, as_condition
+    from .partition import _TORCH_DT, model_ledger
+    from .patterns import DeviceUnsupported, StencilError, _check_env, combinator_kind
+
+    lib = N.require_cuda()
+    dist = _dist()
+    block = block if isinstance(block, Grid) else Grid.from_tensor(block)
+    if block.ndim != 2:
+        raise DeviceUnsupported("rank blocks are 2D row blocks")
+    rows, cols = block.dims
+    plan = _as_plan(f, k, op, env, indexed=indexed, delta=delta)
+    k = plan.k
+    _check_env(plan.env, block.dims)
+    counts = [c[0] for c in _all_ints([rows], group)]
+    if any(c < max(k, 1) for c in counts) and world > 1:
+        raise ValueError(f"every rank needs at least {max(k, 1)} rows, got {counts}")
+    row0, grows = sum(counts[:rank]), sum(counts)
+    cond = as_condition(cond, max_iterations)
+    reduce = combinator_kind(plan.op)  # sum / max: the device's cross-rank fold
+    dk = getattr(plan.fn, "device", None)
+    if dk is not None and not isinstance(dk, JitKernel):
+        raise DeviceUnsupported("block_loop runs compiled elementals; use DeviceBlock for "
+                                "the Helmholtz kernel")
+    prog = build_program(plan, block, dims=(grows, cols))
+    dev = torch.device("cuda", torch.cuda.current_device())
+    ht = k if rank > 0 else 0
+    hb = k if rank < world - 1 else 0
+    R = ht + rows + hb
+
+    def with_halos(g, dtype):
+        t = g.tensor(device=dev)
+        if t.dtype != _TORCH_DT[dtype]:
+            t = t.to(_TORCH_DT[dtype])
+        buf = torch.zeros((R, cols), dtype=t.dtype, device=dev)
+        buf[ht:ht + rows] = t.reshape(rows, cols)
+        exchange_halos(buf, rank, world, ht, rows, group, k=k) if k else None
+        return buf
+
+    src = with_halos(block, prog.in_dtype)
+    env_grids = plan.env if isinstance(plan.env, tuple) else (
+        (plan.env,) if isinstance(plan.env, Grid) else ())
+    envs = [with_halos(g, d) for g, d in zip(env_grids, prog.env_dtypes)]
+    bufs = [torch.zeros((R, cols), dtype=_TORCH_DT[prog.out_dtype], device=dev) for _ in range(2)]
+    p = N.sk_plan()
+    p.kernel, p.dtype = N.SK_KERNEL_JIT, 0
+    p.rows, p.cols, p.partitions = rows, cols, 1
+    p.reduce_op, p.delta_op = prog.reduce, N.SK_DELTA_NONE
+    p.halo_top, p.halo_bottom = ht, hb
+    p.identity = float(plan.op.identity)
+    p.params[0], p.params[1], p.params[2] = float(prog.tile_rows), float(row0), float(grows)
+    n = len(envs)
+    eptr = (C.c_void_p * 4)(*[C.c_void_p(t[ht].data_ptr()) for t in envs])
+    epitch = (C.c_int64 * 4)(*[t.stride(0) for t in envs])
+    h = C.c_void_p()
+    N.check(lib.sk_run_begin_jit(C.byref(p), prog.handle, C.c_void_p(src.data_ptr()), cols,
+                                 eptr, epitch, n, C.c_void_p(bufs[0].data_ptr()),
+                                 C.c_void_p(bufs[1].data_ptr()), cols,
+                                 N.stream_handle(torch.cuda.current_stream()), C.byref(h)))
+    try:
+        vp = C.c_void_p()
+        N.check(lib.sk_run_value_ptr(h, C.byref(vp)))
+        partial = torch.as_tensor(_DevPtr(vp.value, 1), device=dev)
+        gathered = torch.zeros(world, dtype=torch.float64, device=dev)
+        dc = cond.device
+        c = N.sk_cond()
+        if dc is not None:
+            c.kind = {"lt": N.SK_COND_LT, "rms_lt": N.SK_COND_RMS_LT, "mean_lt": N.SK_COND_MEAN_LT,
+                      "iter_ge": N.SK_COND_ITER_GE}[dc.kind]
+            c.a, c.n = dc.a, dc.n
+        else:
+            c.kind = N.SK_COND_HOST
+        c.max_iterations = cond.max_iterations
+        launched = 0
+        step_batch = batch if dc is not None else 1
+
+        def status():
+            it, val, stp, ex = C.c_int64(), C.c_double(), C.c_int32(), C.c_int32()
+            N.check(lib.sk_run_status(h, C.byref(it), C.byref(val), C.byref(stp), C.byref(ex)))
+            code, index, eit = C.c_int32(), C.c_int64(), C.c_int64()
+            N.check(lib.sk_run_error(h, C.byref(code), C.byref(index), C.byref(eit)))
+            return it.value, val.value, bool(stp.value), bool(ex.value), code.value, index.value
+
+        while True:
+            for _ in range(step_batch):
+                N.check(lib.sk_run_launch(h, 1))
+                launched += 1
+                if k:
+                    exchange_halos(bufs[launched & 1], rank, world, ht, rows, group, k=k)
+                gather_partials(partial, gathered, group)
+                N.check(lib.sk_run_combine(h, C.c_void_p(gathered.data_ptr()), world, C.byref(c)))
+            it, val, stopped, ex, code, index = status()
+            host_stop = False
+            if dc is None and not stopped and code == 0:
+                host_stop = bool(cond.fn(val, it, None))
+            # one decision for every rank: stop if any rank stopped or failed
+            flags = _all_ints([int(stopped or host_stop), int(code != 0), int(ex)], group)
+            if any(fl[1] for fl in flags):
+                if code:
+                    from .jit import error_cause
+
+                    i, j = divmod(index, cols)
+                    raise StencilError((i, j), error_cause(code), partition=rank)
+                raise StencilError(None, RuntimeError("an elemental failed on another rank"),
+                                   partition=rank)
+            if all(fl[0] for fl in flags) or it >= cond.max_iterations:
+                exhausted = not (stopped and not ex) and not host_stop
+                break
+        which = bufs[it & 1]
+        out = Grid.from_tensor(which[ht:ht + rows].contiguous(), logical_dtype=prog.out_dtype)
+        value = int(val) if prog.int_value else val
+        rep = LoopReport(iterations=it, final_reduce=value,
+                         copies=model_ledger((grows, cols), world, k, it), exhausted=exhausted)
+        return out, rep
+    finally:
+        N.check(lib.sk_run_destroy(h))

@@ -87,6 +87,7 @@ def error_cause(code: int) -> BaseException:
         ERR_GRID: GridError("env index out of range"),
         ERR_INDEX: IndexError("window offset outside the radius"),
         ERR_NEGPOW: ValueError("integer power with a negative exponent"),
+        9: IndexError("env row beyond this rank's row block and halo"),
     }.get(code, RuntimeError(f"device error code {code}"))
 
 
@@ -869,8 +870,9 @@ class Translator:
         cst, sem = self.win.env[slot]
         ii = self.fresh(INT, i.c)
         jj = self.fresh(INT, j.c)
-        self.emit(f"if (!env.ok({ii}, {jj})) err.set(6);")
-        c = f"(env.ok({ii}, {jj}) ? ({CTYPE[sem]})env.get<{cst}>({slot}, {ii}, {jj}) : ({CTYPE[sem]})0)"
+        self.emit(f"if (!env.ok({ii}, {jj})) err.set(6); else if (!env.resident({ii})) err.set(9);")
+        c = (f"((env.ok({ii}, {jj}) && env.resident({ii})) ? "
+             f"({CTYPE[sem]})env.get<{cst}>({slot}, {ii}, {jj}) : ({CTYPE[sem]})0)")
         return num(c, sem)
 
     def _args(self, e):
@@ -1523,8 +1525,9 @@ def grid_dtype(g) -> np.dtype:
     return np.dtype(sd)
 
 
-def build_program(plan, grid) -> Program:
-    """The CUDA program of a plan whose elemental has no built-in kernel."""
+def build_program(plan, grid, dims=None) -> Program:
+    """The CUDA program of a plan whose elemental has no built-in kernel.
+    `dims`: the global grid dims when `grid` is one rank's row block."""
     fn = plan.fn
     k = plan.k
     if k > 8:
@@ -1534,7 +1537,8 @@ def build_program(plan, grid) -> Program:
     env_kind, env_grids, env_obj = _env_spec(plan.env)
     env_types = [storage_of(grid_dtype(g)) for g in env_grids]
     win = WindowSpec(k=k, in_c=in_c, in_t=in_t, indexed=bool(plan.indexed), env=env_types,
-                     env_kind=env_kind, env_obj=env_obj, ndim=grid.ndim, dims=tuple(grid.dims))
+                     env_kind=env_kind, env_obj=env_obj, ndim=grid.ndim,
+                     dims=tuple(dims if dims is not None else grid.dims))
     dk = getattr(fn, "device", None)
     pad_edge = 1 if fn.pad_mode == "edge" else 0
     pad = fn.pad_value
