@@ -274,6 +274,27 @@ def bench_weak_scaling(args, world: int, rank: int, local: int, ClockSampler, me
     res, _, _ = solve()
     iters = res.iterations
     cells = float(world) * n * n * iters
+    # e2e: every rank's block from pinned host memory and its result back,
+    # copies inside the timed region (max over ranks)
+    h_u0 = torch.zeros((n, n), dtype=torch.float32).pin_memory()
+    h_f = torch.ones((n, n), dtype=torch.float32).pin_memory()
+    h_out = torch.empty((n, n), dtype=torch.float32).pin_memory()
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    du0 = h_u0.to("cuda", non_blocking=True)
+    df = h_f.to("cuda", non_blocking=True)
+    blk = DeviceBlock(du0, df, consts, rank=rank, world=world)
+    r2 = run_block_loop(blk, cond)
+    h_out.copy_(r2.out, non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    blk.close()
+    del du0, df
+    e2e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    e2e_ms = float(e2e_ms.item())
     peak, peak_kind = measured_peaks()
     avg = kms / max(kn, 1)
     alg = 12.0 * n * n
@@ -290,7 +311,9 @@ def bench_weak_scaling(args, world: int, rank: int, local: int, ClockSampler, me
                    "NCCL halo rows + device-side rank-ordered combine",
                    "l2": "inputs 4.3 GB/array > 126 MB L2 (no flush needed)"},
         "gpu_launches": launches,
-        "e2e": None,
+        "e2e": {"value": cells / (e2e_ms / 1e3), "unit": "cell-updates/s",
+                "h2d_bytes_per_step": 2 * 4 * n * n * world, "d2h_bytes_per_step": 4 * n * n * world,
+                "ms_per_step": e2e_ms},
         "roofline": {"bound": "hbm", "achieved": alg / (avg / 1e3) / 1e9, "peak": peak,
                      "unit": "GB/s", "frac": alg / (avg / 1e3) / 1e9 / peak, "traffic": None,
                      "kernel": "helmholtz_sweep<float> (rank 0)", "avg_kernel_ms": avg,
