@@ -228,7 +228,8 @@ int sk_jit_destroy(sk_jit* program);
  * (the program's SK_TH), [1] global row of owned row 0 and [2] global row
  * count when this run is one rank's row block of a larger grid (0, 0 for a
  * whole grid).  Each d_env[i] points at the env row of owned row 0; a row
- * block's env carries the same halo rows as its grid, before and after.   d_src is the input grid (element type of
+ * block's env carries the same halo rows as its grid, before and after;
+ * all env grids share one pitch (in elements).   d_src is the input grid (element type of
  * the program's sk_in_t), d_buf0/1 the iteration buffers (sk_val_t); d_env
  * holds n_env (0..4) read-only grids aligned with the loop grid, each with
  * its own pitch in elements.  Other calls as for sk_run_begin. */

@@ -164,6 +164,11 @@ int jit_setup(sk_run* r) {
     set_error("negative halo rows");
     return SK_ERR_ARG;
   }
+  for (int i = 1; i < r->jit_nenv; ++i)
+    if (r->jit_env_pitch[i] != r->jit_env_pitch[0]) {
+      set_error("sk_run_begin_jit: env grids must share one pitch (elements)");
+      return SK_ERR_ARG;
+    }
   CUfunction f;
   int rc = jit_function(j, r->device, &f);
   if (rc) return rc;

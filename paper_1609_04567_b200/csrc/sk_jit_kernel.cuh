@@ -31,7 +31,10 @@
 
 namespace sk {
 
-constexpr int kJitTWP = SK_TW + 2 * SK_K;
+// left/right frame of the staged tile: the radius rounded up to 4 elements,
+// so tile rows start on 16-byte boundaries of the grid row (vector staging)
+constexpr int kJitKA = (SK_K + 3) / 4 * 4;
+constexpr int kJitTWP = SK_TW + 2 * kJitKA;
 constexpr int kJitTileElems = (SK_TH + 2 * SK_K) * kJitTWP;
 constexpr int kJitElemMax = sizeof(sk_in_t) > sizeof(sk_val_t) ? sizeof(sk_in_t) : sizeof(sk_val_t);
 
@@ -44,7 +47,7 @@ __device__ __forceinline__ void jit_fail(Status* st, long long index, int code) 
   atomicMax(&st->err, ~(((unsigned long long)index << 8) | (unsigned)code));
 }
 
-// Stage rows [r0 - K, r0 + nr + K) x columns [c0 - K, c0 + TW + K) of the
+// Stage rows [r0 - K, r0 + nr + K) x columns [c0 - KA, c0 + TW + KA) of the
 // front into the tile: off-grid slots take the pad value ("constant") or the
 // nearest border element ("edge"), like the reference's context assembly
 // (partition.py:278-288, 551-581).
@@ -65,12 +68,28 @@ __device__ __forceinline__ void stage_one(V* dst, const V* src) {
 template <class V>
 __device__ __forceinline__ void jit_stage(V* tile, const V* front, long long fp, int r0, int nr,
                                           int c0, int rlo, int rhi, int cols) {
-  const int tx = threadIdx.x % SK_TW, ty = threadIdx.x / SK_TW;
   const int nrow = nr + 2 * SK_K;
-  const bool inner = r0 - SK_K >= rlo && r0 + nr + SK_K <= rhi && c0 - SK_K >= 0 &&
-                     c0 + SK_TW + SK_K <= cols;
-  if (inner) {  // the whole window frame lies on the grid: plain copies
-    const V* p = front + (long long)(r0 - SK_K) * fp + (c0 - SK_K);
+  const bool rows_in = r0 - SK_K >= rlo && r0 + nr + SK_K <= rhi;
+  const bool cols_in = c0 - kJitKA >= 0 && c0 + SK_TW + kJitKA <= cols;
+  const V* p = front + (long long)(r0 - SK_K) * fp + (c0 - kJitKA);
+  if constexpr (sizeof(V) == 4 || sizeof(V) == 8) {
+    // interior tile on 16-byte aligned rows: 16-byte cp.async vectors
+    const bool aligned = ((reinterpret_cast<unsigned long long>(front) | (fp * sizeof(V))) & 15) == 0;
+    if (rows_in && cols_in && aligned) {
+      constexpr int VE = 16 / sizeof(V);
+      constexpr int NV = kJitTWP / VE;  // vectors per tile row
+      for (int v = threadIdx.x; v < nrow * NV; v += SK_BLOCK) {
+        const int tr = v / NV, cv = v - tr * NV;
+        const unsigned d = (unsigned)__cvta_generic_to_shared(tile + tr * kJitTWP + cv * VE);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d),
+                     "l"(p + (long long)tr * fp + cv * VE));
+      }
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+      return;
+    }
+  }
+  const int tx = threadIdx.x % SK_TW, ty = threadIdx.x / SK_TW;
+  if (rows_in && cols_in) {  // the whole window frame lies on the grid: plain copies
 #pragma unroll 4
     for (int tr = ty; tr < nrow; tr += SK_BLOCK / SK_TW) {
       const V* rp = p + (long long)tr * fp;
@@ -89,7 +108,7 @@ __device__ __forceinline__ void jit_stage(V* tile, const V* front, long long fp,
       V* tp = tile + tr * kJitTWP;
 #pragma unroll
       for (int tc = tx; tc < kJitTWP; tc += SK_TW) {
-        int gj = c0 - SK_K + tc;
+        int gj = c0 - kJitKA + tc;
 #if SK_PAD_EDGE
         gj = gj < 0 ? 0 : (gj >= cols ? cols - 1 : gj);
         stage_one(tp + tc, rp + gj);
@@ -154,16 +173,22 @@ __device__ __forceinline__ void jit_sweep(const JitArgs& a, long long it, V* til
       __syncthreads();
       const V* tile = tiles + buf * kJitTileElems;
       if (gj < cols) {
-        for (int lr = ty; lr < nr; lr += SK_BLOCK / SK_TW) {
-          const int gi = t0 + lr;
-          SkNb<V> nb;
-          nb.c = tile + (lr + SK_K) * kJitTWP + tx + SK_K;
-          nb.stride = kJitTWP;
-          nb.i = gi + row0;  // global row
-          nb.j = gj;
-          nb.rows = grows;
-          nb.cols = cols;
-          nb.k = SK_K;
+        // per-element pointers advance by a fixed stride (no index
+        // arithmetic in the loop)
+        constexpr int RS = SK_BLOCK / SK_TW;  // rows between a thread's elements
+        SkNb<V> nb;
+        nb.c = tile + (ty + SK_K) * kJitTWP + tx + kJitKA;
+        nb.stride = kJitTWP;
+        nb.i = t0 + ty + row0;  // global row
+        nb.j = gj;
+        nb.rows = grows;
+        nb.cols = cols;
+        nb.k = SK_K;
+        nb.eidx = (long long)(t0 + ty) * a.env.pitch[0] + gj;  // env element of the centre
+        const long long estep = (long long)RS * a.env.pitch[0];
+        sk_val_t* bp = back + (long long)(t0 + ty) * g.pitch + gj;
+        const long long bstep = (long long)RS * g.pitch;
+        for (int lr = ty; lr < nr; lr += RS) {
           SkErr err;
           sk_val_t nw;
           sk_delta_t d;
@@ -174,14 +199,18 @@ __device__ __forceinline__ void jit_sweep(const JitArgs& a, long long it, V* til
             nw = sk_elemental_n(nb, a.env, err);
             d = sk_delta_n(nw, nb.center(), err);
           }
-          back[(long long)gi * g.pitch + gj] = nw;
-          if (err.code) jit_fail(a.L.st, (long long)(gi + row0) * cols + gj, err.code);
+          *bp = nw;
+          if (err.code) jit_fail(a.L.st, (long long)nb.i * cols + gj, err.code);
 #ifdef SK_LOCAL_MAX
           lmax = lany ? jit_lmax(lmax, d) : d;
           lany = true;
 #else
           acc = comb(acc, (double)d);
 #endif
+          nb.c += RS * kJitTWP;
+          nb.i += RS;
+          nb.eidx += estep;
+          bp += bstep;
         }
       }
       __syncthreads();  // tile `buf` is free for the tile after next

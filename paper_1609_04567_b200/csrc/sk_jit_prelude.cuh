@@ -53,6 +53,7 @@ struct SkNb {
   int i, j;         // global row / column of the centre
   int rows, cols;   // grid dims
   int k;            // radius
+  long long eidx;   // element index of the centre in the env grids (all pitch == env.pitch[0])
   __device__ __forceinline__ V at(int di, int dj) const { return c[di * stride + dj]; }
   __device__ __forceinline__ bool ok(int di, int dj) const {
     return (unsigned)(i + di) < (unsigned)rows && (unsigned)(j + dj) < (unsigned)cols;
@@ -75,6 +76,11 @@ struct SkEnv {
   }
   __device__ __forceinline__ bool ok(long long i, long long j) const {
     return i >= 0 && i < rows && j >= 0 && j < cols;
+  }
+  // the centre element of env grid `slot` (the common env.at(*nb.center_index))
+  template <class T>
+  __device__ __forceinline__ T at_centre(int slot, long long eidx) const {
+    return __ldg(static_cast<const T*>(p[slot]) + eidx);
   }
   // on the grid but not resident on this rank (a row block's env rows end
   // with its halo rows)

@@ -868,6 +868,9 @@ class Translator:
             self.fail(node, "env indices must be integers")
         slot = g.slot
         cst, sem = self.win.env[slot]
+        if i.c == "((long long)nb.i)" and j.c == "((long long)nb.j)":
+            # the centre's own env element: on the grid and resident
+            return num(f"(({CTYPE[sem]})env.at_centre<{cst}>({slot}, nb.eidx))", sem)
         ii = self.fresh(INT, i.c)
         jj = self.fresh(INT, j.c)
         self.emit(f"if (!env.ok({ii}, {jj})) err.set(6); else if (!env.resident({ii})) err.set(9);")
@@ -1601,4 +1604,5 @@ def build_program(plan, grid, dims=None) -> Program:
 def tile_rows(k: int, esize: int) -> int:
     """Rows per staged tile: 16, or 8 when two 16-row buffers of the window
     (+ radius frame, 128 columns wide) would pass 40 KB of shared memory."""
-    return 16 if 2 * (16 + 2 * k) * (128 + 2 * k) * esize <= 40 * 1024 else 8
+    ka = (k + 3) // 4 * 4
+    return 16 if 2 * (16 + 2 * k) * (128 + 2 * ka) * esize <= 40 * 1024 else 8
