@@ -300,6 +300,7 @@ class _RestoreBatcher:
         self.pending = []
         self.closed = False
         self.detect = detect  # run the detector on each batch first (masks not given)
+        self.device = torch.cuda.current_device()
         self.stream = torch.cuda.Stream()
         self.thread = threading.Thread(target=self._run, daemon=True)
         self.thread.start()
@@ -338,6 +339,7 @@ class _RestoreBatcher:
     def _run(self):
         import torch
 
+        torch.cuda.set_device(self.device)  # the thread restores on its creator's GPU
         while True:
             batch = self._take()
             if batch is None:
