@@ -233,19 +233,23 @@ def _func_node(fn):
                     cands.append(node)
     if not cands:
         raise TranslateError(f"cannot locate the source of {getattr(fn, '__name__', fn)}")
-    if len(cands) > 1:  # several lambdas on one line: match the bytecode
-        for node in cands:
-            try:
-                mod = ast.Expression(body=node) if isinstance(node, ast.Lambda) else None
-                if mod is None:
-                    continue
-                ast.fix_missing_locations(mod)
-                co = compile(mod, fname, "eval")
-                inner = [c for c in co.co_consts if hasattr(c, "co_code")]
-                if inner and inner[0].co_code == code.co_code and inner[0].co_names == code.co_names:
-                    return node
-            except Exception:
-                continue
+    if len(cands) > 1:  # several lambdas on one line: match source columns
+        pos = [(ln, col) for ln, _e, col, ec in code.co_positions()
+               if ln is not None and col is not None and ec is not None and ec > col]
+        pos = [(ln - base, col) for ln, col in pos]
+
+        def contains(node):
+            lo = (node.lineno, node.col_offset)
+            hi = (node.end_lineno, node.end_col_offset)
+            return bool(pos) and all(lo <= q < hi for q in pos)
+
+        inside = [n for n in cands if contains(n)]
+        # nested lambdas also contain the positions: take the innermost
+        inside.sort(key=lambda n: (n.end_lineno - n.lineno, n.end_col_offset - n.col_offset))
+        if not inside:
+            raise TranslateError(f"cannot tell which lambda on line {code.co_firstlineno} "
+                                 f"is {getattr(fn, '__qualname__', fn)}")
+        return inside[0]
     return cands[0]
 
 

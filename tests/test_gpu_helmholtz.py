@@ -29,11 +29,12 @@ def _f32_case(golden, name, *, host_cond=False, P=None):
     tol = m["tol"]
     if m["reduce"] == "max":
         op, delta = sk.max_combinator(0.0), sk.abs_change()
-        cond = (lambda v, it, s: v < tol) if host_cond else sk.Condition.below(tol)
+        # bool(...) keeps the predicate opaque to device_form: the host-driven path
+        cond = (lambda v, it, s: bool(v < tol)) if host_cond else sk.Condition.below(tol)
     else:
         op, delta = sk.sum_combinator(0.0), sk.sq_change()
         nm = n * c
-        cond = (lambda v, it, s: math.sqrt(v / nm) < tol) if host_cond else \
+        cond = (lambda v, it, s: bool(math.sqrt(v / nm) < tol)) if host_cond else \
             sk.Condition.rms_below(tol, nm)
     P = m["P"] if P is None else P
     out, rep = sk.parallel_loop("1:n" if P > 1 else "1:1", P, 1, helmholtz_kernel(cfg), op, cond,
@@ -109,7 +110,8 @@ def test_exhaustion_flag_and_cap():
     u0 = sk.Grid((n, n), np.zeros((n, n), np.float32))
     f = sk.Grid((n, n), np.ones((n, n), np.float32))
     for cond in (sk.Condition.below(1e-30, max_iterations=7),
-                 sk.Condition(lambda v, it, s: v < 1e-30, max_iterations=7)):
+                 sk.Condition(lambda v, it, s: v < 1e-30, max_iterations=7),  # -> device
+                 sk.Condition(lambda v, it, s: bool(v < 1e-30), max_iterations=7)):  # host
         out, rep = sk.parallel_loop("1:1", 1, 1, helmholtz_kernel(cfg), sk.max_combinator(0.0),
                                     cond, u0, env=f, delta=sk.abs_change())
         assert rep.iterations == 7 and rep.exhausted

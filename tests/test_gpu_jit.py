@@ -190,3 +190,18 @@ def test_cuda_source_delta_and_combinator():
     meta, arrays = golden()
     assert np.array_equal(out.to_array(), arrays["box_mean_r2"])
     assert math.isclose(rep.final_reduce, meta["box_mean_r2"]["final_reduce"], rel_tol=1e-12)
+
+
+def test_plain_lambda_condition_runs_on_the_device():
+    """A threshold lambda (`v < tol`) is recognised and the loop runs on the
+    device (one persistent launch), with the host-driven loop's result."""
+    spec = J.CASES["jacobi_f64"]
+    g, env = inputs(spec)
+    ex = sk.DeviceExecutor(1)
+    tol = spec["cond"][1]
+    out, rep = sk.loop_stencil_reduce_d(1, sk.ElementalFn(J.jacobi, 1), sk.abs_change(),
+                                        sk.max_combinator(0.0),
+                                        sk.Condition(lambda v, it, s: v < tol, spec["max_it"]),
+                                        as_grid(g), env=as_grid(env), executor=ex)
+    assert ex.launches == 1
+    _check("jacobi_f64", out, rep)
