@@ -192,7 +192,7 @@ __device__ __forceinline__ void jit_sweep(const JitArgs& a, long long it, V* til
           SkErr err;
           sk_val_t nw;
           sk_delta_t d;
-          if (FIRST) {
+          if constexpr (FIRST) {
             nw = sk_elemental_1(nb, a.env, err);
             d = sk_delta_1(nw, nb.center(), err);
           } else {

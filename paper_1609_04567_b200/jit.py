@@ -511,7 +511,7 @@ class Translator:
     def assign(self, tgt, v: Val):
         if isinstance(tgt, ast.Name):
             name = tgt.id
-            if v.kind in ("nb", "env", "envgrid", "obj", "absent", "none") and v.kind != "absent":
+            if v.kind in ("nb", "env", "envgrid", "obj", "none", "array"):
                 # translate-time alias (e.g. e = env[0], tbl = _RING)
                 self.local_vals[name] = v
                 return
@@ -624,6 +624,17 @@ class Translator:
             return
         src = self.expr(it)
         # the window: nb.values() / nb.pairs() / iter(nb)
+        if src.kind == "array":
+            self.tmp += 1
+            i = f"ai{self.tmp}"
+            self.emit(f"for (int {i} = 0; {i} < {src.obj}; ++{i}) {{")
+            self.depth += 1
+            self.assign(s.target, num(f"{src.c}[{i}]", src.t))
+            for b in s.body:
+                self.stmt(b)
+            self.depth -= 1
+            self.emit("}")
+            return
         if src.kind == "obj" and isinstance(src.obj, _WindowIter):
             self._window_loop(s, src.obj)
             return
@@ -822,6 +833,19 @@ class Translator:
     def x_Subscript(self, e):
         base = self.expr(e.value)
         idx = e.slice
+        if base.kind == "obj" and isinstance(base.obj, _WindowIter) and base.obj.what == "values":
+            base = self._materialize(base.obj, sort=False, node=e)
+        if base.kind == "array":
+            if isinstance(idx, ast.Slice):
+                self.fail(e, "slices of window values are not supported")
+            i = self.present(self.expr(idx), e)
+            if i.t not in (INT, BOOL):
+                self.fail(e, "list indices must be integers")
+            ii = self.fresh(INT, self.cast(i, INT))
+            n = base.obj
+            self.emit(f"if ({ii} < -(long long){n} || {ii} >= (long long){n}) err.set(7);")
+            return num(f"{base.c}[{ii} < 0 ? ({ii} + {n} < 0 ? 0 : {ii} + {n}) : "
+                       f"({ii} >= {n} ? 0 : {ii})]", base.t)
         if base.kind == "env":
             i = self.expr(idx)
             if i.const is None:
@@ -948,6 +972,62 @@ class Translator:
             return Val("obj", obj=_WindowIter(name))
         self.fail(e, f"nb.{name}")
 
+    def _materialize(self, w: "_WindowIter", sort: bool, node) -> Val:
+        """The window's in-grid values as a local array (`sorted(nb.values())`,
+        `list(nb.values())`, `nb.values()[i]`): row-major, then an insertion
+        sort -- Python's sort of numbers is that order too (stable, `<`)."""
+        win = self.win
+        t = win.in_t
+        self.tmp += 1
+        arr, i = f"arr{self.tmp}", f"wa{self.tmp}"
+        cnt, ea, eb = self._win_slots(i)
+        self.emit(f"{CTYPE[t]} {arr}[{cnt}]; int {arr}_n = 0;")
+        self.emit(f"for (int {i} = 0; {i} < {cnt}; ++{i}) {{")
+        self.emit(f"  const int {i}a = {ea}, {i}b = {eb};")
+        self.emit(f"  if (nb.ok({i}a, {i}b)) {arr}[{arr}_n++] = {self._win_value(f'{i}a', f'{i}b').c};")
+        self.emit("}")
+        val = Val("array", c=arr, t=t, obj=f"{arr}_n")
+        if sort:
+            self._sort_array(val)
+        return val
+
+    def _copy_array(self, a: Val) -> Val:
+        self.tmp += 1
+        arr = f"arr{self.tmp}"
+        self.emit(f"{CTYPE[a.t]} {arr}[sizeof({a.c}) / sizeof({a.c}[0])]; const int {arr}_n = {a.obj};")
+        self.emit(f"for (int q = 0; q < {arr}_n; ++q) {arr}[q] = {a.c}[q];")
+        return Val("array", c=arr, t=a.t, obj=f"{arr}_n")
+
+    def _sort_array(self, a: Val) -> None:
+        self.tmp += 1
+        i, j, x = f"si{self.tmp}", f"sj{self.tmp}", f"sx{self.tmp}"
+        self.emit(f"for (int {i} = 1; {i} < {a.obj}; ++{i}) {{")
+        self.emit(f"  const {CTYPE[a.t]} {x} = {a.c}[{i}]; int {j} = {i} - 1;")
+        self.emit(f"  while ({j} >= 0 && {x} < {a.c}[{j}]) {{ {a.c}[{j} + 1] = {a.c}[{j}]; --{j}; }}")
+        self.emit(f"  {a.c}[{j} + 1] = {x};")
+        self.emit("}")
+
+    def _reduce_array(self, how: str, a: Val) -> Val:
+        t = INT if (how == "sum" and a.t == BOOL) else a.t
+        if how == "len":
+            return num(f"((long long){a.obj})", INT)
+        self.tmp += 1
+        acc = f"ra{self.tmp}"
+        self.emit(f"{CTYPE[t]} {acc} = 0;")
+        if how == "sum":
+            if t == F64:  # CPython >= 3.12 sum(): Neumaier compensation
+                self.emit(f"{{ double c_ = 0.0; for (int q = 0; q < {a.obj}; ++q) {{ "
+                          f"const double x_ = {a.c}[q], t_ = {acc} + x_; "
+                          f"c_ += (fabs({acc}) >= fabs(x_)) ? ({acc} - t_) + x_ : (x_ - t_) + {acc}; "
+                          f"{acc} = t_; }} if (c_ != 0.0 && isfinite(c_)) {acc} += c_; }}")
+            else:
+                self.emit(f"for (int q = 0; q < {a.obj}; ++q) {acc} = {acc} + ({CTYPE[t]}){a.c}[q];")
+            return num(acc, t)
+        fn = "py_max" if how == "max" else "py_min"
+        self.emit(f"if ({a.obj} == 0) err.set(3); else {{ {acc} = {a.c}[0]; "
+                  f"for (int q = 1; q < {a.obj}; ++q) {acc} = {fn}({acc}, ({CTYPE[t]}){a.c}[q]); }}")
+        return num(acc, t)
+
     def _reduce_window(self, how, w: "_WindowIter", e):
         """sum / max / min / len over nb.values() as an inline loop."""
         win = self.win
@@ -995,6 +1075,15 @@ class Translator:
         mod = getattr(fo, "__module__", None) or ""
         name = getattr(fo, "__name__", "")
         # window aggregates
+        if fo in (sorted, list) and len(args) == 1 and args[0].kind == "obj" \
+                and isinstance(args[0].obj, _WindowIter) and args[0].obj.what == "values":
+            return self._materialize(args[0].obj, sort=fo is sorted, node=e)
+        if fo is sorted and len(args) == 1 and args[0].kind == "array":
+            arr = self._copy_array(args[0])
+            self._sort_array(arr)
+            return arr
+        if fo in (sum, max, min, len) and len(args) == 1 and args[0].kind == "array":
+            return self._reduce_array(fo.__name__, args[0])
         if fo in (sum, max, min, len) and len(args) == 1 and args[0].kind == "obj" \
                 and isinstance(args[0].obj, _WindowIter) and args[0].obj.what == "values":
             return self._reduce_window(fo.__name__, args[0].obj, e)

@@ -267,3 +267,30 @@ CASES_1D = {
                      delta=lambda new, old: abs(new - old), cond=("after", 7),
                      grid=lambda: _rng_f64(15, (517,)), env=lambda: _rng_f64(16, (517,))),
 }
+
+
+def median_filter(nb, env):
+    """Median of the in-grid window values (radius 2), by sorting them."""
+    vals = sorted(nb.values())
+    n = len(vals)
+    if n % 2:
+        return vals[n // 2]
+    return (vals[n // 2 - 1] + vals[n // 2]) / 2
+
+
+def trimmed_mean(nb, env):
+    """Mean of the window without its extremes (negative indices, sum of a list)."""
+    vals = sorted(nb.values())
+    inner = 0.0
+    for v in vals:
+        inner += v
+    return (inner - vals[0] - vals[-1]) / (len(vals) - 2)
+
+
+CASES["median_filter"] = dict(point=median_filter, k=2, op=("sum", None), identity=0,
+                              delta=None, cond=("after", 2),
+                              grid=lambda: np.random.default_rng(17).integers(0, 50, (27, 133)).astype(np.int64),
+                              env=None)
+CASES["trimmed_mean"] = dict(point=trimmed_mean, k=1, op=("max", None), identity=0.0,
+                             delta=lambda new, old: abs(new - old), cond=("after", 3),
+                             grid=lambda: _rng_f64(18, (25, 131), -3, 3), env=None)
