@@ -48,6 +48,9 @@ struct Status {
   // 0 = none; atomicMax keeps the lowest row-major index
   unsigned long long err;
   long long err_iter;   // iteration whose fold first saw `err` (0 = none)
+  int fix;              // two-iteration launches: the loop stopped at the first
+                        // of the pair; its grid must be recomputed (sk_run_loop)
+  int pad4;
 };
 
 constexpr int kMaxParts = 64;

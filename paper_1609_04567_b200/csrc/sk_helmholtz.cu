@@ -22,6 +22,7 @@
 // rounded to the grid dtype first (numpy NEP 50).  Results are bit-identical
 // to the reference block route in fp32 and fp64.
 #include <cstdlib>
+#include <cstring>
 
 #include "sk_internal.h"
 #include "sk_sweep.cuh"
@@ -192,6 +193,228 @@ __global__ void __launch_bounds__(BLOCK, (sizeof(T) == 8 ? (PERSIST ? 4 : SK_F64
   it = loop_barrier<BLOCK>(a.L, it, sh);
   if (it == 0) return;
   }  // iterations
+}
+
+// ---------------------------------------------------------------- two iterations per pass
+// Temporal blocking: one launch computes iterations t and t+1 of the loop
+// while every grid element crosses HBM once (read u(t-1), f; write
+// u(t+1)) -- u(t) lives only in registers.  A thread keeps, per output row
+// r, the window u(t-1) rows r..r+2, u(t) rows r-1..r+1 and f rows r, r+1;
+// per row it loads u(t-1) row r+2 and f row r+1, computes u(t) row r+1
+// (delta_t accumulated for owned rows), then u(t+1) row r (delta_{t+1}),
+// and stores it.  Horizontal neighbours come from warp shuffles; at warp
+// edges lanes 0 / 31 also compute u(t) one column beyond the warp (from two
+// extra scalar columns of u(t-1)).  Every value is computed with
+// helmholtz_sweep's exact expression, so u(t+1), both deltas and both
+// chunk partials are bit-identical to two single sweeps (same chunks, same
+// accumulation order).  The loop test runs for t, then t+1: if the loop
+// stops at t, u(t) is recomputed by one single sweep from u(t-1), which
+// this launch did not overwrite (sk_run_loop does that fix-up).
+// Buffers: launch L (iterations 2L+1, 2L+2) reads src / buf[(L-1)&1] and
+// writes buf[L&1].
+template <typename T>
+__device__ __forceinline__ T helm_at(const T* p, long long off, bool ok) {
+  return ok ? __ldg(p + off) : T(0);
+}
+
+template <typename T, int BLOCK, int U, int DELTA, int REDUCE>
+__global__ void __launch_bounds__(BLOCK, (sizeof(T) == 8 ? 3 : 4))
+    helmholtz_sweep2(const __grid_constant__ HelmArgs<T> a) {
+  constexpr int VEC = 4;
+  constexpr unsigned FULL = 0xffffffffu;
+  __shared__ double sh[BLOCK / 32];
+  __shared__ int s_chunk;
+  const Sweep2D& g = a.g;
+  const long long t = loop_enter(a.L);  // first of the two iterations (odd)
+  if (t == 0) return;
+  const long long L2 = (t - 1) >> 1;
+  const T* front = static_cast<const T*>(L2 == 0 ? g.src : g.buf[(L2 - 1) & 1]);
+  const long long fp = L2 == 0 ? g.src_pitch : g.pitch;
+  T* back = static_cast<T*>(g.buf[L2 & 1]);
+  const T* env = static_cast<const T*>(g.env);
+  const long long ep = g.env_pitch;
+  const int lane = threadIdx.x & 31;
+  const int cols = g.cols, rows = g.rows;
+  const T rb = rcp_rn(a.b);
+  const bool fast = a.fast_div != 0;
+  const int total = a.L.part_chunk[a.L.nparts];
+  double* part2 = a.L.partials + total;  // partials of iteration t+1
+
+  for (int c = next_chunk(a.L, &s_chunk); c < total; c = next_chunk(a.L, &s_chunk)) {
+    int cb, r0, r1;
+    chunk_geom(a.L, g, c, &cb, &r0, &r1);
+    const int col = cb * (BLOCK * VEC) + (int)threadIdx.x * VEC;
+    const int nvalid = cols - col;
+    const bool active = nvalid > 0;
+    const bool L0 = lane == 0, L31 = lane == 31;
+    const bool okl = L0 && col >= 1 && active, okl2 = L0 && col >= 2 && active;
+    const bool okr = L31 && nvalid > VEC, okr2 = L31 && nvalid > VEC + 1;
+    const bool el_in = okl, er_in = okr;  // the extra u(t) column lies on the grid
+
+    auto rowok = [&](long long r) { return r >= 0 && r < rows; };
+    auto ld4 = [&](const T* base, long long pitch, long long r) -> Vec4<T> {
+      return (active && rowok(r)) ? ldg4(base + r * pitch + col) : zero4<T>();
+    };
+    // one updated value (the reference's expression; see helm_update)
+    auto upd = [&](T cc, T l, T rt, T up, T dn, T fv) -> T {
+      return helm_update(cc, l, rt, up, dn, fv, a, rb, fast);
+    };
+    // u at time (level) of a full 4-vector row: centre / up / down rows, the
+    // lanes' left / right neighbours (lv for lane 0, rv for lane 31), f row
+    auto upd4 = [&](const Vec4<T>& cen, const Vec4<T>& up, const Vec4<T>& dn, T lv_edge,
+                    T rv_edge, const Vec4<T>& fv) -> Vec4<T> {
+      T lv = __shfl_up_sync(FULL, cen.v[VEC - 1], 1);
+      T rv = __shfl_down_sync(FULL, cen.v[0], 1);
+      if (L0) lv = lv_edge;
+      if (L31) rv = rv_edge;
+      Vec4<T> o;
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+        const T l = e == 0 ? lv : cen.v[e - 1];
+        T rt = e == VEC - 1 ? rv : cen.v[e + 1];
+        if (e + 1 >= nvalid) rt = T(0);
+        const T out = upd(cen.v[e], l, rt, up.v[e], dn.v[e], fv.v[e]);
+        o.v[e] = e < nvalid ? out : T(0);
+      }
+      return o;
+    };
+    T accm1 = -INFINITY, accm2 = -INFINITY;
+    double accs1 = 0.0, accs2 = 0.0;
+    auto acc_delta = [&](const Vec4<T>& nw, const Vec4<T>& old, T& accm, double& accs) {
+      T dd[VEC];
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+        T d;
+        if (DELTA == SK_DELTA_ABS) {
+          d = tabs(xsub(nw.v[e], old.v[e]));
+        } else if (DELTA == SK_DELTA_SQUARE) {
+          const T tt = xsub(nw.v[e], old.v[e]);
+          d = xmul(tt, tt);
+        } else {
+          d = nw.v[e];
+        }
+        const bool in = e < nvalid;
+        if (REDUCE == SK_REDUCE_MAX) {
+          if (in) accm = max_nan(accm, d);
+        } else {
+          dd[e] = in ? d : T(0);
+        }
+      }
+      if (REDUCE == SK_REDUCE_SUM) accs += (double)xadd(xadd(dd[0], dd[1]), xadd(dd[2], dd[3]));
+    };
+
+    // ---- prologue: u(t-1) rows r0-2 .. r0+1, f rows r0-1, r0; u(t) rows r0-1, r0
+    Vec4<T> pm2 = ld4(front, fp, r0 - 2), pm1 = ld4(front, fp, r0 - 1);
+    Vec4<T> P1 = ld4(front, fp, r0), P2 = ld4(front, fp, r0 + 1);
+    Vec4<T> fm1 = ld4(env, ep, r0 - 1), F1 = ld4(env, ep, r0);
+    // edge columns of u(t-1): c-1, c-2 (lane 0), c+4, c+5 (lane 31)
+    auto el = [&](long long r, int dc, bool ok) { return helm_at(front, r * fp + col + dc, ok && rowok(r)); };
+    auto fe = [&](long long r, int dc, bool ok) { return helm_at(env, r * ep + col + dc, ok && rowok(r)); };
+    T lm2 = el(r0 - 2, -1, okl), lm1 = el(r0 - 1, -1, okl), l1 = el(r0, -1, okl), l2 = el(r0 + 1, -1, okl);
+    T llm1 = el(r0 - 1, -2, okl2), ll1 = el(r0, -2, okl2);
+    T rm2 = el(r0 - 2, VEC, okr), rm1 = el(r0 - 1, VEC, okr), rr1 = el(r0, VEC, okr), rr2 = el(r0 + 1, VEC, okr);
+    T rrm1 = el(r0 - 1, VEC + 1, okr2), rrr1 = el(r0, VEC + 1, okr2);
+    // u(t) rows r0-1 (halo, not reduced) and r0, own columns + edge columns
+    Vec4<T> Q0 = rowok(r0 - 1) ? upd4(pm1, pm2, P1, lm1, rm1, fm1) : zero4<T>();
+    T e0l = (el_in && rowok(r0 - 1)) ? upd(lm1, llm1, pm1.v[0], lm2, l1, fe(r0 - 1, -1, okl)) : T(0);
+    T e0r = (er_in && rowok(r0 - 1)) ? upd(rm1, pm1.v[VEC - 1], rrm1, rm2, rr1, fe(r0 - 1, VEC, okr)) : T(0);
+    Vec4<T> Q1 = upd4(P1, pm1, P2, l1, rr1, F1);
+    acc_delta(Q1, P1, accm1, accs1);
+    T e1l = el_in ? upd(l1, ll1, P1.v[0], lm1, l2, fe(r0, -1, okl)) : T(0);
+    T e1r = er_in ? upd(rr1, P1.v[VEC - 1], rrr1, rm1, rr2, fe(r0, VEC, okr)) : T(0);
+    T ll2 = el(r0 + 1, -2, okl2), rrr2 = el(r0 + 1, VEC + 1, okr2);
+
+    T* po = back + (long long)r0 * g.pitch + col;
+    for (int r = r0; r < r1; r += U) {
+      // prefetch u(t-1) rows r+2.., f rows r+1.. (+ edge columns)
+      Vec4<T> pu[U], pfv[U];
+      T pl[U], pll[U], pr[U], prr[U], pfl[U], pfr[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (r + u < r1) {
+          const long long rr = r + u + 2, rf = r + u + 1;
+          pu[u] = ld4(front, fp, rr);
+          pfv[u] = ld4(env, ep, rf);
+          pl[u] = el(rr, -1, okl);
+          pll[u] = el(rr, -2, okl2);
+          pr[u] = el(rr, VEC, okr);
+          prr[u] = el(rr, VEC + 1, okr2);
+          pfl[u] = fe(rf, -1, okl);
+          pfr[u] = fe(rf, VEC, okr);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int rw = r + u;
+        if (rw < r1) {
+          const Vec4<T> P3 = pu[u];
+          // u(t) row rw+1 (0 below the grid); reduced when owned
+          Vec4<T> Q2;
+          T e2l = T(0), e2r = T(0);
+          if (rw + 1 < rows) {
+            Q2 = upd4(P2, P1, P3, l2, rr2, pfv[u]);
+            if (el_in) e2l = upd(l2, ll2, P2.v[0], l1, pl[u], pfl[u]);
+            if (er_in) e2r = upd(rr2, P2.v[VEC - 1], rrr2, rr1, pr[u], pfr[u]);
+            if (rw + 1 < r1) acc_delta(Q2, P2, accm1, accs1);
+          } else {
+            Q2 = zero4<T>();
+          }
+          // u(t+1) row rw
+          const Vec4<T> O = upd4(Q1, Q0, Q2, e1l, e1r, F1);
+          acc_delta(O, Q1, accm2, accs2);
+          if (active) st4(po, O);
+          po += g.pitch;
+          // rotate the windows
+          P1 = P2;
+          P2 = P3;
+          l1 = l2;
+          l2 = pl[u];
+          ll2 = pll[u];
+          rr1 = rr2;
+          rr2 = pr[u];
+          rrr2 = prr[u];
+          Q0 = Q1;
+          Q1 = Q2;
+          e1l = e2l;
+          e1r = e2r;
+          F1 = pfv[u];
+        }
+      }
+    }
+    const double mine1 = REDUCE == SK_REDUCE_MAX ? (double)accm1 : accs1;
+    const double v1 = block_reduce<BLOCK>(REDUCE, mine1, sh);
+    const double mine2 = REDUCE == SK_REDUCE_MAX ? (double)accm2 : accs2;
+    const double v2 = block_reduce<BLOCK>(REDUCE, mine2, sh);
+    if (threadIdx.x == 0) {
+      a.L.partials[c] = v1;
+      part2[c] = v2;
+    }
+  }
+  // ---- finish: iteration t, then (unless the loop stops at t) t+1
+  __shared__ int s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned prev = atomicAdd(&a.L.st->ticket, 1u);
+    s_last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  int stop = fold_and_decide<BLOCK>(a.L, t, sh);
+  if (stop) {
+    if (threadIdx.x == 0) a.L.st->fix = 1;  // the result is u(t): recompute it
+  } else {
+    LoopCtl L2c = a.L;
+    L2c.partials = part2;
+    stop = fold_and_decide<BLOCK>(L2c, t + 1, sh);
+  }
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+#ifndef __CUDACC_RTC__
+    if (a.L.use_graph) cudaGraphSetConditional(a.L.gh, stop ? 0u : 1u);
+#endif
+  }
 }
 
 // ---------------------------------------------------------------- resident loop
@@ -635,7 +858,37 @@ int launch_resident(sk_run* r, const LoopCtl& L, cudaStream_t s, const HelmArgs<
 }
 
 template <typename T>
-int launch_t(sk_run* r, const LoopCtl& L, cudaStream_t s) {
+using Kernel2Fn = void (*)(const HelmArgs<T>);
+
+template <typename T>
+Kernel2Fn<T> pick2(int delta, int reduce) {
+#define SK_H2(D, R) \
+  if (delta == D && reduce == R) return helmholtz_sweep2<T, kBlock, (sizeof(T) == 8 ? 2 : 4), D, R>;
+  SK_H2(SK_DELTA_NONE, SK_REDUCE_SUM)
+  SK_H2(SK_DELTA_NONE, SK_REDUCE_MAX)
+  SK_H2(SK_DELTA_ABS, SK_REDUCE_SUM)
+  SK_H2(SK_DELTA_ABS, SK_REDUCE_MAX)
+  SK_H2(SK_DELTA_SQUARE, SK_REDUCE_SUM)
+  SK_H2(SK_DELTA_SQUARE, SK_REDUCE_MAX)
+#undef SK_H2
+  return nullptr;
+}
+
+// Two iterations per launch for device-decided loops over one whole grid,
+// opt-in (SK_TWOSTEP=1): measured on B200 at 32768^2 fp32 it is slower --
+// 6.2 ms per launch (2 iterations) against 2 x 1.99 ms -- because the exact
+// update costs ~25 instructions per cell, so halving the HBM traffic leaves
+// the kernel issue- and latency-bound (47% issue-active at 16 warps/SM);
+// see DESIGN.md.
+bool twostep_ok(const sk_run* r, const LoopCtl& L) {
+  const char* on = getenv("SK_TWOSTEP");
+  if (!(on && on[0] == '1')) return false;
+  return !L.persistent && L.cond.kind != SK_COND_HOST && r->plan.halo_top == 0 &&
+         r->plan.halo_bottom == 0 && r->env != nullptr;
+}
+
+template <typename T>
+HelmArgs<T> helm_args(const sk_run* r, const LoopCtl& L) {
   const sk_plan& p = r->plan;
   HelmArgs<T> a;
   Sweep2D& g = a.g;
@@ -661,6 +914,52 @@ int launch_t(sk_run* r, const LoopCtl& L, cudaStream_t s) {
   a.keep = (T)p.params[3];
   a.relax = (T)p.params[4];
   a.fast_div = r->aux_n[0] ? 1 : 0;
+  a.xpitch = 0;
+  return a;
+}
+
+// The loop stopped at the first iteration `it` of a two-iteration launch:
+// recompute u(it) from u(it-1) (the launch's front, untouched) into the
+// launch's back buffer with one single sweep under a scratch status.
+template <typename T>
+int fixup_t(sk_run* r, long long it, cudaStream_t s) {
+  const long long L2 = (it - 1) >> 1;
+  if (!r->aux[6]) SK_CUDA(cudaMallocAsync(&r->aux[6], sizeof(Status), s));
+  SK_CUDA(cudaMemsetAsync(r->aux[6], 0, sizeof(Status), s));
+  LoopCtl L;
+  memset(&L, 0, sizeof(L));
+  L.st = static_cast<Status*>(r->aux[6]);
+  L.partials = r->d_partials;
+  L.nparts = r->nparts;
+  for (int i = 0; i <= r->nparts; ++i) L.part_chunk[i] = r->part_chunk[i];
+  L.reduce = r->plan.reduce_op;
+  L.identity = r->plan.identity;
+  L.cond.kind = SK_COND_ITER_GE;
+  L.cond.n = 1.0;
+  L.cond.max_it = 1;
+  HelmArgs<T> a = helm_args<T>(r, L);
+  a.g.src = L2 == 0 ? r->src : r->buf[(L2 - 1) & 1];
+  a.g.src_pitch = L2 == 0 ? r->src_pitch : r->pitch;
+  a.g.buf[0] = a.g.buf[1] = r->buf[L2 & 1];
+  KernelFn<T> fn = pick<T>(r->plan.delta_op, r->plan.reduce_op, false);
+  SK_CUDA(launch_kernel(fn, r->grid, r->block, a, s, false));
+  return SK_OK;
+}
+
+template <typename T>
+int launch_t(sk_run* r, const LoopCtl& L, cudaStream_t s) {
+  const sk_plan& p = r->plan;
+  HelmArgs<T> a = helm_args<T>(r, L);
+  if (twostep_ok(r, L)) {
+    Kernel2Fn<T> fn2 = pick2<T>(p.delta_op, p.reduce_op);
+    if (fn2) {
+      r->steps_per_launch = 2;
+      const int occ2 = occupancy(reinterpret_cast<const void*>(fn2), r->block);
+      const int slots = device_sms(r->device) * occ2;
+      SK_CUDA(launch_kernel(fn2, r->grid < slots ? r->grid : slots, r->block, a, s, false));
+      return SK_OK;
+    }
+  }
   const bool persist = L.persistent != 0;
   if (persist && (long long)p.rows * p.cols > kPersistMaxCells) {
     set_error("helmholtz: persistent loop reserved for small grids");
@@ -695,14 +994,20 @@ int launch(sk_run* r, const LoopCtl& L, cudaStream_t s) {
   return launch_t<double>(r, L, s);
 }
 
-void teardown(sk_run* r) {
-  if (r->aux[7]) {
-    cudaFreeAsync(r->aux[7], r->stream);
-    r->aux[7] = nullptr;
-  }
+int fixup(sk_run* r, long long it, cudaStream_t s) {
+  if (r->plan.dtype == SK_F32) return fixup_t<float>(r, it, s);
+  return fixup_t<double>(r, it, s);
 }
 
-const KernelOps kOps = {setup, launch, teardown};
+void teardown(sk_run* r) {
+  for (int i : {6, 7})
+    if (r->aux[i]) {
+      cudaFreeAsync(r->aux[i], r->stream);
+      r->aux[i] = nullptr;
+    }
+}
+
+const KernelOps kOps = {setup, launch, teardown, fixup};
 
 }  // namespace
 

@@ -28,6 +28,9 @@ struct KernelOps {
   int (*setup)(sk_run*);
   int (*launch)(sk_run*, const LoopCtl&, cudaStream_t);
   void (*teardown)(sk_run*);
+  // after a device loop whose launches compute two iterations each stopped
+  // at the first of a pair: recompute that iteration's grid (may be null)
+  int (*fixup)(sk_run*, long long it, cudaStream_t) = nullptr;
 };
 
 const KernelOps* helmholtz_ops();
@@ -120,6 +123,7 @@ struct sk_run {
   long long jit_env_pitch[4] = {};
   int jit_nenv = 0;
   bool no_graph = false;  // the kernel cannot drive a graph WHILE node
+  int steps_per_launch = 1;  // 2: launches compute iterations 2L+1, 2L+2 (results in buf[L & 1])
 
   // kernel-specific device state (restore: flagged list, change flags)
   void* aux[8] = {};  // kernel-specific device allocations

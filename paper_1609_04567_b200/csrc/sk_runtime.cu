@@ -135,7 +135,8 @@ static int launch_timed(sk_run* r, const LoopCtl& L) {
     SK_CUDA(cudaEventRecord(b, r->stream));
     r->t_start.push_back(a);
     r->t_stop.push_back(b);
-    r->t_iter.push_back(r->launched);
+    // first iteration this launch computes (two per launch: 2L+1)
+    r->t_iter.push_back(r->steps_per_launch == 2 ? 2 * r->launched - 1 : r->launched);
   }
   cudaEvent_t& ev = r->ev_done[r->launched % kRing];
   if (!ev) SK_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -295,7 +296,8 @@ int begin_impl(const sk_plan* plan, const sk_jit* jit, const void* d_src, int64_
     return fail(ce, "cudaMallocAsync(status)");
   if ((ce = cudaMemsetAsync(r->d_status, 0, sizeof(Status), r->stream)))
     return fail(ce, "cudaMemsetAsync(status)");
-  const size_t np = (size_t)(r->nchunks > r->grid ? r->nchunks : r->grid) + 1;
+  // two partials slots per chunk: two-iteration launches reduce both
+  const size_t np = 2 * ((size_t)(r->nchunks > r->grid ? r->nchunks : r->grid) + 1);
   if ((ce = cudaMallocAsync(reinterpret_cast<void**>(&r->d_partials), np * sizeof(double), r->stream)))
     return fail(ce, "cudaMallocAsync(partials)");
   if ((rc = g_ring.take(&r->h_ring, &r->d_ring))) {
@@ -431,7 +433,17 @@ int sk_run_loop(sk_run* r, const sk_cond* c, int64_t* iterations, double* final_
     set_error("sk_run_loop: device loop ended without a decision");
     return SK_ERR_STATE;
   }
-  if (use_graph) r->total_launches += st.iter;  // one sweep per WHILE-body execution
+  if (use_graph)  // one sweep kernel per WHILE-body execution
+    r->total_launches += r->steps_per_launch == 2 ? (st.iter + 1) / 2 : st.iter;
+  if (st.fix) {  // stopped at the first iteration of a two-iteration launch
+    if (!r->ops->fixup) {
+      set_error("sk_run_loop: kernel cannot recompute a skipped iteration");
+      return SK_ERR_STATE;
+    }
+    if ((rc = r->ops->fixup(r, st.iter, r->stream))) return rc;
+    r->total_launches += 1;
+    SK_CUDA(cudaStreamSynchronize(r->stream));
+  }
   r->launched = st.iter;  // committed iterations
   if (iterations) *iterations = st.iter;
   if (final_value) *final_value = st.value;
@@ -444,7 +456,9 @@ int sk_run_result(sk_run* r, int64_t it, int32_t* which) {
     set_error("sk_run_result: iteration out of range");
     return SK_ERR_ARG;
   }
-  *which = it == 0 ? -1 : (int32_t)(it & 1);
+  if (it == 0) *which = -1;
+  else if (r->steps_per_launch == 2) *which = (int32_t)(((it - 1) >> 1) & 1);
+  else *which = (int32_t)(it & 1);
   return SK_OK;
 }
 
