@@ -13,7 +13,9 @@ from .ledger import CopyLedger
 from .loop import (Condition, DeviceCond, LoopReport, LoopState, loop_stencil_reduce,
                    loop_stencil_reduce_d, loop_stencil_reduce_i, loop_stencil_reduce_s,
                    stop_after)
-from .partition import (DeploymentMode, DeviceExecutor, DeviceRows, Partition, PartitionSet,
+from .loop import SequentialExecutor
+from .partition import (BlockInfo, DeploymentMode, DeviceExecutor, DeviceRows, ParallelExecutor,
+                        Partition, PartitionSet,
                         WorkerGroup, halo_exchange, model_ledger, parallel_loop, parallel_step,
                         partition)
 from .patterns import (Combinator, Delta, DeviceKernel, DeviceUnsupported, ElementalFn,

@@ -767,6 +767,30 @@ class DeviceExecutor(Executor):
         N.check(rc)
 
 
+class ParallelExecutor(DeviceExecutor):
+    """The reference's partitioned executor (partition.py:596-664) by name:
+    `partitions` row partitions on the GPU (a DeviceExecutor)."""
+
+    def __init__(self, partitions: int, group: Optional[WorkerGroup] = None):
+        super().__init__(partitions, group)
+
+
+@dataclass(frozen=True)
+class BlockInfo:
+    """Geometry of a padded block handed to a numpy block kernel
+    (partition.py:60-73): block[k + r, k + c] is global element (row0 + r, c);
+    `valid` marks the block cells inside the grid.  Kept for code that builds
+    or inspects block-kernel inputs; the device engine never calls numpy
+    block forms."""
+
+    row0: int
+    rows: int
+    cols: int
+    dims: tuple
+    k: int
+    valid: Any
+
+
 def parallel_loop(mode, partitions: int, k, f, op: Combinator, cond, a: Grid,
                   env: Any = None, *, delta=None, indexed: bool = False,
                   state: Optional[LoopState] = None,
