@@ -127,7 +127,9 @@ def _lit(v, t: str) -> str:
         v = int(v)
         if not -(1 << 63) <= v < (1 << 63):
             raise TranslateError(f"integer constant {v} does not fit 64 bits")
-        return f"({v}LL)" if v >= 0 else f"(-{-v}LL)" if v != -(1 << 63) else "(-9223372036854775807LL-1)"
+        if v == -(1 << 63):
+            return "(-9223372036854775807LL-1)"
+        return f"({v}LL)" if v >= 0 else f"(-{-v}LL)"
     f = float(v)
     if math.isnan(f):
         s = "__longlong_as_double(0x7ff8000000000000LL)"
@@ -780,10 +782,9 @@ class Translator:
         if name in self.local_vals:
             return self.local_vals[name]
         if name in self.types or name in self.new_types:
+            # (first typing pass: the type seen so far; its code is discarded)
             shape = self.types.get(name) or self.new_types.get(name)
             ok = f"v_{name}_ok" if name in self.absentable else None
-            if name not in self.types:  # first typing pass
-                return self._load(name, shape, ok)
             return self._load(name, shape, ok)
         if name in self.nonlocals:
             return self._pyval(self.nonlocals[name])
@@ -1037,8 +1038,7 @@ class Translator:
             t = INT
         self.tmp += 1
         acc, cnt, i = f"acc{self.tmp}", f"cnt{self.tmp}", f"q{self.tmp}"
-        init = "0" if how in ("sum", "len") else "0"
-        self.emit(f"{CTYPE[t] if how != 'len' else 'long long'} {acc} = {init}; long long {cnt} = 0;")
+        self.emit(f"{CTYPE[t] if how != 'len' else 'long long'} {acc} = 0; long long {cnt} = 0;")
         if how == "sum" and t == F64:
             self.emit(f"double {acc}c = 0.0;")
         cntw, ea, eb = self._win_slots(i)
