@@ -305,6 +305,102 @@ __device__ __forceinline__ unsigned sobel_byte(unsigned gxm, unsigned gym) {
 #endif
 }
 
+// ------------------------------------------------- Sobel, paired fp32 (f32x2)
+// Blackwell issues fp32 add/mul/fma on register PAIRS (FADD2/FMUL2/FFMA2):
+// one instruction, two lanes.  A thread's 8 pixels x0..x7 are held as four
+// pairs Q_k = (x_k, x_{k+4}), so the left/right neighbour pairs of Q_k are
+// simply Q_{k-1} / Q_{k+1} (plus two edge pairs (x_-1, x_3), (x_4, x_8)).
+// Each byte becomes the exact float 2^23 + 256 x with ONE PRMT (the byte in
+// mantissa bits 8..15 under the exponent word K); the bias cancels in every
+// feature (D = R - L, S = L + 2Q + R = 4 * 2^23 + 256 s, exact below 2^26
+// because 256 s is a multiple of the ulp 4), so features and outputs are the
+// integer Sobel quantities scaled by 256 with no conversion instructions:
+//   gx*256 = Dm + 2 Dc + Dp,  gy*256 = Sp - Sm,  n*2^16 = gx^2 + gy^2 (exact,
+//   < 2^37 with 21 significant bits),  sqrt -> 256 sqrt(n) (same relative
+//   error as unscaled: the scale is an even power of two),
+//   rint: s * 2^-8 + 1.5 * 2^23 in one FFMA (one rounding, half-to-even),
+//   leaving rint(sqrt(n)) <= 1443 in the low 16 bits; the clip to 255 is one
+//   VIMNMX.U16x2 per two pixels after packing.
+struct F2 {
+  unsigned long long v;
+};
+__device__ __forceinline__ F2 f2_pack(float lo, float hi) {
+  F2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r.v) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void f2_unpack(F2 a, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a.v));
+}
+__device__ __forceinline__ F2 f2_add(F2 a, F2 b) {
+  F2 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+  return r;
+}
+__device__ __forceinline__ F2 f2_sub(F2 a, F2 b) {
+  F2 r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+  return r;
+}
+__device__ __forceinline__ F2 f2_mul(F2 a, F2 b) {
+  F2 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+  return r;
+}
+__device__ __forceinline__ F2 f2_fma(F2 a, F2 b, F2 c) {
+  F2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.v) : "l"(a.v), "l"(b.v), "l"(c.v));
+  return r;
+}
+__device__ __forceinline__ F2 f2_splat(float x) { return f2_pack(x, x); }
+
+// byte k (0..3) of w -> float 2^23 + 256 * byte (K = 0x4B000000)
+template <int k>
+__device__ __forceinline__ float byte_f(unsigned w, unsigned K) {
+  return __uint_as_float(__byte_perm(w, K, 0x7604u | (k << 4)));
+}
+
+// rint(s / 256) in the low 16 bits of the returned word (s = 256 sqrt(n))
+__device__ __forceinline__ void sobel_round2(F2 n, unsigned& lo, unsigned& hi) {
+  float a, b;
+  f2_unpack(n, a, b);
+  asm("sqrt.approx.ftz.f32 %0, %0;" : "+f"(a));
+  asm("sqrt.approx.ftz.f32 %0, %0;" : "+f"(b));
+  F2 r = f2_fma(f2_pack(a, b), f2_splat(0.00390625f), f2_splat(12582912.0f));
+  float x, y;
+  f2_unpack(r, x, y);
+  lo = __float_as_uint(x);
+  hi = __float_as_uint(y);
+}
+
+#ifndef SK_SOBEL_MINB
+#define SK_SOBEL_MINB 5
+#endif
+
+// cp.async primitives (shared addresses are 32-bit)
+__device__ __forceinline__ void cp_async8(unsigned dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async4_if(bool p, unsigned dst, const void* src) {
+  asm volatile(
+      "{ .reg .pred q; setp.ne.b32 q, %0, 0; @q cp.async.ca.shared.global [%1], [%2], 4; }" ::"r"(
+          (int)p),
+      "r"(dst), "l"(src)
+      : "memory");
+}
+__device__ __forceinline__ void st_global_if(bool p, void* q, unsigned v) {
+  asm volatile("{ .reg .pred r; setp.ne.b32 r, %0, 0; @r st.global.u32 [%1], %2; }" ::"r"((int)p),
+               "l"(q), "r"(v)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 // One border pixel with the reference's rule (off-image reads = centre),
 // reading the three rows straight from memory.  Out of line: border work is
 // rare, and inlining it would bloat the hot loop's instruction footprint.
@@ -320,15 +416,20 @@ __device__ __noinline__ unsigned sobel_border_px(const unsigned char* front, lon
   return (unsigned)sobel_mag(-nw + ne - 2 * w + 2 * e - sw + se, -nw - 2 * n - ne + sw + 2 * so + se);
 }
 
-template <int BLOCK, int REDUCE, bool BATCH>
-__global__ void __launch_bounds__(BLOCK) sobel_sweep(const __grid_constant__ U8Args a) {
+template <int BLOCK, int REDUCE, bool BATCH, bool PAIRED>
+__global__ void __launch_bounds__(BLOCK, PAIRED ? SK_SOBEL_MINB : 1) sobel_sweep(const __grid_constant__ U8Args a) {
   constexpr int VEC = 8;
   constexpr int U = 6;  // multiple of the 3-row feature rotation: no register moves
   constexpr unsigned FULL = 0xffffffffu;
   __shared__ double sh[BLOCK / 32];
+  // PAIRED: per-warp ring of RING input-row slots
+  constexpr int RING = 8, SLOT = 288;
+  __shared__ __align__(128) unsigned char ring_mem[PAIRED ? (BLOCK / 32) * RING * SLOT : 16];
   unsigned K;  // 0x4B000000, opaque to the compiler (see lane_lo)
   asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(K) : "l"(a.magic));
   const Sweep2D& g = a.g;
+  const unsigned ring = (unsigned)__cvta_generic_to_shared(ring_mem) +
+                        (PAIRED ? (threadIdx.x >> 5) * RING * SLOT : 0u);
   for (long long it = BATCH ? 1 : loop_enter(a.L); it != 0;
        it = BATCH ? 0 : loop_next<BLOCK>(a.L, it, sh)) {
   const int lane = threadIdx.x & 31;
@@ -425,6 +526,136 @@ __global__ void __launch_bounds__(BLOCK) sobel_sweep(const __grid_constant__ U8A
 
     unsigned acc = 0;
     int accm = -1;
+    auto finish = [&](unsigned lo, unsigned hi, unsigned char* q) {
+      lo &= mlo;
+      hi &= mhi;
+      if (REDUCE == SK_REDUCE_MAX) {
+        const unsigned m = __vmaxu4(lo, hi);
+        const unsigned m2 = __vmaxu4(m, m >> 16);
+        accm = max(accm, (int)max(m2 & 0xffu, (m2 >> 8) & 0xffu));
+      } else {
+        acc = __dp4a(lo, 0x01010101u, acc);
+        acc = __dp4a(hi, 0x01010101u, acc);
+      }
+      if (active) *reinterpret_cast<uint2*>(q) = make_uint2(lo, hi);
+    };
+    if constexpr (PAIRED) {
+    // Input rows stream through the warp's shared-memory ring by cp.async,
+    // RING - 1 rows ahead of the row being consumed, so the bytes in flight
+    // cost no registers.  Slot byte 16 + j holds column cb*256 + j: each lane
+    // copies its own 8 bytes plus the 4-byte words either side of them (the
+    // inner ones duplicate a neighbour lane's bytes; the outer ones are the
+    // warp's left / right neighbour columns), so every lane runs the same
+    // copy pattern with immediate offsets.  Bytes outside the image only
+    // reach masked lanes or border pixels, which the border pass redoes.
+    const int n_in = r1 - r0 + 2;  // input rows r0-1 .. r1, clamped to the image
+    const unsigned dst = ring + 16 + lane * VEC;  // this lane's bytes in slot 0
+    const bool cpl = lcol > 0, cpr = nvalid > VEC;  // neighbour words inside the row
+    // copies past the chunk's last input row repeat that row (an L2 hit)
+    const int rlim = r1 < rows - 1 ? r1 : rows - 1;
+    const unsigned fp32 = (unsigned)fp;  // pitches < 2^31 (checked by the host)
+    int ri = r0 - 1;  // image row of the next copy
+    auto issue = [&](unsigned so) {  // one commit group per call
+      const unsigned rc = (unsigned)min(max(ri, 0), rlim);
+      const unsigned char* p;  // pbase + rc * pitch in one IMAD.WIDE.U32
+      asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(p) : "r"(rc), "r"(fp32), "l"(pbase));
+      cp_async8(dst + so, p);
+      cp_async4_if(cpl, dst + so - 4, p - 4);
+      cp_async4_if(cpr, dst + so + VEC, p + VEC);
+      cp_async_commit();
+      ++ri;
+    };
+    // Compute layout (independent of the copy layout): lane j owns pixel
+    // quads X = columns c0+4j .. +3 and Y = c0+128+4j .. +3, paired as
+    // Q_t = (x_t, y_t); the neighbour pairs are (x_-1, y_-1) and (x_4, y_4),
+    // all read from the slot, so no value sits in two register pairs.
+    const int colx = cb * (32 * VEC) + lane * 4;
+    const unsigned qx = ring + 16 + lane * 4;  // X quad in slot 0 (Y at +128)
+    const int nx = cols - colx, ny = nx - 128;
+    const unsigned mx = nx >= 4 ? 0xffffffffu : (nx <= 0 ? 0u : 0xffffffffu >> (32 - 8 * nx));
+    const unsigned my = ny >= 4 ? 0xffffffffu : (ny <= 0 ? 0u : 0xffffffffu >> (32 - 8 * ny));
+    // features of the input row in slot `so`; its slot is then refilled
+    auto take = [&](unsigned so, F2* S, F2* D) {
+      cp_async_wait<RING - 1>();
+      __syncwarp();  // the slot holds bytes copied by other lanes
+      const unsigned px = qx + so;
+      unsigned wx, wy, xl, xr, yl, yr;
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(wx) : "r"(px) : "memory");
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(wy) : "r"(px + 128) : "memory");
+      asm volatile("ld.shared.u8 %0, [%1];" : "=r"(xl) : "r"(px - 1) : "memory");
+      asm volatile("ld.shared.u8 %0, [%1];" : "=r"(xr) : "r"(px + 4) : "memory");
+      asm volatile("ld.shared.u8 %0, [%1];" : "=r"(yl) : "r"(px + 127) : "memory");
+      asm volatile("ld.shared.u8 %0, [%1];" : "=r"(yr) : "r"(px + 132) : "memory");
+      __syncwarp();  // slot fully read
+      issue(so);
+      const F2 Q0 = f2_pack(byte_f<0>(wx, K), byte_f<0>(wy, K));
+      const F2 Q1 = f2_pack(byte_f<1>(wx, K), byte_f<1>(wy, K));
+      const F2 Q2 = f2_pack(byte_f<2>(wx, K), byte_f<2>(wy, K));
+      const F2 Q3 = f2_pack(byte_f<3>(wx, K), byte_f<3>(wy, K));
+      const F2 L0 = f2_pack(byte_f<0>(xl, K), byte_f<0>(yl, K));
+      const F2 R3 = f2_pack(byte_f<0>(xr, K), byte_f<0>(yr, K));
+      const F2 two = f2_splat(2.0f);
+      S[0] = f2_fma(Q0, two, f2_add(L0, Q1));
+      S[1] = f2_fma(Q1, two, f2_add(Q0, Q2));
+      S[2] = f2_fma(Q2, two, f2_add(Q1, Q3));
+      S[3] = f2_fma(Q3, two, f2_add(Q2, R3));
+      D[0] = f2_sub(Q1, L0);
+      D[1] = f2_sub(Q2, Q0);
+      D[2] = f2_sub(Q3, Q1);
+      D[3] = f2_sub(R3, Q2);
+    };
+    // Running state at input row i: G = D(i-2) + 2 D(i-1) (gx of output row
+    // i-1 before its lower neighbour), S(i-2), S(i-1), D(i-1).  Output row
+    // i-1 = (G + D(i), S(i) - S(i-2)).  Two S and two D arrays alternate, so
+    // a pair of steps needs no register moves.
+    F2 G[4], SA[4], SB[4], DA[4], DB[4];
+    unsigned char* po = back + (long long)r0 * op + colx;
+    const F2 two_c = f2_splat(2.0f);
+    auto step = [&](unsigned so, F2* Sold, F2* Dprev, F2* Dnew) {
+      F2 S[4];
+      take(so, S, Dnew);
+      unsigned o[8];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const F2 gx = f2_add(G[k], Dnew[k]);
+        const F2 gy = f2_sub(S[k], Sold[k]);
+        sobel_round2(f2_fma(gx, gx, f2_mul(gy, gy)), o[k], o[k + 4]);
+        G[k] = f2_fma(Dnew[k], two_c, Dprev[k]);
+        Sold[k] = S[k];
+      }
+      const unsigned x01 = __vminu2(__byte_perm(o[0], o[1], 0x5410u), 0x00ff00ffu);
+      const unsigned x23 = __vminu2(__byte_perm(o[2], o[3], 0x5410u), 0x00ff00ffu);
+      const unsigned y01 = __vminu2(__byte_perm(o[4], o[5], 0x5410u), 0x00ff00ffu);
+      const unsigned y23 = __vminu2(__byte_perm(o[6], o[7], 0x5410u), 0x00ff00ffu);
+      const unsigned ox = __byte_perm(x01, x23, 0x6420u) & mx;
+      const unsigned oy = __byte_perm(y01, y23, 0x6420u) & my;
+      if (REDUCE == SK_REDUCE_MAX) {
+        const unsigned m = __vmaxu4(ox, oy);
+        const unsigned m2 = __vmaxu4(m, m >> 16);
+        accm = max(accm, (int)max(m2 & 0xffu, (m2 >> 8) & 0xffu));
+      } else {
+        acc = __dp4a(ox, 0x01010101u, acc);
+        acc = __dp4a(oy, 0x01010101u, acc);
+      }
+      st_global_if(nx > 0, po, ox);  // predicated, no branch
+      st_global_if(ny > 0, po + 128, oy);
+      po += op;
+    };
+#pragma unroll
+    for (int u = 0; u < RING; ++u) issue(u * SLOT);
+    take(0, SA, DA);  // input row 0 (r0-1): S in SA, D in DA
+    take(SLOT, SB, DB);  // input row 1 (r0)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) G[k] = f2_fma(DB[k], two_c, DA[k]);
+    // step i: S(i-2) is in SA for even i, SB for odd i; D(i-1) in DB / DA
+    int i = 2;
+#pragma unroll 1
+    for (; i + 2 <= n_in; i += 2) {
+      step((i & (RING - 1)) * SLOT, SA, DB, DA);
+      step(((i + 1) & (RING - 1)) * SLOT, SB, DA, DB);
+    }
+    if (i < n_in) step((i & (RING - 1)) * SLOT, SA, DB, DA);
+    } else {
     unsigned S0[4], D0[4], S1[4], D1[4], S2[4], D2[4];
     {
       uint2 w;
@@ -485,6 +716,7 @@ __global__ void __launch_bounds__(BLOCK) sobel_sweep(const __grid_constant__ U8A
         D1[i] = D2[i];
       }
     }
+    }  // SWAR
     // Border pass: pixels of image rows 0 / rows-1 and columns 0 / cols-1
     // follow the centre-substitution rule.  Border rows: each lane redoes its
     // own 8 pixels.  Border columns: the warp's lanes split the chunk's rows
@@ -547,15 +779,31 @@ namespace {
 
 constexpr int kBlock = 128;
 constexpr int kVec = 8;
+// Sobel feature form: f32x2 pairs (default) or the 16-bit SWAR kernel
+// (SK_SOBEL_SWAR=1, kept for A/B measurement)
+bool sobel_swar() {
+  static const bool v = [] {
+    const char* e = getenv("SK_SOBEL_SWAR");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
 
 using U8Fn = void (*)(const U8Args);
 
-U8Fn pick(int op, int reduce, bool batch) {
-  if (batch) return op == U8_SOBEL ? sobel_sweep<kBlock, SK_REDUCE_SUM, true>
+// aligned16: every row start the sweep reads is 16-byte aligned (the
+// bulk-copy ring needs it); otherwise Sobel takes the SWAR kernel
+U8Fn pick(int op, int reduce, bool batch, bool aligned16) {
+  if (op == U8_SOBEL && (sobel_swar() || !aligned16)) {
+    if (batch) return sobel_sweep<kBlock, SK_REDUCE_SUM, true, false>;
+    return reduce == SK_REDUCE_MAX ? sobel_sweep<kBlock, SK_REDUCE_MAX, false, false>
+                                   : sobel_sweep<kBlock, SK_REDUCE_SUM, false, false>;
+  }
+  if (batch) return op == U8_SOBEL ? sobel_sweep<kBlock, SK_REDUCE_SUM, true, true>
                                    : u8_sweep<U8_LIFE, kBlock, SK_REDUCE_SUM, true>;
   if (op == U8_SOBEL)
-    return reduce == SK_REDUCE_MAX ? sobel_sweep<kBlock, SK_REDUCE_MAX, false>
-                                   : sobel_sweep<kBlock, SK_REDUCE_SUM, false>;
+    return reduce == SK_REDUCE_MAX ? sobel_sweep<kBlock, SK_REDUCE_MAX, false, true>
+                                   : sobel_sweep<kBlock, SK_REDUCE_SUM, false, true>;
   return reduce == SK_REDUCE_MAX ? u8_sweep<U8_LIFE, kBlock, SK_REDUCE_MAX, false>
                                  : u8_sweep<U8_LIFE, kBlock, SK_REDUCE_SUM, false>;
 }
@@ -591,6 +839,13 @@ int geometry(int device, U8Fn fn, long long rows, long long cols, int nparts, co
 
 int op_of(const sk_run* r) { return r->plan.kernel == SK_KERNEL_LIFE ? U8_LIFE : U8_SOBEL; }
 
+bool aligned16(const sk_run* r) {
+  auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  return r->src_pitch % 16 == 0 && r->pitch % 16 == 0 && r->src_pitch < (1ll << 31) &&
+         r->pitch < (1ll << 31) && al(r->src) && al(r->buf[0]) &&
+         al(r->buf[1]);
+}
+
 int setup(sk_run* r) {
   if (r->plan.dtype != SK_U8) {
     set_error("sobel/life: grid must be u8");
@@ -600,7 +855,7 @@ int setup(sk_run* r) {
     set_error("sobel/life: no delta reduce");
     return SK_ERR_UNSUPPORTED;
   }
-  U8Fn fn = pick(op_of(r), r->plan.reduce_op, false);
+  U8Fn fn = pick(op_of(r), r->plan.reduce_op, false, aligned16(r));
   return geometry(r->device, fn, r->plan.rows, r->plan.cols, r->nparts, r->part_row, 1,
                   &r->colblocks, &r->chunk_rows, r->part_chunk, &r->nchunks, &r->grid);
 }
@@ -626,7 +881,7 @@ int launch(sk_run* r, const LoopCtl& L, cudaStream_t s) {
   a.magic = magic_ptr();
   fill_geom(r, a.g);
   a.L = L;
-  U8Fn fn = pick(op_of(r), r->plan.reduce_op, false);
+  U8Fn fn = pick(op_of(r), r->plan.reduce_op, false, aligned16(r));
   SK_CUDA(launch_kernel(fn, r->grid, kBlock, a, s, L.persistent != 0));
   return SK_OK;
 }
@@ -652,7 +907,9 @@ int sobel_frames(const uint8_t* in, long long in_pitch, long long in_fs, uint8_t
   }
   int dev = 0;
   SK_CUDA(cudaGetDevice(&dev));
-  U8Fn fn = pick(U8_SOBEL, SK_REDUCE_SUM, true);
+  const bool al16 = in_pitch % 16 == 0 && in_fs % 16 == 0 && in_pitch < (1ll << 31) &&
+                    (reinterpret_cast<uintptr_t>(in) & 15) == 0;
+  U8Fn fn = pick(U8_SOBEL, SK_REDUCE_SUM, true, al16);
   U8Args a{};
   a.magic = magic_ptr();
   int part_row[2] = {0, (int)rows};
