@@ -202,6 +202,11 @@ def c2(args, ClockSampler, measured_peaks, local=0, world=1, rank=0):
     s, e = _events()
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
+        # GPU-side gate (outside the timed region): the host enqueues all K
+        # steps while the GPU spins ~20 ms, so a host-side hiccup (page
+        # faults, GC, the clock sampler's fork) cannot open gaps between the
+        # timed launches; the events still bracket exactly the K steps
+        torch.cuda._sleep(40_000_000)
         s.record()
         for _ in range(args.steps):
             step(ev)
@@ -254,7 +259,7 @@ def c2(args, ClockSampler, measured_peaks, local=0, world=1, rank=0):
                      "frac": ach / peak, "traffic": _traffic("sobel_2048_per_frame", B),
                      "avg_kernel_ms": kms,
                      "kernel": f"sobel_sweep batched ({B} frames/launch), 2 B/pixel",
-                     "note": "instruction-issue-bound (70% issue-active): exact per-pixel sqrt/round path",
+                     "note": "issue-bound: f32x2 features, exact per-pixel sqrt/round path (profiles/r01e_ncu_sobel.json)",
                      "peak_source": pk},
         "cpu_baseline": None if cpu is None else
         {"value": cpu, "unit": "frames/s", "cores": cores, "kind": "port", "sample": sample},

@@ -28,6 +28,7 @@ struct AmfArgs {
   int rows, cols, frames, wmax;
   int tiles_x, tiles_per_frame;
   long long* counts;  // batch mode: per-frame flagged count
+  unsigned* work;     // batch mode: the stream's chunk counter (stream_counter)
   LoopCtl L;          // loop mode
   const void* src;    // loop mode: iteration-1 front
   void* buf[2];
@@ -125,7 +126,10 @@ __global__ void __launch_bounds__(kTW * kTH) amf_kernel(const __grid_constant__ 
   const int tid = threadIdx.x;  // 1D block: (tx, ty) = (tid % kTW, tid / kTW)
   const int txl = tid % kTW, tyl = tid / kTW;
   const int K2 = a.wmax / 2;
-  for (int c = next_chunk(a.L, &s_chunk); c < total; c = next_chunk(a.L, &s_chunk)) {
+  auto next = [&]() {
+    return BATCH ? next_chunk_stream(a.work, total, &s_chunk) : next_chunk(a.L, &s_chunk);
+  };
+  for (int c = next(); c < total; c = next()) {
     const int frame = BATCH ? c / a.tiles_per_frame : 0;
     const int t = c - frame * a.tiles_per_frame;
     const int ty0 = (t / a.tiles_x) * kTH, tx0 = (t % a.tiles_x) * kTW;
@@ -270,15 +274,12 @@ int amf_frames(const uint8_t* in, long long in_pitch, long long in_fs, uint8_t* 
   a.tiles_per_frame = a.tiles_x * (int)((rows + kTH - 1) / kTH);
   a.counts = counts;
   a.L.nparts = 1;
-  Status* st = nullptr;
-  SK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&st), sizeof(Status), s));
-  SK_CUDA(cudaMemsetAsync(st, 0, sizeof(Status), s));
+  a.work = stream_counter(dev, s);
+  if (!a.work) return SK_ERR_CUDA;
   SK_CUDA(cudaMemsetAsync(counts, 0, sizeof(long long) * frames, s));
-  a.L.st = st;
   const long long tiles = (long long)a.tiles_per_frame * frames;
   pick<true>(wmax)<<<grid_for(dev, (const void*)pick<true>(wmax), tiles), kTW * kTH, 0, s>>>(a);
   cudaError_t e = cudaGetLastError();
-  cudaFreeAsync(st, s);
   if (e != cudaSuccess) return cuda_fail(e, "amf_frames launch");
   return SK_OK;
 }

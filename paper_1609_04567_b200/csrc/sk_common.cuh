@@ -215,6 +215,20 @@ __device__ __forceinline__ int next_chunk(const LoopCtl& L, int* s_chunk) {
   return *s_chunk;
 }
 
+// The same from a stream's self-resetting counter (stream_counter): each CTA
+// fetches exactly once past `total`, so fetch total + gridDim.x - 1 is the
+// launch's last use of the counter and puts it back to 0.
+__device__ __forceinline__ int next_chunk_stream(unsigned* work, int total, int* s_chunk) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int c = (int)atomicAdd(work, 1u);
+    if (c == total + (int)gridDim.x - 1) *work = 0u;
+    *s_chunk = c;
+  }
+  __syncthreads();
+  return *s_chunk;
+}
+
 // The engine's own reduce ops (SUM / MAX, patterns.py:195-211).  JIT
 // kernels pass their user combinator instead (same interface).
 struct OpCombine {

@@ -49,6 +49,11 @@ int begin_impl(const sk_plan* plan, const sk_jit* jit, const void* d_src, int64_
 
 int device_sms(int device);
 
+// A device word that is 0 whenever no kernel on stream `s` is running: the
+// chunk counter of one-launch batched kernels, which reset it before they
+// exit (allocated once per (device, stream), never freed).
+unsigned* stream_counter(int device, cudaStream_t s);
+
 // Resident CTAs per SM for a kernel at a block size (cached per process: the
 // driver query costs tens of microseconds and runs are created per frame).
 int occupancy(const void* fn, int block);

@@ -35,6 +35,37 @@ int device_sms(int device) {
   return cache[device];
 }
 
+unsigned* stream_counter(int device, cudaStream_t s) {
+  constexpr int kSlab = 4096;
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, unsigned*> slots;
+  static unsigned* slab[64] = {};
+  static int used[64] = {};
+  std::lock_guard<std::mutex> lk(mu);
+  if (device < 0 || device >= 64) return nullptr;
+  auto key = std::make_pair(device, s);
+  auto it = slots.find(key);
+  if (it != slots.end()) return it->second;
+  unsigned* p = nullptr;
+  if (!slab[device]) {
+    if (cudaMalloc(reinterpret_cast<void**>(&slab[device]), kSlab * sizeof(unsigned)) != cudaSuccess ||
+        cudaMemset(slab[device], 0, kSlab * sizeof(unsigned)) != cudaSuccess) {
+      set_error("stream_counter: cannot allocate the counter slab");
+      slab[device] = nullptr;
+      return nullptr;
+    }
+  }
+  if (used[device] < kSlab) {
+    p = slab[device] + used[device]++;
+  } else if (cudaMalloc(reinterpret_cast<void**>(&p), sizeof(unsigned)) != cudaSuccess ||
+             cudaMemset(p, 0, sizeof(unsigned)) != cudaSuccess) {
+    set_error("stream_counter: cannot allocate a counter");
+    return nullptr;
+  }
+  slots[key] = p;
+  return p;
+}
+
 int occupancy(const void* fn, int block) {
   static std::mutex mu;
   static std::map<std::pair<const void*, int>, int> cache;

@@ -36,6 +36,7 @@ struct U8Args {
   int frames;
   int chunks_per_frame;
   const unsigned* magic;  // -> 0x4B000000 (Sobel lane extraction)
+  unsigned* work;         // BATCH: the stream's chunk counter (0 between launches)
 };
 
 __device__ const unsigned kMagicWord = 0x4B000000u;
@@ -98,9 +99,17 @@ __global__ void __launch_bounds__(BLOCK) u8_sweep(const __grid_constant__ U8Args
   const int cols = g.cols, rows = g.rows;
   const int total = BATCH ? a.frames * a.chunks_per_frame : a.L.part_chunk[a.L.nparts];
 
+  // chunks come from an atomic counter (loop mode: the run's; batched
+  // frames: the stream's, which the last fetch resets to 0 -- every warp
+  // makes exactly one fetch past the end, so fetch total + warps - 1 is the
+  // last use of the counter in this launch)
+  unsigned* const work = BATCH ? a.work : &a.L.st->work;
   for (;;) {
     int c = 0;
-    if (lane == 0) c = (int)atomicAdd(&a.L.st->work, 1u);
+    if (lane == 0) {
+      c = (int)atomicAdd(work, 1u);
+      if (BATCH && c == total + (int)(gridDim.x * (BLOCK / 32)) - 1) *work = 0u;
+    }
     c = __shfl_sync(FULL, c, 0);
     if (c >= total) break;
     int frame = 0, cb, r0, r1, cc = c;
@@ -310,63 +319,41 @@ __device__ __forceinline__ unsigned sobel_byte(unsigned gxm, unsigned gym) {
 // one instruction, two lanes.  A thread's 8 pixels x0..x7 are held as four
 // pairs Q_k = (x_k, x_{k+4}), so the left/right neighbour pairs of Q_k are
 // simply Q_{k-1} / Q_{k+1} (plus two edge pairs (x_-1, x_3), (x_4, x_8)).
-// Each byte becomes the exact float 2^23 + 256 x with ONE PRMT (the byte in
-// mantissa bits 8..15 under the exponent word K); the bias cancels in every
-// feature (D = R - L, S = L + 2Q + R = 4 * 2^23 + 256 s, exact below 2^26
-// because 256 s is a multiple of the ulp 4), so features and outputs are the
-// integer Sobel quantities scaled by 256 with no conversion instructions:
-//   gx*256 = Dm + 2 Dc + Dp,  gy*256 = Sp - Sm,  n*2^16 = gx^2 + gy^2 (exact,
-//   < 2^37 with 21 significant bits),  sqrt -> 256 sqrt(n) (same relative
-//   error as unscaled: the scale is an even power of two),
-//   rint: s * 2^-8 + 1.5 * 2^23 in one FFMA (one rounding, half-to-even),
-//   leaving rint(sqrt(n)) <= 1443 in the low 16 bits; the clip to 255 is one
+// Each byte becomes the exact float 2^15 + x with ONE PRMT (the byte in
+// mantissa bits 8..15 under the exponent word K2 = 0x47000000); the bias
+// cancels in every feature (D = R - L, S = L + 2Q + R = 2^17 + s, exact: the
+// ulp at 2^17 is 2^-6), so features and outputs are the integer Sobel
+// quantities with no conversion instructions:
+//   gx = Dm + 2 Dc + Dp,  gy = Sp - Sm,  n = gx^2 + gy^2 (exact, < 2^22),
+//   rint: sqrt(n) + 1.5 * 2^23 in one FADD (round half-to-even), leaving
+//   rint(sqrt(n)) <= 1443 in the low 16 bits; the clip to 255 is one
 //   VIMNMX.U16x2 per two pixels after packing.
-struct F2 {
-  unsigned long long v;
-};
-__device__ __forceinline__ F2 f2_pack(float lo, float hi) {
-  F2 r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r.v) : "f"(lo), "f"(hi));
-  return r;
-}
+// the CUDA 12.8+ sm_100 builtins (FADD2 / FMUL2 / FFMA2 on register pairs)
+using F2 = float2;
+__device__ __forceinline__ F2 f2_pack(float lo, float hi) { return make_float2(lo, hi); }
 __device__ __forceinline__ void f2_unpack(F2 a, float& lo, float& hi) {
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a.v));
+  lo = a.x;
+  hi = a.y;
 }
-__device__ __forceinline__ F2 f2_add(F2 a, F2 b) {
-  F2 r;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
-  return r;
-}
-__device__ __forceinline__ F2 f2_sub(F2 a, F2 b) {
-  F2 r;
-  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
-  return r;
-}
-__device__ __forceinline__ F2 f2_mul(F2 a, F2 b) {
-  F2 r;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
-  return r;
-}
-__device__ __forceinline__ F2 f2_fma(F2 a, F2 b, F2 c) {
-  F2 r;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.v) : "l"(a.v), "l"(b.v), "l"(c.v));
-  return r;
-}
+__device__ __forceinline__ F2 f2_add(F2 a, F2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ F2 f2_sub(F2 a, F2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+__device__ __forceinline__ F2 f2_mul(F2 a, F2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ F2 f2_fma(F2 a, F2 b, F2 c) { return __ffma2_rn(a, b, c); }
 __device__ __forceinline__ F2 f2_splat(float x) { return f2_pack(x, x); }
 
-// byte k (0..3) of w -> float 2^23 + 256 * byte (K = 0x4B000000)
+// byte k (0..3) of w -> float 2^15 + byte (K2 = 0x47000000)
 template <int k>
 __device__ __forceinline__ float byte_f(unsigned w, unsigned K) {
   return __uint_as_float(__byte_perm(w, K, 0x7604u | (k << 4)));
 }
 
-// rint(s / 256) in the low 16 bits of the returned word (s = 256 sqrt(n))
+// rint(sqrt(n)) in the low 16 bits of each returned word
 __device__ __forceinline__ void sobel_round2(F2 n, unsigned& lo, unsigned& hi) {
   float a, b;
   f2_unpack(n, a, b);
   asm("sqrt.approx.ftz.f32 %0, %0;" : "+f"(a));
   asm("sqrt.approx.ftz.f32 %0, %0;" : "+f"(b));
-  F2 r = f2_fma(f2_pack(a, b), f2_splat(0.00390625f), f2_splat(12582912.0f));
+  F2 r = f2_add(f2_pack(a, b), f2_splat(12582912.0f));
   float x, y;
   f2_unpack(r, x, y);
   lo = __float_as_uint(x);
@@ -376,6 +363,10 @@ __device__ __forceinline__ void sobel_round2(F2 n, unsigned& lo, unsigned& hi) {
 #ifndef SK_SOBEL_MINB
 #define SK_SOBEL_MINB 5
 #endif
+#ifndef SK_SOBEL_UNROLL
+#define SK_SOBEL_UNROLL 2
+#endif
+constexpr int kSobelUnroll = SK_SOBEL_UNROLL;
 
 // cp.async primitives (shared addresses are 32-bit)
 __device__ __forceinline__ void cp_async8(unsigned dst, const void* src) {
@@ -427,6 +418,7 @@ __global__ void __launch_bounds__(BLOCK, PAIRED ? SK_SOBEL_MINB : 1) sobel_sweep
   __shared__ __align__(128) unsigned char ring_mem[PAIRED ? (BLOCK / 32) * RING * SLOT : 16];
   unsigned K;  // 0x4B000000, opaque to the compiler (see lane_lo)
   asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(K) : "l"(a.magic));
+  const unsigned K2 = K - 0x04000000u;  // 0x47000000: exponent word of 2^15 (PAIRED)
   const Sweep2D& g = a.g;
   const unsigned ring = (unsigned)__cvta_generic_to_shared(ring_mem) +
                         (PAIRED ? (threadIdx.x >> 5) * RING * SLOT : 0u);
@@ -436,9 +428,17 @@ __global__ void __launch_bounds__(BLOCK, PAIRED ? SK_SOBEL_MINB : 1) sobel_sweep
   const int cols = g.cols, rows = g.rows;
   const int total = BATCH ? a.frames * a.chunks_per_frame : a.L.part_chunk[a.L.nparts];
 
+  // chunks come from an atomic counter (loop mode: the run's; batched
+  // frames: the stream's, which the last fetch resets to 0 -- every warp
+  // makes exactly one fetch past the end, so fetch total + warps - 1 is the
+  // last use of the counter in this launch)
+  unsigned* const work = BATCH ? a.work : &a.L.st->work;
   for (;;) {
     int c = 0;
-    if (lane == 0) c = (int)atomicAdd(&a.L.st->work, 1u);
+    if (lane == 0) {
+      c = (int)atomicAdd(work, 1u);
+      if (BATCH && c == total + (int)(gridDim.x * (BLOCK / 32)) - 1) *work = 0u;
+    }
     c = __shfl_sync(FULL, c, 0);
     if (c >= total) break;
     int frame = 0, cb, r0, r1, cc = c;
@@ -541,7 +541,7 @@ __global__ void __launch_bounds__(BLOCK, PAIRED ? SK_SOBEL_MINB : 1) sobel_sweep
     };
     if constexpr (PAIRED) {
     // Input rows stream through the warp's shared-memory ring by cp.async,
-    // RING - 1 rows ahead of the row being consumed, so the bytes in flight
+    // RING - 2 rows ahead of the row being consumed, so the bytes in flight
     // cost no registers.  Slot byte 16 + j holds column cb*256 + j: each lane
     // copies its own 8 bytes plus the 4-byte words either side of them (the
     // inner ones duplicate a neighbour lane's bytes; the outer ones are the
@@ -576,7 +576,7 @@ __global__ void __launch_bounds__(BLOCK, PAIRED ? SK_SOBEL_MINB : 1) sobel_sweep
     const unsigned my = ny >= 4 ? 0xffffffffu : (ny <= 0 ? 0u : 0xffffffffu >> (32 - 8 * ny));
     // features of the input row in slot `so`; its slot is then refilled
     auto take = [&](unsigned so, F2* S, F2* D) {
-      cp_async_wait<RING - 1>();
+      cp_async_wait<RING - 2>();
       __syncwarp();  // the slot holds bytes copied by other lanes
       const unsigned px = qx + so;
       unsigned wx, wy, xl, xr, yl, yr;
@@ -586,14 +586,15 @@ __global__ void __launch_bounds__(BLOCK, PAIRED ? SK_SOBEL_MINB : 1) sobel_sweep
       asm volatile("ld.shared.u8 %0, [%1];" : "=r"(xr) : "r"(px + 4) : "memory");
       asm volatile("ld.shared.u8 %0, [%1];" : "=r"(yl) : "r"(px + 127) : "memory");
       asm volatile("ld.shared.u8 %0, [%1];" : "=r"(yr) : "r"(px + 132) : "memory");
-      __syncwarp();  // slot fully read
-      issue(so);
-      const F2 Q0 = f2_pack(byte_f<0>(wx, K), byte_f<0>(wy, K));
-      const F2 Q1 = f2_pack(byte_f<1>(wx, K), byte_f<1>(wy, K));
-      const F2 Q2 = f2_pack(byte_f<2>(wx, K), byte_f<2>(wy, K));
-      const F2 Q3 = f2_pack(byte_f<3>(wx, K), byte_f<3>(wy, K));
-      const F2 L0 = f2_pack(byte_f<0>(xl, K), byte_f<0>(yl, K));
-      const F2 R3 = f2_pack(byte_f<0>(xr, K), byte_f<0>(yr, K));
+      // refill the slot read by the previous step (those reads are complete:
+      // this step's __syncwarp follows them)
+      issue(so == 0 ? (RING - 1) * SLOT : so - SLOT);
+      const F2 Q0 = f2_pack(byte_f<0>(wx, K2), byte_f<0>(wy, K2));
+      const F2 Q1 = f2_pack(byte_f<1>(wx, K2), byte_f<1>(wy, K2));
+      const F2 Q2 = f2_pack(byte_f<2>(wx, K2), byte_f<2>(wy, K2));
+      const F2 Q3 = f2_pack(byte_f<3>(wx, K2), byte_f<3>(wy, K2));
+      const F2 L0 = f2_pack(byte_f<0>(xl, K2), byte_f<0>(yl, K2));
+      const F2 R3 = f2_pack(byte_f<0>(xr, K2), byte_f<0>(yr, K2));
       const F2 two = f2_splat(2.0f);
       S[0] = f2_fma(Q0, two, f2_add(L0, Q1));
       S[1] = f2_fma(Q1, two, f2_add(Q0, Q2));
@@ -637,19 +638,19 @@ __global__ void __launch_bounds__(BLOCK, PAIRED ? SK_SOBEL_MINB : 1) sobel_sweep
         acc = __dp4a(ox, 0x01010101u, acc);
         acc = __dp4a(oy, 0x01010101u, acc);
       }
-      st_global_if(nx > 0, po, ox);  // predicated, no branch
-      st_global_if(ny > 0, po + 128, oy);
+      if (nx > 0) *reinterpret_cast<unsigned*>(po) = ox;
+      if (ny > 0) *reinterpret_cast<unsigned*>(po + 128) = oy;
       po += op;
     };
 #pragma unroll
-    for (int u = 0; u < RING; ++u) issue(u * SLOT);
+    for (int u = 0; u < RING - 1; ++u) issue(u * SLOT);
     take(0, SA, DA);  // input row 0 (r0-1): S in SA, D in DA
     take(SLOT, SB, DB);  // input row 1 (r0)
 #pragma unroll
     for (int k = 0; k < 4; ++k) G[k] = f2_fma(DB[k], two_c, DA[k]);
     // step i: S(i-2) is in SA for even i, SB for odd i; D(i-1) in DB / DA
     int i = 2;
-#pragma unroll 1
+#pragma unroll (kSobelUnroll)
     for (; i + 2 <= n_in; i += 2) {
       step((i & (RING - 1)) * SLOT, SA, DB, DA);
       step(((i + 1) & (RING - 1)) * SLOT, SB, DA, DB);
@@ -894,8 +895,8 @@ const KernelOps kOps = {setup, launch, teardown};
 
 const KernelOps* u8_ops() { return &kOps; }
 
-// Batched Sobel over frames (stream mode).  Uses a small device scratch for
-// the chunk counter (Status) allocated per call on the stream's pool.
+// Batched Sobel over frames (stream mode): one memset (the per-frame sums)
+// and one launch per call.
 int sobel_frames(const uint8_t* in, long long in_pitch, long long in_fs, uint8_t* out,
                  long long out_pitch, long long out_fs, int frames, long long rows, long long cols,
                  long long* sums, cudaStream_t s) {
@@ -931,14 +932,11 @@ int sobel_frames(const uint8_t* in, long long in_pitch, long long in_fs, uint8_t
   a.sums = sums;
   a.frames = frames;
   a.chunks_per_frame = nch;
-  Status* st = nullptr;
-  SK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&st), sizeof(Status), s));
-  SK_CUDA(cudaMemsetAsync(st, 0, sizeof(Status), s));
+  a.work = stream_counter(dev, s);
+  if (!a.work) return SK_ERR_CUDA;
   SK_CUDA(cudaMemsetAsync(sums, 0, sizeof(long long) * frames, s));
-  a.L.st = st;
   fn<<<grid, kBlock, 0, s>>>(a);
   cudaError_t e = cudaGetLastError();
-  cudaFreeAsync(st, s);
   if (e != cudaSuccess) return cuda_fail(e, "sobel_frames launch");
   return SK_OK;
 }

@@ -211,3 +211,34 @@ def test_restore_frames_batch_matches_single_frame_runs(golden_large):
         ref, ri, rv, rex = O.restore_loop(small[i], mk[i].cpu().numpy())
         assert reps[i].iterations == ri and reps[i].exhausted == rex, i
         assert np.array_equal(outs[i].cpu().numpy(), ref), i
+
+
+def test_batched_launches_reuse_stream_counters():
+    """Batched Sobel / AMF launches take chunks from a per-stream counter that
+    each launch resets on exit: many launches over several streams (and
+    interleaved Sobel / AMF on one stream) give the single-launch results."""
+    import torch
+
+    from paper_1609_04567_b200.apps import amf_frames
+
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    frames = torch.randint(0, 256, (6, 257, 300), dtype=torch.uint8, device="cuda", generator=gen)
+    fr16 = torch.zeros((6, 257, 304), dtype=torch.uint8, device="cuda")
+    fr16[:, :, :300] = frames
+    view = fr16[:, :, :300]  # 16-byte pitch: the ring kernel
+    ref_e, ref_s = sobel_frames(view)
+    ref_m, ref_c = amf_frames(view)
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in range(3)]
+    outs = []
+    for rep in range(4):
+        for i, st in enumerate(streams):
+            with torch.cuda.stream(st):
+                outs.append(sobel_frames(view, stream=st))
+                outs.append(amf_frames(view))
+    torch.cuda.synchronize()
+    for k, o in enumerate(outs):
+        if k % 2 == 0:
+            assert torch.equal(o[0], ref_e) and torch.equal(o[1], ref_s)
+        else:
+            assert torch.equal(o[0], ref_m) and torch.equal(o[1], ref_c)
