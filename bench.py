@@ -313,6 +313,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=32768)
+    ap.add_argument("--transport", default="peer", choices=["peer", "collective"],
+                    help="C4 with N>1: halo rows + partials by peer stores from the sweep "
+                         "kernel (default) or by NCCL send/recv + all-gather")
     ap.add_argument("--workload", default="c4", choices=["c1", "c2", "c3", "c4", "c5"],
                     help="BASELINE.json config (default c4: the cell-updates/s headline)")
     args = ap.parse_args()

@@ -164,6 +164,44 @@ int sk_run_value_ptr(sk_run* run, void** d_value);
  * enqueue several iterations ahead without reading anything back. */
 int sk_run_combine(sk_run* run, const double* d_partials, int32_t n, const sk_cond* cond);
 
+/* ---- peer transport (multi-GPU without a collective library) ----------
+ * Replaces the NCCL halo send/recv + all-gather of the reference's
+ * halo_exchange / partial fold (partition.py:247-262, 642-646) for ranks on
+ * one node.  The Helmholtz sweep stores its first / last owned row straight
+ * into the neighbours' halo rows (peer memory: NVLink, or the same device),
+ * and the launch's finalizing CTA writes this rank's value into every
+ * rank's mailbox and then the launch sequence number into every rank's
+ * flag word (system-scope fences in between).  The host then enqueues
+ * sk_run_peer_wait (a stream wait on the local flags -- no SM spins) and
+ * sk_run_combine over the local mailbox. */
+#define SK_MAX_PEERS 8
+
+typedef struct sk_peers {
+  int32_t rank, world; /* world in [2, SK_MAX_PEERS] */
+  void* up_rows[2];    /* rank-1's bottom halo row in its buf0 / buf1 (NULL on rank 0) */
+  void* down_rows[2];  /* rank+1's top halo row in its buf0 / buf1 (NULL on the last rank) */
+  double* mail[SK_MAX_PEERS];  /* rank p's mailbox, double[2][world] (mapped here) */
+  uint32_t* flags[SK_MAX_PEERS]; /* rank p's flag words, uint32[world], zero at start */
+} sk_peers;
+
+/* Attach the peer transport to a Helmholtz run (before its first launch);
+ * every later launch publishes its value and sequence number (1, 2, ...). */
+int sk_run_set_peers(sk_run* run, const sk_peers* peers);
+
+/* Enqueue on the run's stream: wait until every other rank has published
+ * launch `seq` (its flag word here >= seq).  The mailbox row to combine is
+ * mail[rank] + (seq & 1) * world. */
+int sk_run_peer_wait(sk_run* run, int64_t seq);
+
+/* Device memory that other processes can map (cudaMalloc + CUDA IPC):
+ * allocate (zeroed), export a 64-byte handle, map a peer's handle, unmap,
+ * free. */
+int sk_ipc_alloc(int64_t bytes, void** d_ptr);
+int sk_ipc_handle(void* d_ptr, uint8_t handle[64]);
+int sk_ipc_open(const uint8_t handle[64], void** d_ptr);
+int sk_ipc_close(void* d_ptr);
+int sk_ipc_free(void* d_ptr);
+
 /* Synchronise the run's stream and read its loop status: completed
  * iterations, the last combined value (cross-rank if sk_run_combine is used),
  * whether the loop stopped and whether the cap was hit. */

@@ -32,7 +32,11 @@ EXPORTS = (
     "sk_run_launches", "sk_run_destroy", "sk_verify_div_f32", "sk_sobel_frames",
     "sk_amf_frames", "sk_jit_compile", "sk_jit_log", "sk_jit_cubin_size", "sk_jit_cubin", "sk_jit_destroy",
     "sk_run_begin_jit", "sk_run_error",
+    "sk_run_set_peers", "sk_run_peer_wait", "sk_ipc_alloc", "sk_ipc_handle", "sk_ipc_open",
+    "sk_ipc_close", "sk_ipc_free",
 )
+
+SK_MAX_PEERS = 8
 
 
 class DeviceUnavailable(RuntimeError):
@@ -58,6 +62,12 @@ class sk_plan(C.Structure):
 class sk_cond(C.Structure):
     _fields_ = [("kind", C.c_int32), ("pad", C.c_int32), ("a", C.c_double), ("n", C.c_double),
                 ("max_iterations", C.c_int64)]
+
+
+class sk_peers(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("world", C.c_int32),
+                ("up_rows", C.c_void_p * 2), ("down_rows", C.c_void_p * 2),
+                ("mail", C.c_void_p * SK_MAX_PEERS), ("flags", C.c_void_p * SK_MAX_PEERS)]
 
 
 _lock = threading.Lock()
@@ -115,6 +125,13 @@ def _declare(lib):
         "sk_run_begin_jit": [C.POINTER(sk_plan), P, P, I64, C.POINTER(P), C.POINTER(I64), I32, P, P,
                              I64, P, C.POINTER(P)],
         "sk_run_error": [P, C.POINTER(I32), C.POINTER(I64), C.POINTER(I64)],
+        "sk_run_set_peers": [P, C.POINTER(sk_peers)],
+        "sk_run_peer_wait": [P, I64],
+        "sk_ipc_alloc": [I64, C.POINTER(P)],
+        "sk_ipc_handle": [P, C.c_char_p],
+        "sk_ipc_open": [C.c_char_p, C.POINTER(P)],
+        "sk_ipc_close": [P],
+        "sk_ipc_free": [P],
     }
     lib.sk_jit_log.argtypes = [P]
     lib.sk_jit_log.restype = C.c_char_p

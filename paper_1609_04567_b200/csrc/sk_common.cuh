@@ -54,6 +54,7 @@ struct Status {
 };
 
 constexpr int kMaxParts = 64;
+constexpr int kMaxPeers = 8;  // SK_MAX_PEERS
 
 struct CondDev {
   int kind;             // SK_COND_*
@@ -77,7 +78,27 @@ struct LoopCtl {
   cudaGraphConditionalHandle gh;
   int use_graph;
   int persistent;  // whole loop inside one cooperative launch (loop_barrier)
+  // multi-GPU peer transport (sk_run_set_peers; world 0 = off): every launch
+  // publishes this rank's value into each rank's mailbox, then its sequence
+  // number into each rank's flag word
+  struct {
+    int rank, world;
+    unsigned seq;
+    double* mail[kMaxPeers];
+    unsigned* flag[kMaxPeers];
+  } peer;
 };
+
+// Publish launch L.peer.seq: value -> mail[p][(seq & 1) * world + rank] for
+// every rank p, a system-scope fence (the caller fenced this launch's halo
+// rows already), then seq -> flag[p][rank].  One thread.
+__device__ __forceinline__ void peer_publish(const LoopCtl& L, double v) {
+  const int w = L.peer.world, me = L.peer.rank;
+  const unsigned q = L.peer.seq;
+  for (int p = 0; p < w; ++p) L.peer.mail[p][(q & 1u) * w + me] = v;
+  __threadfence_system();
+  for (int p = 0; p < w; ++p) *reinterpret_cast<volatile unsigned*>(L.peer.flag[p] + me) = q;
+}
 
 // ---------------------------------------------------------------- exact math
 // The reference evaluates numpy/Python expressions op by op: no fused
@@ -200,6 +221,9 @@ __device__ __forceinline__ long long loop_enter(const LoopCtl& L) {
 #ifndef __CUDACC_RTC__
     if (L.use_graph && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(L.gh, 0u);
 #endif
+    // launches after the decided stop still publish their sequence number:
+    // the peers' stream waits for it
+    if (L.peer.world > 1 && blockIdx.x == 0 && threadIdx.x == 0) peer_publish(L, 0.0);
     return 0;
   }
   return st->iter + 1;
@@ -316,7 +340,10 @@ __device__ void loop_finalize(const LoopCtl& L, long long it, double* sh, const 
   __shared__ int s_last;
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
+    // peer transport: this CTA's halo-row stores to the neighbours must be
+    // visible system-wide before the finalizer raises the flags
+    if (L.peer.world > 1) __threadfence_system();
+    else __threadfence();
     unsigned prev = atomicAdd(&L.st->ticket, 1u);
     s_last = (prev == gridDim.x - 1);
   }
@@ -326,6 +353,7 @@ __device__ void loop_finalize(const LoopCtl& L, long long it, double* sh, const 
   const int stop = fold_and_decide<BLOCK>(L, it, sh, pick_comb(L, comb));
   if (threadIdx.x == 0) {
     __threadfence_system();
+    if (L.peer.world > 1) peer_publish(L, ((volatile Status*)L.st)->value);
 #ifndef __CUDACC_RTC__
     if (L.use_graph) cudaGraphSetConditional(L.gh, stop ? 0u : 1u);
 #endif

@@ -46,6 +46,10 @@ struct HelmArgs {
   T ax, ay, b, keep, relax;
   int fast_div;  // b inside div_b_ok and verified: use div_const for safe numerators
   long long xpitch;  // resident loop: row stride of the edge-row exchange buffer
+  // peer transport (sk_run_set_peers): the neighbours' halo rows in their
+  // buf0 / buf1, written with this rank's first / last owned row
+  T* peer_up[2];
+  T* peer_dn[2];
 };
 
 __device__ __forceinline__ float rcp_rn(float b) { return __frcp_rn(b); }
@@ -77,6 +81,8 @@ __global__ void __launch_bounds__(BLOCK, (sizeof(T) == 8 ? (PERSIST ? 4 : SK_F64
   const T* env = static_cast<const T*>(g.env) + (long long)g.halo_top * g.env_pitch;
   const int lane = threadIdx.x & 31;
   const int cols = g.cols, rows = g.rows;
+  T* const peer_up = a.peer_up[it & 1];  // null unless the peer transport is on
+  T* const peer_dn = a.peer_dn[it & 1];
   const T ax = a.ax, ay = a.ay, b = a.b, keep = a.keep, relax = a.relax;
   const T rb = rcp_rn(b);
   const bool fast = a.fast_div != 0;
@@ -173,7 +179,13 @@ __global__ void __launch_bounds__(BLOCK, (sizeof(T) == 8 ? (PERSIST ? 4 : SK_F64
             s4 = xadd(xadd(dd[0], dd[1]), xadd(dd[2], dd[3]));
             accs += (double)s4;
           }
-          if (active) st4(po, o);
+          if (active) {
+            st4(po, o);
+            // boundary rows also land in the neighbours' halo rows (peer
+            // stores, overlapped with the rest of the sweep)
+            if (rr == 0 && peer_up) st4(peer_up + col, o);
+            if (rr == rows - 1 && peer_dn) st4(peer_dn + col, o);
+          }
           up = cen;
           cen = dn[u];
           pc += fp;
@@ -915,6 +927,10 @@ HelmArgs<T> helm_args(const sk_run* r, const LoopCtl& L) {
   a.relax = (T)p.params[4];
   a.fast_div = r->aux_n[0] ? 1 : 0;
   a.xpitch = 0;
+  for (int j = 0; j < 2; ++j) {
+    a.peer_up[j] = r->has_peers ? static_cast<T*>(r->peers.up_rows[j]) : nullptr;
+    a.peer_dn[j] = r->has_peers ? static_cast<T*>(r->peers.down_rows[j]) : nullptr;
+  }
   return a;
 }
 
@@ -950,7 +966,11 @@ template <typename T>
 int launch_t(sk_run* r, const LoopCtl& L, cudaStream_t s) {
   const sk_plan& p = r->plan;
   HelmArgs<T> a = helm_args<T>(r, L);
-  if (twostep_ok(r, L)) {
+  if (r->has_peers && L.persistent) {
+    set_error("helmholtz: the peer transport drives one launch per iteration");
+    return SK_ERR_UNSUPPORTED;
+  }
+  if (!r->has_peers && twostep_ok(r, L)) {
     Kernel2Fn<T> fn2 = pick2<T>(p.delta_op, p.reduce_op);
     if (fn2) {
       r->steps_per_launch = 2;

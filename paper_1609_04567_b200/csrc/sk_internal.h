@@ -128,6 +128,8 @@ struct sk_run {
   long long jit_env_pitch[4] = {};
   int jit_nenv = 0;
   bool no_graph = false;  // the kernel cannot drive a graph WHILE node
+  bool has_peers = false;  // peer transport attached (sk_run_set_peers)
+  sk_peers peers{};
   int steps_per_launch = 1;  // 2: launches compute iterations 2L+1, 2L+2 (results in buf[L & 1])
 
   // kernel-specific device state (restore: flagged list, change flags)

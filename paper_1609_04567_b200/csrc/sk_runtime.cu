@@ -8,6 +8,9 @@
 #include <mutex>
 #include <string>
 
+#include <cuda.h>
+#include <cstring>
+
 #include "sk_internal.h"
 
 namespace sk {
@@ -148,10 +151,26 @@ static LoopCtl make_ctl(sk_run* r, const sk_cond* c, bool graph, cudaGraphCondit
   L.gh = gh;
   L.use_graph = graph ? 1 : 0;
   L.persistent = 0;
+  L.peer.rank = L.peer.world = 0;
+  L.peer.seq = 0;
+  for (int p = 0; p < kMaxPeers; ++p) {
+    L.peer.mail[p] = nullptr;
+    L.peer.flag[p] = nullptr;
+  }
+  if (r->has_peers) {
+    L.peer.rank = r->peers.rank;
+    L.peer.world = r->peers.world;
+    for (int p = 0; p < r->peers.world; ++p) {
+      L.peer.mail[p] = r->peers.mail[p];
+      L.peer.flag[p] = r->peers.flags[p];
+    }
+  }
   return L;
 }
 
-static int launch_timed(sk_run* r, const LoopCtl& L) {
+static int launch_timed(sk_run* r, const LoopCtl& L0) {
+  LoopCtl L = L0;
+  L.peer.seq = (unsigned)(r->launched + 1);  // this launch's sequence number
   cudaEvent_t a = nullptr, b = nullptr;
   if (r->timing) {
     SK_CUDA(cudaEventCreate(&a));
@@ -540,6 +559,113 @@ int sk_run_combine(sk_run* r, const double* d_partials, int32_t n, const sk_cond
                                          r->plan.identity, cd, r->d_ring);
   SK_CUDA(cudaGetLastError());
   r->combined = true;
+  return SK_OK;
+}
+
+int sk_run_set_peers(sk_run* r, const sk_peers* p) {
+  if (!r || !p || p->world < 2 || p->world > SK_MAX_PEERS || p->rank < 0 || p->rank >= p->world) {
+    set_error("sk_run_set_peers: bad argument");
+    return SK_ERR_ARG;
+  }
+  if (r->plan.kernel != SK_KERNEL_HELMHOLTZ) {
+    set_error("sk_run_set_peers: the peer transport is implemented for the Helmholtz sweep");
+    return SK_ERR_UNSUPPORTED;
+  }
+  if (r->launched != 0) {
+    set_error("sk_run_set_peers: attach before the first launch");
+    return SK_ERR_STATE;
+  }
+  for (int q = 0; q < p->world; ++q)
+    if (!p->mail[q] || !p->flags[q]) {
+      set_error("sk_run_set_peers: every rank needs a mailbox and flag words");
+      return SK_ERR_ARG;
+    }
+  if ((p->rank > 0) != (p->up_rows[0] && p->up_rows[1]) ||
+      (p->rank < p->world - 1) != (p->down_rows[0] && p->down_rows[1]) ||
+      (p->rank > 0) != (r->plan.halo_top == 1) || (p->rank < p->world - 1) != (r->plan.halo_bottom == 1)) {
+    set_error("sk_run_set_peers: neighbour halo rows do not match the run's halo layout");
+    return SK_ERR_ARG;
+  }
+  r->peers = *p;
+  r->has_peers = true;
+  return SK_OK;
+}
+
+int sk_run_peer_wait(sk_run* r, int64_t seq) {
+  if (!r || !r->has_peers || seq < 1) {
+    set_error("sk_run_peer_wait: run has no peer transport, or bad sequence number");
+    return SK_ERR_ARG;
+  }
+  static decltype(&cuStreamWaitValue32) wait32 = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuStreamWaitValue32", &f, 12000, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      wait32 = reinterpret_cast<decltype(&cuStreamWaitValue32)>(f);
+  });
+  if (!wait32) {
+    set_error("sk_run_peer_wait: cuStreamWaitValue32 unavailable");
+    return SK_ERR_UNSUPPORTED;
+  }
+  const sk_peers& p = r->peers;
+  uint32_t* mine = p.flags[p.rank];
+  for (int q = 0; q < p.world; ++q) {
+    if (q == p.rank) continue;
+    CUresult e = wait32(reinterpret_cast<CUstream>(r->stream), reinterpret_cast<CUdeviceptr>(mine + q),
+                        (cuuint32_t)seq, CU_STREAM_WAIT_VALUE_GEQ);
+    if (e != CUDA_SUCCESS) {
+      set_error("sk_run_peer_wait: cuStreamWaitValue32 failed (" + std::to_string((int)e) + ")");
+      return SK_ERR_CUDA;
+    }
+  }
+  return SK_OK;
+}
+
+int sk_ipc_alloc(int64_t bytes, void** d_ptr) {
+  if (bytes < 1 || !d_ptr) {
+    set_error("sk_ipc_alloc: bad argument");
+    return SK_ERR_ARG;
+  }
+  SK_CUDA(cudaMalloc(d_ptr, (size_t)bytes));
+  SK_CUDA(cudaMemset(*d_ptr, 0, (size_t)bytes));
+  return SK_OK;
+}
+
+int sk_ipc_handle(void* d_ptr, uint8_t handle[64]) {
+  if (!d_ptr || !handle) {
+    set_error("sk_ipc_handle: null argument");
+    return SK_ERR_ARG;
+  }
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  cudaIpcMemHandle_t h;
+  SK_CUDA(cudaIpcGetMemHandle(&h, d_ptr));
+  memcpy(handle, &h, 64);
+  return SK_OK;
+}
+
+int sk_ipc_open(const uint8_t handle[64], void** d_ptr) {
+  if (!handle || !d_ptr) {
+    set_error("sk_ipc_open: null argument");
+    return SK_ERR_ARG;
+  }
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, 64);
+  SK_CUDA(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return SK_OK;
+}
+
+int sk_ipc_close(void* d_ptr) {
+  if (!d_ptr) return SK_OK;
+  SK_CUDA(cudaIpcCloseMemHandle(d_ptr));
+  return SK_OK;
+}
+
+int sk_ipc_free(void* d_ptr) {
+  if (!d_ptr) return SK_OK;
+  SK_CUDA(cudaFree(d_ptr));
   return SK_OK;
 }
 

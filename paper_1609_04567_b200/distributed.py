@@ -111,19 +111,94 @@ class BlockResult:
     out: object  # this rank's owned rows (device tensor view)
 
 
+class PeerRegion:
+    """This rank's share of the peer transport, and every rank's as mapped here.
+
+    One device allocation per rank (cudaMalloc, exported by CUDA IPC):
+    [buf0 | buf1 | mailbox double[2][world] | flag words uint32[world]],
+    the same layout on every rank (buffers sized for the largest block).
+    Other ranks' regions are mapped with cudaIpcOpenMemHandle -- over
+    NVLink on a multi-GPU node, or the same device when ranks share a GPU.
+    """
+
+    def __init__(self, buf_bytes: int, rank: int, world: int, group=None):
+        lib = N.require_cuda()
+        self.lib, self.rank, self.world, self.group = lib, rank, world, group
+        al = lambda x: -(-x // 256) * 256
+        self.off_buf = (0, al(buf_bytes))
+        self.off_mail = 2 * al(buf_bytes)
+        self.off_flag = self.off_mail + al(16 * world)
+        total = self.off_flag + al(4 * world)
+        ptr = C.c_void_p()
+        N.check(lib.sk_ipc_alloc(total, C.byref(ptr)))
+        self.own = ptr.value
+        h = C.create_string_buffer(64)
+        N.check(lib.sk_ipc_handle(C.c_void_p(self.own), h))
+        handles = _all_objects(bytes(h.raw), group)
+        self.base = []
+        for p, hb in enumerate(handles):
+            if p == rank:
+                self.base.append(self.own)
+                continue
+            q = C.c_void_p()
+            N.check(lib.sk_ipc_open(C.create_string_buffer(hb, 64), C.byref(q)))
+            self.base.append(q.value)
+
+    def buf(self, p: int, j: int) -> int:
+        return self.base[p] + self.off_buf[j]
+
+    def mail(self, p: int) -> int:
+        return self.base[p] + self.off_mail
+
+    def flags(self, p: int) -> int:
+        return self.base[p] + self.off_flag
+
+    def close(self) -> None:
+        """Collective: no rank may still write into a region being freed."""
+        if self.own is None:
+            return
+        _dist().barrier(group=self.group)
+        for p, b in enumerate(self.base):
+            if p != self.rank:
+                N.check(self.lib.sk_ipc_close(C.c_void_p(b)))
+        N.check(self.lib.sk_ipc_free(C.c_void_p(self.own)))
+        self.own = None
+
+
+def _all_objects(obj, group=None):
+    dist = _dist()
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, obj, group=group)
+    return out
+
+
 class DeviceBlock:
     """One rank's Helmholtz row block on its GPU, driven through the C-ABI.
 
     u0 / f: [rows, cols] device tensors of this rank's owned rows (fp32 or
     fp64).  The initial halo rows are exchanged at construction.
+
+    transport: "collective" -- halo rows by send/recv and the partials by an
+    all-gather over the process group (NCCL, or gloo staged through the
+    host); "peer" -- the sweep kernel itself stores its boundary rows into
+    the neighbours' halo rows and publishes its partial and a flag into
+    every rank's mailbox (PeerRegion), the stream waits on the flags with
+    no SM involvement, then the rank-ordered combine runs (no collective
+    library on the iteration path; ranks on one node).
     """
 
     def __init__(self, u0, f, consts, *, rank: int, world: int, reduce: str = "max",
-                 delta: str = "abs", identity: float = 0.0, timing: bool = False, group=None):
+                 delta: str = "abs", identity: float = 0.0, timing: bool = False, group=None,
+                 transport: str = "collective"):
         import torch
 
+        if transport not in ("collective", "peer"):
+            raise ValueError(f"unknown transport {transport!r}")
+        if transport == "peer" and not 2 <= world <= N.SK_MAX_PEERS:
+            transport = "collective"  # one rank: nothing to exchange
         lib = N.require_cuda()
         self.lib, self.rank, self.world, self.group = lib, rank, world, group
+        self.transport = transport
         rows, cols = u0.shape
         self.rows, self.cols = rows, cols
         self.ht = 1 if rank > 0 else 0
@@ -138,7 +213,29 @@ class DeviceBlock:
         self.src[self.ht:self.ht + rows, :cols] = u0
         self.env = torch.zeros((R, pitch), dtype=dt, device=dev)
         self.env[self.ht:self.ht + rows, :cols] = f
-        self.bufs = [torch.zeros((R, pitch), dtype=dt, device=dev) for _ in range(2)]
+        self.region = None
+        if transport == "peer":
+            es = u0.element_size()
+            shapes = [v[0] for v in _all_ints([rows], group)]  # every rank's owned rows
+            Rmax = max(shapes) + 2
+            self.region = PeerRegion(Rmax * pitch * es, rank, world, group)
+            typestr = "<f4" if dt == torch.float32 else "<f8"
+            self.bufs = [torch.as_tensor(_DevPtr(self.region.buf(rank, j), R * pitch, typestr),
+                                         device=dev).view(R, pitch) for j in range(2)]
+            pe = N.sk_peers()
+            pe.rank, pe.world = rank, world
+            for j in range(2):
+                if rank > 0:  # rank-1's bottom halo row: after its ht + rows rows
+                    ht_up = 1 if rank - 1 > 0 else 0
+                    pe.up_rows[j] = self.region.buf(rank - 1, j) + (ht_up + shapes[rank - 1]) * pitch * es
+                if rank < world - 1:  # rank+1's top halo row is its row 0
+                    pe.down_rows[j] = self.region.buf(rank + 1, j)
+            for p in range(world):
+                pe.mail[p] = self.region.mail(p)
+                pe.flags[p] = self.region.flags(p)
+            self._peers = pe
+        else:
+            self.bufs = [torch.zeros((R, pitch), dtype=dt, device=dev) for _ in range(2)]
         exchange_halos(self.src, rank, world, self.ht, rows, group)
         p = N.sk_plan()
         p.kernel = N.SK_KERNEL_HELMHOLTZ
@@ -167,14 +264,28 @@ class DeviceBlock:
         self.partial = torch.as_tensor(self._vptr, device=dev)
         self.gathered = torch.zeros(world, dtype=torch.float64, device=dev)
         self.launched = 0
+        if transport == "peer":
+            N.check(lib.sk_run_set_peers(h, C.byref(self._peers)))
+            # every rank's buffers exist and are zeroed before anyone's first
+            # sweep stores into them
+            torch.cuda.synchronize()
+            _dist().barrier(group=group)
 
     def buffer_of(self, t: int):
         return self.bufs[t & 1]
 
     def step(self, cond: "N.sk_cond") -> None:
-        """Enqueue one iteration: sweep -> halo exchange -> gather -> combine."""
+        """Enqueue one iteration: sweep -> halo exchange -> gather -> combine
+        (peer transport: sweep with fused halo/partial stores -> stream wait
+        on the peers' flags -> combine)."""
         N.check(self.lib.sk_run_launch(self.h, 1))
         self.launched += 1
+        if self.transport == "peer":
+            q = self.launched
+            N.check(self.lib.sk_run_peer_wait(self.h, q))
+            row = self.region.mail(self.rank) + (q & 1) * self.world * 8
+            N.check(self.lib.sk_run_combine(self.h, C.c_void_p(row), self.world, C.byref(cond)))
+            return
         exchange_halos(self.buffer_of(self.launched), self.rank, self.world, self.ht, self.rows,
                        self.group)
         gather_partials(self.partial, self.gathered, self.group)
@@ -198,9 +309,15 @@ class DeviceBlock:
         return n.value
 
     def close(self):
+        """Collective when the peer transport is on (the region is freed
+        only after every rank's last sweep)."""
         if self.h is not None:
             N.check(self.lib.sk_run_destroy(self.h))
             self.h = None
+        if self.region is not None:
+            self.bufs = None
+            self.region.close()
+            self.region = None
 
 
 def make_cond(kind: str, a: float = 0.0, n: float = 0.0, max_iterations: int = 10_000):
@@ -236,13 +353,15 @@ def bench_weak_scaling(args, world: int, rank: int, local: int, ClockSampler, me
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     n = args.n
+    transport = getattr(args, "transport", "peer")
     consts = (1.0, 1.0, 5.0, 0.0, 1.0)
     cond = make_cond("lt", 1e-4, 0.0, 10_000)
     u0 = torch.zeros((n, n), dtype=torch.float32, device="cuda")
     f = torch.ones((n, n), dtype=torch.float32, device="cuda")
 
     def solve(timing=False):
-        blk = DeviceBlock(u0, f, consts, rank=rank, world=world, timing=timing)
+        blk = DeviceBlock(u0, f, consts, rank=rank, world=world, timing=timing,
+                          transport=transport)
         res = run_block_loop(blk, cond)
         kt = blk.kernel_time() if timing else (0.0, 0)
         nl = blk.launches()
@@ -285,7 +404,7 @@ def bench_weak_scaling(args, world: int, rank: int, local: int, ClockSampler, me
     e0.record()
     du0 = h_u0.to("cuda", non_blocking=True)
     df = h_f.to("cuda", non_blocking=True)
-    blk = DeviceBlock(du0, df, consts, rank=rank, world=world)
+    blk = DeviceBlock(du0, df, consts, rank=rank, world=world, transport=transport)
     r2 = run_block_loop(blk, cond)
     h_out.copy_(r2.out, non_blocking=True)
     e1.record()
@@ -307,8 +426,12 @@ def bench_weak_scaling(args, world: int, rank: int, local: int, ClockSampler, me
         "dtype": "f32", "data": "synthetic (rhs=1, u0=0)",
         "config": {"workload": f"C4 Helmholtz/Jacobi ({n}*{world})x{n} fp32, MAX|delta|<1e-4",
                    "rows_per_gpu": n, "cols": n, "iterations_per_step": iters,
-                   "final_reduce": res.final_reduce, "parallelism": f"row blocks x{world}, "
-                   "NCCL halo rows + device-side rank-ordered combine",
+                   "final_reduce": res.final_reduce, "parallelism": f"row blocks x{world}, " + (
+                       "halo rows + partials stored by the sweep kernel into peer memory, "
+                       "stream waits on peer flags, device-side rank-ordered combine"
+                       if transport == "peer" else
+                       "NCCL halo rows + all-gather, device-side rank-ordered combine"),
+                   "transport": transport,
                    "l2": "inputs 4.3 GB/array > 126 MB L2 (no flush needed)"},
         "gpu_launches": launches,
         "e2e": {"value": cells / (e2e_ms / 1e3), "unit": "cell-updates/s",

@@ -17,7 +17,7 @@ import torch.multiprocessing as mp
 pytestmark = pytest.mark.gpu
 
 
-def _worker(rank, world, port, n, m, q):
+def _worker(rank, world, port, n, m, q, transport="collective"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -30,7 +30,7 @@ def _worker(rank, world, port, n, m, q):
         u0 = torch.zeros((hi - lo, m), dtype=torch.float32, device="cuda")
         f = torch.from_numpy(rhs[lo:hi]).cuda()
         consts = (4.0, 16.0, 40.5, 1.0 - 0.8, 0.8)  # alpha .5, dx .5, dy .25, relax .8
-        blk = DeviceBlock(u0, f, consts, rank=rank, world=world)
+        blk = DeviceBlock(u0, f, consts, rank=rank, world=world, transport=transport)
         res = run_block_loop(blk, make_cond("lt", 1e-4), batch=3)
         out = res.out.contiguous().cpu()
         blk.close()
@@ -50,8 +50,14 @@ def _port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("world,n", [(2, 200), (3, 131)])
-def test_two_ranks_one_gpu_equal_single_gpu(world, n):
+@pytest.mark.parametrize("world,n,transport", [(2, 200, "collective"), (3, 131, "collective"),
+                                               (2, 200, "peer"), (3, 131, "peer"),
+                                               (4, 97, "peer")])
+def test_two_ranks_one_gpu_equal_single_gpu(world, n, transport):
+    """transport="peer": the sweep kernel stores boundary rows into the
+    neighbours' halo rows and publishes its partial + flag into every rank's
+    mailbox (CUDA IPC mappings of the other processes' memory on the same
+    device); the stream waits on the flags; no collective on the path."""
     import paper_1609_04567_b200 as sk
     from paper_1609_04567_b200.apps import HelmholtzConfig, helmholtz_kernel
 
@@ -59,13 +65,19 @@ def test_two_ranks_one_gpu_equal_single_gpu(world, n):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    ps = [ctx.Process(target=_worker, args=(r, world, port, n, m, q)) for r in range(world)]
+    ps = [ctx.Process(target=_worker, args=(r, world, port, n, m, q, transport))
+          for r in range(world)]
     for p in ps:
         p.start()
-    it, val, grid = q.get(timeout=300)
-    for p in ps:
-        p.join(timeout=120)
-        assert p.exitcode == 0
+    try:
+        it, val, grid = q.get(timeout=300)
+        for p in ps:
+            p.join(timeout=120)
+            assert p.exitcode == 0
+    finally:
+        for p in ps:  # a rank stuck on a stream wait must not outlive the test
+            if p.is_alive():
+                p.kill()
     rhs = np.random.default_rng(5).random((n, m)).astype(np.float32)
     cfg = HelmholtzConfig(n, m, alpha=0.5, dx=0.5, dy=0.25, relax=0.8)
     out, rep = sk.parallel_loop("1:1", 1, 1, helmholtz_kernel(cfg), sk.max_combinator(0.0),
