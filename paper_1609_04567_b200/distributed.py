@@ -111,6 +111,10 @@ class BlockResult:
     out: object  # this rank's owned rows (device tensor view)
 
 
+class PeerUnavailable(RuntimeError):
+    """The peer transport cannot be set up on these ranks (raised on all)."""
+
+
 class PeerRegion:
     """This rank's share of the peer transport, and every rank's as mapped here.
 
@@ -129,20 +133,47 @@ class PeerRegion:
         self.off_mail = 2 * al(buf_bytes)
         self.off_flag = self.off_mail + al(16 * world)
         total = self.off_flag + al(4 * world)
-        ptr = C.c_void_p()
-        N.check(lib.sk_ipc_alloc(total, C.byref(ptr)))
-        self.own = ptr.value
-        h = C.create_string_buffer(64)
-        N.check(lib.sk_ipc_handle(C.c_void_p(self.own), h))
-        handles = _all_objects(bytes(h.raw), group)
-        self.base = []
+        # every step is agreed across ranks, so a failure anywhere (no IPC in
+        # the container, no peer access) makes every rank raise PeerUnavailable
+        # together instead of leaving the others in a collective
+        self.own, mine = None, None
+        try:
+            ptr = C.c_void_p()
+            N.check(lib.sk_ipc_alloc(total, C.byref(ptr)))
+            self.own = ptr.value
+            h = C.create_string_buffer(64)
+            N.check(lib.sk_ipc_handle(C.c_void_p(self.own), h))
+            mine = bytes(h.raw)
+        except N.NativeError as e:
+            mine = f"error: {e}"
+        handles = _all_objects(mine, group)
+        bad = [x for x in handles if not isinstance(x, bytes)]
+        if bad:
+            self._free_own()
+            raise PeerUnavailable(bad[0])
+        self.base, err = [], None
         for p, hb in enumerate(handles):
             if p == rank:
                 self.base.append(self.own)
                 continue
             q = C.c_void_p()
-            N.check(lib.sk_ipc_open(C.create_string_buffer(hb, 64), C.byref(q)))
-            self.base.append(q.value)
+            try:
+                N.check(lib.sk_ipc_open(C.create_string_buffer(hb, 64), C.byref(q)))
+                self.base.append(q.value)
+            except N.NativeError as e:
+                err = err or f"rank {rank} cannot map rank {p}: {e}"
+        errs = [x for x in _all_objects(err, group) if x]
+        if errs:
+            for p, b in enumerate(self.base):
+                if p != rank:
+                    self.lib.sk_ipc_close(C.c_void_p(b))
+            self._free_own()
+            raise PeerUnavailable(errs[0])
+
+    def _free_own(self):
+        if self.own is not None:
+            self.lib.sk_ipc_free(C.c_void_p(self.own))
+            self.own = None
 
     def buf(self, p: int, j: int) -> int:
         return self.base[p] + self.off_buf[j]
@@ -218,7 +249,11 @@ class DeviceBlock:
             es = u0.element_size()
             shapes = [v[0] for v in _all_ints([rows], group)]  # every rank's owned rows
             Rmax = max(shapes) + 2
-            self.region = PeerRegion(Rmax * pitch * es, rank, world, group)
+            try:
+                self.region = PeerRegion(Rmax * pitch * es, rank, world, group)
+            except PeerUnavailable:
+                transport = self.transport = "collective"  # every rank falls back together
+        if transport == "peer":
             typestr = "<f4" if dt == torch.float32 else "<f8"
             self.bufs = [torch.as_tensor(_DevPtr(self.region.buf(rank, j), R * pitch, typestr),
                                          device=dev).view(R, pitch) for j in range(2)]
