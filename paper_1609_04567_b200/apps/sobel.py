@@ -59,8 +59,10 @@ def sobel_frames(frames, out=None, stream=None):
     if frames.dtype != torch.uint8 or frames.dim() != 3 or not frames.is_cuda:
         raise GridError("sobel_frames expects a [F, H, W] uint8 CUDA tensor")
     F, H, W = frames.shape
-    if out is None:
-        out = torch.empty_like(frames)
+    if out is None:  # rows padded to 16 bytes (the kernels' pitch rule)
+        Wp = -(-frames.shape[2] // 16) * 16
+        out = torch.empty((frames.shape[0], frames.shape[1], Wp), dtype=torch.uint8,
+                          device=frames.device)[:, :, :frames.shape[2]]
     sums = torch.empty(F, dtype=torch.int64, device=frames.device)
     st = stream if stream is not None else torch.cuda.current_stream()
     N.check(lib.sk_sobel_frames(C.c_void_p(frames.data_ptr()), frames.stride(1),

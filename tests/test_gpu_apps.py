@@ -226,16 +226,20 @@ def test_batched_launches_reuse_stream_counters():
     fr16 = torch.zeros((6, 257, 304), dtype=torch.uint8, device="cuda")
     fr16[:, :, :300] = frames
     view = fr16[:, :, :300]  # 16-byte pitch: the ring kernel
-    ref_e, ref_s = sobel_frames(view)
-    ref_m, ref_c = amf_frames(view)
+
+    def o16():  # output with the same 304-byte pitch
+        return torch.empty_like(fr16)[:, :, :300]
+
+    ref_e, ref_s = sobel_frames(view, out=o16())
+    ref_m, ref_c = amf_frames(view, out=o16())
     torch.cuda.synchronize()
     streams = [torch.cuda.Stream() for _ in range(3)]
     outs = []
     for rep in range(4):
         for i, st in enumerate(streams):
             with torch.cuda.stream(st):
-                outs.append(sobel_frames(view, stream=st))
-                outs.append(amf_frames(view))
+                outs.append(sobel_frames(view, out=o16(), stream=st))
+                outs.append(amf_frames(view, out=o16()))
     torch.cuda.synchronize()
     for k, o in enumerate(outs):
         if k % 2 == 0:
