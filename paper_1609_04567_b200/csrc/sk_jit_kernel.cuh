@@ -132,6 +132,63 @@ __device__ __forceinline__ void stage_wait_upto(int pending) {
   }
 }
 
+// a thread's running reduce state across tiles
+template <bool FIRST>
+struct JitAcc {
+  double acc;
+#ifdef SK_LOCAL_MAX
+  sk_delta_t lmax;
+  bool lany;
+#endif
+};
+
+// One tile's rows for this thread: elemental + delta + reduce per element.
+// Per-element pointers advance by a fixed stride (no index arithmetic).
+template <bool FIRST, class NB, class V>
+__device__ __forceinline__ void jit_rows(const JitArgs& a, const V* tile, sk_val_t* back, int t0,
+                                         int nr, int gj, const SkComb& comb, JitAcc<FIRST>& st) {
+  constexpr int RS = SK_BLOCK / SK_TW;  // rows between a thread's elements
+  const int tx = threadIdx.x % SK_TW, ty = threadIdx.x / SK_TW;
+  const Sweep2D& g = a.g;
+  const int cols = g.cols;
+  NB nb;
+  nb.c = tile + (ty + SK_K) * kJitTWP + tx + kJitKA;
+  nb.stride = kJitTWP;
+  nb.i = t0 + ty + a.env.row0;  // global row
+  nb.j = gj;
+  nb.rows = a.env.rows;
+  nb.cols = cols;
+  nb.k = SK_K;
+  nb.eidx = (long long)(t0 + ty) * a.env.pitch[0] + gj;  // env element of the centre
+  const long long estep = (long long)RS * a.env.pitch[0];
+  sk_val_t* bp = back + (long long)(t0 + ty) * g.pitch + gj;
+  const long long bstep = (long long)RS * g.pitch;
+  for (int lr = ty; lr < nr; lr += RS) {
+    SkErr err;
+    sk_val_t nw;
+    sk_delta_t d;
+    if constexpr (FIRST) {
+      nw = sk_elemental_1(nb, a.env, err);
+      d = sk_delta_1(nw, nb.center(), err);
+    } else {
+      nw = sk_elemental_n(nb, a.env, err);
+      d = sk_delta_n(nw, nb.center(), err);
+    }
+    *bp = nw;
+    if (err.code) jit_fail(a.L.st, (long long)nb.i * cols + gj, err.code);
+#ifdef SK_LOCAL_MAX
+    st.lmax = st.lany ? jit_lmax(st.lmax, d) : d;
+    st.lany = true;
+#else
+    st.acc = comb(st.acc, (double)d);
+#endif
+    nb.c += RS * kJitTWP;
+    nb.i += RS;
+    nb.eidx += estep;
+    bp += bstep;
+  }
+}
+
 // A work chunk = one column block x chunk_rows rows = a run of SK_TH-row
 // tiles.  Tiles are double-buffered: while tile t is computed, tile t+1 is
 // already on its way into the other buffer (cp.async), so each CTA keeps
@@ -173,45 +230,23 @@ __device__ __forceinline__ void jit_sweep(const JitArgs& a, long long it, V* til
       __syncthreads();
       const V* tile = tiles + buf * kJitTileElems;
       if (gj < cols) {
-        // per-element pointers advance by a fixed stride (no index
-        // arithmetic in the loop)
-        constexpr int RS = SK_BLOCK / SK_TW;  // rows between a thread's elements
-        SkNb<V> nb;
-        nb.c = tile + (ty + SK_K) * kJitTWP + tx + kJitKA;
-        nb.stride = kJitTWP;
-        nb.i = t0 + ty + row0;  // global row
-        nb.j = gj;
-        nb.rows = grows;
-        nb.cols = cols;
-        nb.k = SK_K;
-        nb.eidx = (long long)(t0 + ty) * a.env.pitch[0] + gj;  // env element of the centre
-        const long long estep = (long long)RS * a.env.pitch[0];
-        sk_val_t* bp = back + (long long)(t0 + ty) * g.pitch + gj;
-        const long long bstep = (long long)RS * g.pitch;
-        for (int lr = ty; lr < nr; lr += RS) {
-          SkErr err;
-          sk_val_t nw;
-          sk_delta_t d;
-          if constexpr (FIRST) {
-            nw = sk_elemental_1(nb, a.env, err);
-            d = sk_delta_1(nw, nb.center(), err);
-          } else {
-            nw = sk_elemental_n(nb, a.env, err);
-            d = sk_delta_n(nw, nb.center(), err);
-          }
-          *bp = nw;
-          if (err.code) jit_fail(a.L.st, (long long)nb.i * cols + gj, err.code);
+        // NB = SkNb<V, true> when all of this thread's windows in the tile
+        // are on the grid: every ABSENT test compiles away
+        const int gi0 = t0 + row0;  // global rows of the tile: [gi0, gi0 + nr)
+        const bool inner = gi0 >= SK_K && gi0 + nr - 1 + SK_K < grows && gj >= SK_K &&
+                           gj + SK_K < cols;
+        JitAcc<FIRST> st{acc};
 #ifdef SK_LOCAL_MAX
-          lmax = lany ? jit_lmax(lmax, d) : d;
-          lany = true;
-#else
-          acc = comb(acc, (double)d);
+        st.lmax = lmax;
+        st.lany = lany;
 #endif
-          nb.c += RS * kJitTWP;
-          nb.i += RS;
-          nb.eidx += estep;
-          bp += bstep;
-        }
+        if (inner) jit_rows<FIRST, SkNb<V, true, kJitTWP>>(a, tile, back, t0, nr, gj, comb, st);
+        else jit_rows<FIRST, SkNb<V, false, kJitTWP>>(a, tile, back, t0, nr, gj, comb, st);
+        acc = st.acc;
+#ifdef SK_LOCAL_MAX
+        lmax = st.lmax;
+        lany = st.lany;
+#endif
       }
       __syncthreads();  // tile `buf` is free for the tile after next
       buf ^= 1;

@@ -45,8 +45,10 @@ struct SkErr {
 // The window around one grid element, staged in shared memory.  `at` reads
 // the staged value (the pad value where the slot is off-grid, replicated
 // border in "edge" pad mode); `ok` says whether the slot is on the grid (the
-// reference's `is not ABSENT`).
-template <class V>
+// reference's `is not ABSENT`).  IN: the whole window is known to be on the
+// grid (interior tiles), so `ok` is the constant true and every ABSENT test
+// in the generated elemental folds away at compile time.
+template <class V, bool IN = false, int STRIDE = 0>
 struct SkNb {
   const V* c;       // centre slot in the staged tile
   int stride;       // tile row stride (elements)
@@ -54,8 +56,15 @@ struct SkNb {
   int rows, cols;   // grid dims
   int k;            // radius
   long long eidx;   // element index of the centre in the env grids (all pitch == env.pitch[0])
-  __device__ __forceinline__ V at(int di, int dj) const { return c[di * stride + dj]; }
+  // STRIDE: the tile row stride as a compile-time constant (0: use `stride`)
+  __device__ __forceinline__ V at(int di, int dj) const {
+    return c[di * (STRIDE ? STRIDE : stride) + dj];
+  }
+  // true when the whole window is on the grid (and, for row blocks, every
+  // env row within the radius is resident): ABSENT / bounds tests fold away
+  __device__ static constexpr bool inner() { return IN; }
   __device__ __forceinline__ bool ok(int di, int dj) const {
+    if constexpr (IN) return true;
     return (unsigned)(i + di) < (unsigned)rows && (unsigned)(j + dj) < (unsigned)cols;
   }
   __device__ __forceinline__ V center() const { return c[0]; }

@@ -38,6 +38,7 @@ import ast
 import builtins
 import ctypes as C
 import inspect
+import re
 import linecache
 import math
 import os
@@ -897,14 +898,21 @@ class Translator:
             self.fail(node, "env indices must be integers")
         slot = g.slot
         cst, sem = self.win.env[slot]
-        if i.c == "((long long)nb.i)" and j.c == "((long long)nb.j)":
+        di, dj = _centre_offset(i.c, "i"), _centre_offset(j.c, "j")
+        if di == 0 and dj == 0:
             # the centre's own env element: on the grid and resident
             return num(f"(({CTYPE[sem]})env.at_centre<{cst}>({slot}, nb.eidx))", sem)
         ii = self.fresh(INT, i.c)
         jj = self.fresh(INT, j.c)
-        self.emit(f"if (!env.ok({ii}, {jj})) err.set(6); else if (!env.resident({ii})) err.set(9);")
-        c = (f"((env.ok({ii}, {jj}) && env.resident({ii})) ? "
-             f"({CTYPE[sem]})env.get<{cst}>({slot}, {ii}, {jj}) : ({CTYPE[sem]})0)")
+        # within the radius of the centre: on the grid and resident whenever
+        # the window is (interior tiles), so the checks compile away there
+        near = di is not None and dj is not None and abs(di) <= self.win.k and abs(dj) <= self.win.k
+        guard = "!nb.inner() && " if near else ""
+        self.emit(f"if ({guard}!env.ok({ii}, {jj})) err.set(6); "
+                  f"else if ({guard}!env.resident({ii})) err.set(9);")
+        okc = f"(nb.inner() || (env.ok({ii}, {jj}) && env.resident({ii})))" if near else \
+            f"(env.ok({ii}, {jj}) && env.resident({ii}))"
+        c = (f"({okc} ? ({CTYPE[sem]})env.get<{cst}>({slot}, {ii}, {jj}) : ({CTYPE[sem]})0)")
         return num(c, sem)
 
     def _args(self, e):
@@ -1621,6 +1629,17 @@ def grid_dtype(g) -> np.dtype:
     return np.dtype(sd)
 
 
+_CENTRE_RE = {ax: re.compile(r"^\(\(long long\)nb\.%s(?: ([+-]) (\d+))?\)$" % ax) for ax in "ij"}
+
+
+def _centre_offset(c: str, ax: str):
+    """d when the C expression `c` is nb.<ax> + d (d a literal), else None."""
+    m = _CENTRE_RE[ax].match(c)
+    if not m:
+        return None
+    return 0 if m.group(1) is None else (int(m.group(2)) if m.group(1) == "+" else -int(m.group(2)))
+
+
 def build_program(plan, grid, dims=None) -> Program:
     """The CUDA program of a plan whose elemental has no built-in kernel.
     `dims`: the global grid dims when `grid` is one rank's row block."""
@@ -1648,8 +1667,8 @@ def build_program(plan, grid, dims=None) -> Program:
         parts.append("__device__ __forceinline__ sk_val_t sk_user(const NB& nb, const SkEnv& env, SkErr& err) {")
         parts.append(body)
         parts.append("}")
-        parts.append("__device__ __forceinline__ sk_val_t sk_elemental_1(const SkNb<sk_in_t>& nb, const SkEnv& env, SkErr& err) { return sk_user(nb, env, err); }")
-        parts.append("__device__ __forceinline__ sk_val_t sk_elemental_n(const SkNb<sk_val_t>& nb, const SkEnv& env, SkErr& err) { return sk_user(nb, env, err); }")
+        parts.append("template <class NB> __device__ __forceinline__ sk_val_t sk_elemental_1(const NB& nb, const SkEnv& env, SkErr& err) { return sk_user(nb, env, err); }")
+        parts.append("template <class NB> __device__ __forceinline__ sk_val_t sk_elemental_n(const NB& nb, const SkEnv& env, SkErr& err) { return sk_user(nb, env, err); }")
     else:
         point = fn.point
         tr1 = Translator(point, [], "elemental", win, ctx=ctx)
@@ -1665,7 +1684,9 @@ def build_program(plan, grid, dims=None) -> Program:
                 f"the elemental's result type changes across iterations ({t1} then {tn})")
         out_dtype = NP_OF[t1]
         for suffix, vt, body in (("1", "sk_in_t", body1), ("n", "sk_val_t", bodyn)):
-            parts.append(f"__device__ sk_val_t sk_elemental_{suffix}(const SkNb<{vt}>& nb, const SkEnv& env, SkErr& err) {{")
+            # templated on the window type: SkNb<V, true> (interior tiles)
+            # folds every ABSENT test away
+            parts.append(f"template <class NB> __device__ sk_val_t sk_elemental_{suffix}(const NB& nb, const SkEnv& env, SkErr& err) {{")
             parts += [ln.replace("RET_T", "sk_val_t") for ln in body]
             parts.append("}")
     red, reduce, int_value = _reduce_parts(plan.op, plan.delta, val_t, in_t, val_c, in_c)
