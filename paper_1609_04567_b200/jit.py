@@ -1706,6 +1706,16 @@ def build_program(plan, grid, dims=None) -> Program:
         f"#define SK_MINB {int(os.environ.get('SK_JIT_MINB', '0')) or 6}",
         f"#define SK_PAD_EDGE {pad_edge}",
         f"#define SK_PAD_VALUE {pad_lit}",
+        f"#define SK_NENV {len(env_types)}",
+        # byte address of env element `eidx` of slot s (the sweep prefetches
+        # a tile's env rows into L1 before computing it)
+        "__device__ __forceinline__ const void* sk_env_elem(const SkEnv& e, int s, long long eidx) {",
+        "  switch (s) {",
+    ] + [f"    case {i}: return static_cast<const {cst}*>(e.p[{i}]) + eidx;"
+         for i, (cst, _sem) in enumerate(env_types)] + [
+        "    default: return nullptr;",
+        "  }",
+        "}",
     ]
     src = "\n".join(head + ctx.sources + parts + red +
                     ["}  // namespace sk", '#include "sk_jit_kernel.cuh"', ""])
