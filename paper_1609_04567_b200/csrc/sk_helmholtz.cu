@@ -55,7 +55,7 @@ struct HelmArgs {
 __device__ __forceinline__ float rcp_rn(float b) { return __frcp_rn(b); }
 __device__ __forceinline__ double rcp_rn(double b) { return __drcp_rn(b); }
 
-template <typename T, int BLOCK, int U, int DELTA, int REDUCE, bool PERSIST>
+template <typename T, int BLOCK, int U, int DELTA, int REDUCE, bool PERSIST, bool PEER = false>
 __global__ void __launch_bounds__(BLOCK, (sizeof(T) == 8 ? (PERSIST ? 4 : SK_F64_MINB) : SK_F32_MINB))
     helmholtz_sweep(const __grid_constant__ HelmArgs<T> a) {
   constexpr int VEC = 4;
@@ -81,8 +81,9 @@ __global__ void __launch_bounds__(BLOCK, (sizeof(T) == 8 ? (PERSIST ? 4 : SK_F64
   const T* env = static_cast<const T*>(g.env) + (long long)g.halo_top * g.env_pitch;
   const int lane = threadIdx.x & 31;
   const int cols = g.cols, rows = g.rows;
-  T* const peer_up = a.peer_up[it & 1];  // null unless the peer transport is on
-  T* const peer_dn = a.peer_dn[it & 1];
+  // PEER (peer transport on): the neighbours' halo rows for this iteration
+  T* const peer_up = PEER ? a.peer_up[it & 1] : nullptr;
+  T* const peer_dn = PEER ? a.peer_dn[it & 1] : nullptr;
   const T ax = a.ax, ay = a.ay, b = a.b, keep = a.keep, relax = a.relax;
   const T rb = rcp_rn(b);
   const bool fast = a.fast_div != 0;
@@ -183,8 +184,10 @@ __global__ void __launch_bounds__(BLOCK, (sizeof(T) == 8 ? (PERSIST ? 4 : SK_F64
             st4(po, o);
             // boundary rows also land in the neighbours' halo rows (peer
             // stores, overlapped with the rest of the sweep)
-            if (rr == 0 && peer_up) st4(peer_up + col, o);
-            if (rr == rows - 1 && peer_dn) st4(peer_dn + col, o);
+            if constexpr (PEER) {
+              if (rr == 0 && peer_up) st4(peer_up + col, o);
+              if (rr == rows - 1 && peer_dn) st4(peer_dn + col, o);
+            }
           }
           up = cen;
           cen = dn[u];
@@ -728,11 +731,12 @@ template <typename T>
 using KernelFn = void (*)(const HelmArgs<T>);
 
 template <typename T>
-KernelFn<T> pick(int delta, int reduce, bool persist = false) {
+KernelFn<T> pick(int delta, int reduce, bool persist = false, bool peer = false) {
 #define SK_H(D, R)                                                                            \
   if (delta == D && reduce == R)                                                              \
     return persist ? helmholtz_sweep<T, kBlock, unroll_for<T>(), D, R, true>                  \
-                   : helmholtz_sweep<T, kBlock, unroll_for<T>(), D, R, false>;
+                   : peer ? helmholtz_sweep<T, kBlock, unroll_for<T>(), D, R, false, true>    \
+                          : helmholtz_sweep<T, kBlock, unroll_for<T>(), D, R, false>;
   SK_H(SK_DELTA_NONE, SK_REDUCE_SUM)
   SK_H(SK_DELTA_NONE, SK_REDUCE_MAX)
   SK_H(SK_DELTA_ABS, SK_REDUCE_SUM)
@@ -990,7 +994,7 @@ int launch_t(sk_run* r, const LoopCtl& L, cudaStream_t s) {
     if (rc == SK_OK) return SK_OK;
     if (rc != SK_ERR_UNSUPPORTED) return rc;
   }
-  KernelFn<T> fn = pick<T>(p.delta_op, p.reduce_op, persist);
+  KernelFn<T> fn = pick<T>(p.delta_op, p.reduce_op, persist, r->has_peers);
   if (persist) {
     // the persistent variant has its own register budget: size the grid to
     // what is co-resident
