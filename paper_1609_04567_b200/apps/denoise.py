@@ -413,13 +413,14 @@ def video_restore_pipeline(frames: Iterable, *, width: int = 1, partitions: int 
             if mask_writer is not None:
                 mask_writer(mask)
             return img, mask
+        if fused_detect:
+            # the detector runs inside the restore batches; the upload happens
+            # in the restore replicas (in parallel) rather than in this stage
+            return img, None
         st = detect_group.stream
         dev = torch.device("cuda", torch.cuda.current_device())
         with torch.cuda.stream(st):
             t = _u8_from(img, "amf", 0, 255, dev)
-            if fused_detect:
-                st.synchronize()
-                return t, None
             masks, _ = amf_frames(t.reshape(1, *img.dims), cfg.amf_wmax, stream=st)
         st.synchronize()
         if mask_writer is not None:
@@ -432,16 +433,33 @@ def video_restore_pipeline(frames: Iterable, *, width: int = 1, partitions: int 
 
     def make_restorer():
         grp = None if batched else WorkerGroup(eff)
+        streams = []
+
+        def upload_stream():  # one per replica, created on first use
+            if not streams:
+                streams.append(torch.cuda.Stream())
+            return streams[0]
 
         class _Restorer:
             def __call__(self, pair):
                 img, mask = pair
                 if batched:
+                    if isinstance(img, Grid):  # fused detect: upload here
+                        if img.ndim != 2:
+                            raise GridError("detection expects a 2D image")
+                        dev = torch.device("cuda", torch.cuda.current_device())
+                        with torch.cuda.stream(upload_stream()):
+                            img = _u8_from(img, "amf", 0, 255, dev)
+                            torch.cuda.current_stream().synchronize()
                     out, _rep = batcher.submit(img, mask)
-                    return out
-                out, _rep = restore_regularize(
-                    img, mask, cfg, partitions=eff,
-                    mode=mode if eff > 1 else DeploymentMode.ONE_TO_ONE, group=grp)
+                else:
+                    out, _rep = restore_regularize(
+                        img, mask, cfg, partitions=eff,
+                        mode=mode if eff > 1 else DeploymentMode.ONE_TO_ONE, group=grp)
+                if writer is not None:
+                    # read the frame back here, in parallel across replicas;
+                    # the ordered writer's to_array() then takes it over
+                    out.prefetch_host()
                 return out
 
             def close(self):
