@@ -468,9 +468,9 @@ __device__ __forceinline__ T helm_update(T c, T l, T rt, T up, T dn, T fv, const
 // fold_and_decide -- and evaluates the loop test on identical data, so all
 // reach the same decision without a second round trip.  CTA 0 publishes the
 // status for the host at the end.  Returns the stop decision.
-template <int BLOCK, bool AMAX>
-__device__ int res_step(const LoopCtl& L, long long it, double mine, unsigned* cnt, double* parts,
-                        int nb, double* sh) {
+template <int BLOCK, bool AMAX, class Pre>
+__device__ __forceinline__ int res_step(const LoopCtl& L, long long it, double mine, unsigned* cnt, double* parts,
+                        int nb, double* sh, const Pre& prefetch) {
   __shared__ int s_stop;
   const double v = block_reduce<BLOCK>(L.reduce, mine, sh);
   double* slot = parts + (it & 1) * nb;
@@ -494,6 +494,9 @@ __device__ int res_step(const LoopCtl& L, long long it, double mine, unsigned* c
     } while ((int)(seen - want) < 0);
   }
   __syncthreads();
+  // every band has published: start the next iteration's halo loads now, so
+  // they are in flight while the decision is read and made
+  prefetch();
   const OpCombine comb{L.reduce};
   double acc = L.identity;
   if (AMAX) {
@@ -628,45 +631,69 @@ __global__ void __launch_bounds__(BLOCK, 1) helm_resident(const __grid_constant_
     __syncthreads();
     T accm = -INFINITY;
     double accs = 0.0;
-    VecN<T, VEC> prev = up;  // old value of the row above the current one
+    // one row's update: centre row r (old values), the rows above / below
+    auto update = [&](int r, const VecN<T, VEC>& cen, const VecN<T, VEC>& above,
+                      const VecN<T, VEC>& below) {
+      T lv = __shfl_up_sync(FULL, cen.v[VEC - 1], 1);
+      T rv = __shfl_down_sync(FULL, cen.v[0], 1);
+      if (lane == 0) lv = warp > 0 ? s_edge[r][1][warp - 1] : T(0);
+      if (lane == 31) rv = warp + 1 < NW ? s_edge[r][0][warp + 1] : T(0);
+      VecN<T, VEC> o;
+      T dd[VEC];
 #pragma unroll
-    for (int r = 0; r < RMAX; ++r) {
-      if (r < R) {
-        const VecN<T, VEC> cen = u[r];
-        const VecN<T, VEC> below = (r + 1 < R) ? u[r + 1 < RMAX ? r + 1 : r] : dn;
-        T lv = __shfl_up_sync(FULL, cen.v[VEC - 1], 1);
-        T rv = __shfl_down_sync(FULL, cen.v[0], 1);
-        if (lane == 0) lv = warp > 0 ? s_edge[r][1][warp - 1] : T(0);
-        if (lane == 31) rv = warp + 1 < NW ? s_edge[r][0][warp + 1] : T(0);
-        VecN<T, VEC> o;
-        T dd[VEC];
-#pragma unroll
-        for (int e = 0; e < VEC; ++e) {
-          const T l = e == 0 ? lv : cen.v[e - 1];
-          T rt = e == VEC - 1 ? rv : cen.v[e + 1];
-          if (e + 1 >= nvalid) rt = T(0);  // Dirichlet-0 right border
-          const T fv = active && e < nvalid ? s_f[r * cols + col + e] : T(0);
-          const T out = helm_update(cen.v[e], l, rt, prev.v[e], below.v[e], fv, a, rb, fast);
-          const bool in = e < nvalid;
-          o.v[e] = in ? out : T(0);
-          T d;
-          if (DELTA == SK_DELTA_ABS) {
-            d = tabs(xsub(out, cen.v[e]));
-          } else if (DELTA == SK_DELTA_SQUARE) {
-            const T t = xsub(out, cen.v[e]);
-            d = xmul(t, t);
-          } else {
-            d = out;
-          }
-          if (REDUCE == SK_REDUCE_MAX) {
-            if (in) accm = max_nan(accm, d);
-          } else {
-            dd[e] = in ? d : T(0);
-          }
+      for (int e = 0; e < VEC; ++e) {
+        const T l = e == 0 ? lv : cen.v[e - 1];
+        T rt = e == VEC - 1 ? rv : cen.v[e + 1];
+        if (e + 1 >= nvalid) rt = T(0);  // Dirichlet-0 right border
+        const T fv = active && e < nvalid ? s_f[r * cols + col + e] : T(0);
+        const T out = helm_update(cen.v[e], l, rt, above.v[e], below.v[e], fv, a, rb, fast);
+        const bool in = e < nvalid;
+        o.v[e] = in ? out : T(0);
+        T d;
+        if (DELTA == SK_DELTA_ABS) {
+          d = tabs(xsub(out, cen.v[e]));
+        } else if (DELTA == SK_DELTA_SQUARE) {
+          const T t = xsub(out, cen.v[e]);
+          d = xmul(t, t);
+        } else {
+          d = out;
         }
-        if (REDUCE == SK_REDUCE_SUM) accs += (double)sumN<T, VEC>(dd);
-        prev = cen;
-        u[r] = o;
+        if (REDUCE == SK_REDUCE_MAX) {
+          if (in) accm = max_nan(accm, d);
+        } else {
+          dd[e] = in ? d : T(0);
+        }
+      }
+      if (REDUCE == SK_REDUCE_SUM) accs += (double)sumN<T, VEC>(dd);
+      return o;
+    };
+    if constexpr (REDUCE == SK_REDUCE_MAX) {
+      // MAX is order-free: rows 1 .. R-1 first (the last one with the halo
+      // row below), row 0 (the halo row above) last, so the halo loads
+      // issued at the previous grid step have the longest time to land
+      const VecN<T, VEC> old0 = u[0];
+      const VecN<T, VEC> old1 = R > 1 ? u[RMAX > 1 ? 1 : 0] : dn;
+      VecN<T, VEC> prev = old0;  // old value of the row above the current one
+#pragma unroll
+      for (int r = 1; r < RMAX; ++r) {
+        if (r < R) {
+          const VecN<T, VEC> cen = u[r];
+          const VecN<T, VEC> below = (r + 1 < R) ? u[r + 1 < RMAX ? r + 1 : r] : dn;
+          u[r] = update(r, cen, prev, below);
+          prev = cen;
+        }
+      }
+      u[0] = update(0, old0, up, old1);
+    } else {  // SUM: row order fixed (the partial's summation order)
+      VecN<T, VEC> prev = up;
+#pragma unroll
+      for (int r = 0; r < RMAX; ++r) {
+        if (r < R) {
+          const VecN<T, VEC> cen = u[r];
+          const VecN<T, VEC> below = (r + 1 < R) ? u[r + 1 < RMAX ? r + 1 : r] : dn;
+          u[r] = update(r, cen, prev, below);
+          prev = cen;
+        }
       }
     }
     // this band's edge rows for the neighbouring bands (iteration parity slot)
@@ -679,23 +706,12 @@ __global__ void __launch_bounds__(BLOCK, 1) helm_resident(const __grid_constant_
     }
     const double mine = REDUCE == SK_REDUCE_MAX ? (double)accm : accs;
     constexpr bool kAmaxOk = REDUCE == SK_REDUCE_MAX && DELTA != SK_DELTA_NONE;
-    const long long nxt =
-        ((kAmaxOk && a.L.nparts == 1) ? res_step<BLOCK, kAmaxOk>(a.L, it, mine, cnt, parts, nb, sh)
-                                      : res_step<BLOCK, false>(a.L, it, mine, cnt, parts, nb, sh))
-            ? 0 : it + 1;
-    if (nxt == 0) {
-      // the loop is over: iteration `it` is the result
-      if (active) {
-        T* out = static_cast<T*>(g.buf[it & 1]) + (long long)g.halo_top * g.pitch;
-#pragma unroll
-        for (int r = 0; r < RMAX; ++r)
-          if (r < R) stN<T, VEC>(out + (long long)(r0 + r) * g.pitch + col, u[r]);
-      }
-      return;
-    }
-    // halo rows of the next iteration: the neighbours' edge rows
-    if (active) {
-      const T* xb = xbuf + (long long)((it & 1) * nb) * 2 * a.xpitch;
+    // halo rows of the next iteration: the neighbours' edge rows (loaded as
+    // soon as the grid step shows every band has published them)
+    const long long cur = it;
+    auto prefetch = [&]() {
+      if (!active) return;
+      const T* xb = xbuf + (long long)((cur & 1) * nb) * 2 * a.xpitch;
       if (blockIdx.x > 0 && !(r0 == 0)) {
         const T* p = xb + ((long long)(blockIdx.x - 1) * 2 + 1) * a.xpitch + col;
 #pragma unroll
@@ -710,6 +726,21 @@ __global__ void __launch_bounds__(BLOCK, 1) helm_resident(const __grid_constant_
       } else {
         dn = zeroN<T, VEC>();
       }
+    };
+    const long long nxt =
+        ((kAmaxOk && a.L.nparts == 1)
+             ? res_step<BLOCK, kAmaxOk>(a.L, it, mine, cnt, parts, nb, sh, prefetch)
+             : res_step<BLOCK, false>(a.L, it, mine, cnt, parts, nb, sh, prefetch))
+            ? 0 : it + 1;
+    if (nxt == 0) {
+      // the loop is over: iteration `it` is the result
+      if (active) {
+        T* out = static_cast<T*>(g.buf[it & 1]) + (long long)g.halo_top * g.pitch;
+#pragma unroll
+        for (int r = 0; r < RMAX; ++r)
+          if (r < R) stN<T, VEC>(out + (long long)(r0 + r) * g.pitch + col, u[r]);
+      }
+      return;
     }
     it = nxt;
   }
@@ -819,13 +850,24 @@ int launch_resident(sk_run* r, const LoopCtl& L, cudaStream_t s, const HelmArgs<
   if (p.halo_top || p.halo_bottom) return SK_ERR_UNSUPPORTED;
   const char* off = getenv("SK_NO_RESIDENT");
   if (off && off[0] == '1') return SK_ERR_UNSUPPORTED;
-  // one column per thread up to 1024 columns (32 warps per SM hide the
-  // shuffle / shared-memory latencies), two up to 2048
-  const int block = 1024;
-  const int vec = p.cols <= 1024 ? 1 : (p.cols <= 2048 ? 2 : 0);
+  // two columns per thread: 512 threads up to 1024 columns (C1: 7% faster
+  // per iteration than 1024 x 1 -- cheaper block barriers and reduces, the
+  // loop is barrier-latency-bound), 1024 threads up to 2048
+  int block = p.cols <= 1024 ? 512 : 1024;
+  int vec = p.cols <= 2048 ? 2 : 0;
   if (!vec) return SK_ERR_UNSUPPORTED;
-  ResFn<T> fn = vec == 1 ? pick_res_b<T, 1024, 1>(p.delta_op, p.reduce_op)
-                         : pick_res_b<T, 1024, 2>(p.delta_op, p.reduce_op);
+  // SK_RES_VEC=1 / 4 for grids up to 1024 columns: 1024 x 1 or 256 x 4
+  // threads (measurement knob)
+  const char* ev = getenv("SK_RES_VEC");
+  const int want = ev ? atoi(ev) : 0;
+  if (p.cols <= 1024 && (want == 1 || want == 4)) {
+    vec = want;
+    block = 1024 / want;
+  }
+  ResFn<T> fn = block == 256   ? pick_res_b<T, 256, 4>(p.delta_op, p.reduce_op)
+                : block == 512 ? pick_res_b<T, 512, 2>(p.delta_op, p.reduce_op)
+                : vec == 1     ? pick_res_b<T, 1024, 1>(p.delta_op, p.reduce_op)
+                               : pick_res_b<T, 1024, 2>(p.delta_op, p.reduce_op);
   if (!fn) return SK_ERR_UNSUPPORTED;
   const int sms = device_sms(r->device);
   // band height: the smallest that gives at most one band per SM
