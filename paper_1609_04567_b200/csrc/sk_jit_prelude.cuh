@@ -96,6 +96,15 @@ struct SkEnv {
   __device__ __forceinline__ bool resident(long long i) const { return i >= lo && i < hi; }
 };
 
+// (i, j) within the radius of an interior window's centre: on the grid and
+// resident, no checks needed (false for border windows)
+template <class NB>
+__device__ __forceinline__ bool sk_env_near(const NB& nb, long long i, long long j) {
+  if constexpr (!NB::inner()) return false;
+  const long long di = i - nb.i, dj = j - nb.j;
+  return di >= -nb.k && di <= nb.k && dj >= -nb.k && dj <= nb.k;
+}
+
 // Kernel parameters of sk_jit_sweep (built on the host in sk_jit.cu).
 struct JitArgs {
   Sweep2D g;

@@ -898,20 +898,21 @@ class Translator:
             self.fail(node, "env indices must be integers")
         slot = g.slot
         cst, sem = self.win.env[slot]
-        di, dj = _centre_offset(i.c, "i"), _centre_offset(j.c, "j")
-        if di == 0 and dj == 0:
+        if _centre_offset(i.c, "i") == 0 and _centre_offset(j.c, "j") == 0:
             # the centre's own env element: on the grid and resident
             return num(f"(({CTYPE[sem]})env.at_centre<{cst}>({slot}, nb.eidx))", sem)
         ii = self.fresh(INT, i.c)
         jj = self.fresh(INT, j.c)
-        # within the radius of the centre: on the grid and resident whenever
-        # the window is (interior tiles), so the checks compile away there
-        near = di is not None and dj is not None and abs(di) <= self.win.k and abs(dj) <= self.win.k
-        guard = "!nb.inner() && " if near else ""
-        self.emit(f"if ({guard}!env.ok({ii}, {jj})) err.set(6); "
-                  f"else if ({guard}!env.resident({ii})) err.set(9);")
-        okc = f"(nb.inner() || (env.ok({ii}, {jj}) && env.resident({ii})))" if near else \
-            f"(env.ok({ii}, {jj}) && env.resident({ii}))"
+        # Within the radius of the centre an env element is on the grid and
+        # resident whenever the window is (interior tiles).  `near` is a
+        # run-time test that the C compiler folds to a constant when the
+        # index is the centre index plus literals (the usual case, however
+        # the Python code names it), so the checks compile away there.
+        near = f"sk_env_near(nb, {ii}, {jj})"
+        self.emit(f"const bool {ii}_near = {near};")
+        self.emit(f"if (!{ii}_near && !env.ok({ii}, {jj})) err.set(6); "
+                  f"else if (!{ii}_near && !env.resident({ii})) err.set(9);")
+        okc = f"({ii}_near || (env.ok({ii}, {jj}) && env.resident({ii})))"
         c = (f"({okc} ? ({CTYPE[sem]})env.get<{cst}>({slot}, {ii}, {jj}) : ({CTYPE[sem]})0)")
         return num(c, sem)
 

@@ -162,3 +162,38 @@ def test_pattern_wrappers_compile():
     mn = sk.Combinator(lambda p, q: p if p < q else q, 10 ** 6)
     jit.build_program(LoopPlan(fn=sk.ElementalFn(point=lambda nb, env: nb.center, k=0), k=0,
                                op=mn), g)
+
+
+def test_interior_window_specialisation():
+    """Elementals are templated on the window type (interior tiles fold the
+    ABSENT tests away); env reads at the centre use the unchecked centre
+    access, env reads within the radius are guarded by nb.inner()."""
+    assert jit._centre_offset("((long long)nb.i)", "i") == 0
+    assert jit._centre_offset("((long long)nb.i + 0)", "i") == 0
+    assert jit._centre_offset("((long long)nb.j - 2)", "j") == -2
+    assert jit._centre_offset("((long long)nb.j + v)", "j") is None
+    assert jit._centre_offset("((long long)nb.i + 1)", "j") is None
+
+    def near(nb, env):
+        i, j = nb.center_index
+        return nb.center + env.at(i, j) + env.at(i - 1, j + 1) + env.at(i + 3, j)
+
+    g = np.random.default_rng(1).random((20, 140))
+    e = np.random.default_rng(2).random((20, 140))
+    plan = LoopPlan(fn=sk.ElementalFn(point=near, k=1), k=1, op=sk.sum_combinator(0.0),
+                    env=sk.Grid(e.shape, e))
+    src = jit.build_program(plan, sk.Grid(g.shape, g)).source
+    assert "template <class NB> __device__ sk_val_t sk_elemental_1(const NB& nb" in src
+    # every env read carries the window-radius test (the C compiler folds it
+    # for centre-plus-literal indices); the bounds checks stay behind it
+    body1 = src[src.index("sk_elemental_1"):src.index("sk_elemental_n")]
+    assert body1.count("sk_env_near(nb, ") == 3
+    assert body1.count("_near && !env.ok(") == 3
+
+    def centre(nb, env):
+        return nb.center + env.at(*nb.center_index)
+
+    plan = LoopPlan(fn=sk.ElementalFn(point=centre, k=1), k=1, op=sk.sum_combinator(0.0),
+                    env=sk.Grid(e.shape, e))
+    src = jit.build_program(plan, sk.Grid(g.shape, g)).source
+    assert "env.at_centre<double>(0, nb.eidx)" in src and "env.ok(" not in src
