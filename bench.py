@@ -210,17 +210,43 @@ def run_ours(args):
     h_out = torch.empty((n, n), dtype=torch.float32).pin_memory()
     e2e_steps = max(1, min(args.steps, 3))
     ex2 = sk.DeviceExecutor(1)
+    # Pipelined like a stream of solves: step k+1's inputs go up on a copy
+    # stream while step k solves, and step k's result comes down on another
+    # (PCIe is full duplex); every step still uploads its inputs from pinned
+    # host memory and reads its result back inside the timed region.
+    cur = torch.cuda.current_stream()
+    up_s, down_s = torch.cuda.Stream(), torch.cuda.Stream()
+    h_out2 = [h_out, torch.empty((n, n), dtype=torch.float32).pin_memory()]
+
+    def upload():
+        with torch.cuda.stream(up_s):
+            du = h_u0.to("cuda", non_blocking=True)
+            df = h_f.to("cuda", non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(up_s)
+        return du, df, ev
+
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for _ in range(e2e_steps):
-        gu = sk.Grid.from_tensor(h_u0.to("cuda", non_blocking=True))
-        gf = sk.Grid.from_tensor(h_f.to("cuda", non_blocking=True))
+    nxt = upload()
+    for k in range(e2e_steps):
+        du, df, ev = nxt
+        cur.wait_event(ev)
+        du.record_stream(cur)
+        df.record_stream(cur)
+        if k + 1 < e2e_steps:
+            nxt = upload()
         o, r2 = sk.loop_stencil_reduce_d(1, kern, sk.abs_change(), sk.max_combinator(0.0), cond,
-                                         gu, env=gf, executor=ex2)
-        h_out.copy_(o.tensor(), non_blocking=True)
-        del o, gu, gf
-    e1.record()
+                                         sk.Grid.from_tensor(du), env=sk.Grid.from_tensor(df),
+                                         executor=ex2)
+        ot = o.tensor()
+        down_s.wait_stream(cur)
+        with torch.cuda.stream(down_s):
+            h_out2[k % 2].copy_(ot, non_blocking=True)
+        ot.record_stream(down_s)
+        del o, ot, du, df
+    e1.record(down_s)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / e2e_steps
     e2e_value = cells / (e2e_ms / 1e3)
@@ -255,7 +281,9 @@ def run_ours(args):
         "gpu_launches": ex.launches,
         "e2e": {"value": e2e_value, "unit": "cell-updates/s",
                 "h2d_bytes_per_step": 2 * 4 * n * n, "d2h_bytes_per_step": 4 * n * n,
-                "ms_per_step": e2e_ms},
+                "ms_per_step": e2e_ms,
+                "mode": f"{e2e_steps} solves through loop_stencil_reduce_d from pinned host "
+                        "buffers, pipelined: step k+1's H2D overlaps step k's solve and D2H"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": "helmholtz_sweep<float> (fused stencil+|delta|+max+loop test)",

@@ -522,6 +522,9 @@ class DeviceExecutor(Executor):
         owns = group is None
         stream = group.stream if group is not None else torch.cuda.current_stream()
         if group is not None:
+            # the run's stream starts after whatever the caller enqueued on
+            # its current stream (e.g. a non-blocking upload of the inputs)
+            stream.wait_stream(torch.cuda.current_stream())
             group.start_run()
         try:
             with torch.cuda.stream(stream):
