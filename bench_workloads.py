@@ -110,9 +110,10 @@ def c1(args, ClockSampler, measured_peaks, local=0):
         torch.cuda.synchronize()
     ms = s.elapsed_time(e) / args.steps
     cells = 36.0 * n * n * per_step
-    # e2e: host numpy in, host numpy out, through the public API
-    h0 = np.zeros((n, n), np.float32)
-    hf = np.ones((n, n), np.float32)
+    # e2e: host numpy in (arrays in pinned memory, as the contract's host
+    # buffers), host numpy out, through the public API
+    h0 = torch.zeros((n, n), dtype=torch.float32).pin_memory().numpy()
+    hf = torch.ones((n, n), dtype=torch.float32).pin_memory().numpy()
     sk.loop_stencil_reduce_d(1, kern, sk.abs_change(), sk.max_combinator(0.0),
                              sk.Condition.below(1e-4), sk.Grid((n, n), h0),
                              env=sk.Grid((n, n), hf))[0].to_array()
