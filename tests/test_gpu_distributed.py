@@ -85,3 +85,58 @@ def test_two_ranks_one_gpu_equal_single_gpu(world, n, transport):
                                 env=sk.Grid(rhs.shape, rhs), delta=sk.abs_change())
     assert it == rep.iterations and val == rep.final_reduce
     assert np.array_equal(grid.view(np.uint32), out.to_array().view(np.uint32))
+
+
+def _worker2(rank, world, port, n, m, q, transport):
+    """fp64, SUM of squared deltas (the RMS form of helmholtz_solve)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1609_04567_b200.distributed import DeviceBlock, make_cond, run_block_loop
+        from paper_1609_04567_b200.partition import _split_ranges
+
+        torch.cuda.set_device(0)
+        rhs = np.random.default_rng(9).random((n, m))
+        lo, hi = _split_ranges(n, world)[rank]
+        u0 = torch.zeros((hi - lo, m), dtype=torch.float64, device="cuda")
+        f = torch.from_numpy(rhs[lo:hi]).cuda()
+        consts = (1.0, 1.0, 5.0, 0.0, 1.0)
+        blk = DeviceBlock(u0, f, consts, rank=rank, world=world, reduce="sum", delta="square",
+                          transport=transport)
+        res = run_block_loop(blk, make_cond("rms_lt", 1e-6, float(n * m)), batch=4)
+        out = res.out.contiguous().cpu()
+        blk.close()
+        parts = [torch.zeros((b - a, m), dtype=torch.float64) for a, b in _split_ranges(n, world)]
+        for r in range(world):
+            dist.broadcast(out if r == rank else parts[r], src=r)
+        parts[rank] = out
+        if rank == 0:
+            q.put((res.iterations, res.final_reduce, torch.cat(parts).numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_transport_fp64_sum_matches_collective():
+    """The two transports give the same grid, iteration count and final SUM
+    (fp64, RMS condition, 3 ranks on one GPU)."""
+    outs = {}
+    for transport in ("collective", "peer"):
+        ctx = mp.get_context("spawn")
+        q = ctx.Queue()
+        port = _port()
+        ps = [ctx.Process(target=_worker2, args=(r, 3, port, 61, 70, q, transport))
+              for r in range(3)]
+        for p in ps:
+            p.start()
+        try:
+            outs[transport] = q.get(timeout=300)
+            for p in ps:
+                p.join(timeout=120)
+                assert p.exitcode == 0
+        finally:
+            for p in ps:
+                if p.is_alive():
+                    p.kill()
+    (i1, v1, g1), (i2, v2, g2) = outs["collective"], outs["peer"]
+    assert i1 == i2 and i1 > 1 and v1 == v2
+    assert np.array_equal(g1.view(np.uint64), g2.view(np.uint64))
