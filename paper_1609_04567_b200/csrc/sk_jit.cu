@@ -173,16 +173,24 @@ int jit_setup(sk_run* r) {
   int rc = jit_function(j, r->device, &f);
   if (rc) return rc;
   r->block = j->block;
-  r->colblocks = (int)((r->plan.cols + kTW - 1) / kTW);
+  // params[3] == 1: a rank-1 grid (one column, pitch 1) run with contiguous
+  // element tiles of SK_TH * SK_TW (program compiled with SK_NDIM 1)
+  const bool rank1 = r->plan.params[3] == 1.0;
+  if (rank1 && r->plan.cols != 1) {
+    set_error("sk_run_begin_jit: a rank-1 program runs on a one-column grid");
+    return SK_ERR_ARG;
+  }
+  r->colblocks = rank1 ? 1 : (int)((r->plan.cols + kTW - 1) / kTW);
   const int kTH = r->plan.params[0] >= 1 ? (int)r->plan.params[0] : 16;  // the program's SK_TH
+  const int tile_rows = rank1 ? kTH * kTW : kTH;  // rows (= elements, rank 1) per tile
   // chunk = a run of tiles: as tall as possible (<= 8 tiles) while leaving
   // ~4 chunks per resident CTA for balance
   {
     const long long slots = (long long)device_sms(r->device) * j->occ[r->device];
-    const long long tiles = ((r->plan.rows + kTH - 1) / kTH) * r->colblocks;
+    const long long tiles = ((r->plan.rows + tile_rows - 1) / tile_rows) * r->colblocks;
     long long m = tiles / (4 * slots);
     m = m < 1 ? 1 : (m > 8 ? 8 : m);
-    r->chunk_rows = (int)(kTH * m);
+    r->chunk_rows = (int)(tile_rows * m);
   }
   int n = 0;
   r->part_chunk[0] = 0;

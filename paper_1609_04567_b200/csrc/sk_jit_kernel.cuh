@@ -277,6 +277,117 @@ __device__ __forceinline__ void jit_sweep(const JitArgs& a, long long it, V* til
   }
 }
 
+#if SK_NDIM == 1
+// ---------------------------------------------------------------- rank-1 grids
+// A rank-1 grid is contiguous (pitch 1): a tile is SK_TH * SK_TW consecutive
+// elements plus the radius on both sides, staged with cp.async; thread t
+// computes elements t, t + SK_BLOCK, ... (coalesced).  Same window type,
+// interior specialisation, reduce order and error reporting as the 2D sweep.
+constexpr int kJit1Elems = SK_TH * SK_TW;
+static_assert(kJit1Elems + 2 * kJitKA <= kJitTileElems, "1D tile fits the 2D tile buffer");
+
+template <class V>
+__device__ __forceinline__ void jit_stage1(V* tile, const V* front, long long fp, int t0, int ne,
+                                           int rlo, int rhi) {
+  // tile[kJitKA + e] = element t0 + e, e in [-SK_K, ne + SK_K)
+  for (int x = threadIdx.x; x < ne + 2 * SK_K; x += SK_BLOCK) {
+    int gi = t0 - SK_K + x;
+    V* dst = tile + kJitKA - SK_K + x;
+#if SK_PAD_EDGE
+    gi = gi < rlo ? rlo : (gi >= rhi ? rhi - 1 : gi);
+    stage_one(dst, front + (long long)gi * fp);
+#else
+    if (gi >= rlo && gi < rhi) stage_one(dst, front + (long long)gi * fp);
+    else *dst = (V)(SK_PAD_VALUE);
+#endif
+  }
+  if constexpr (sizeof(V) == 4 || sizeof(V) == 8)
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+
+template <bool FIRST, class NB, class V>
+__device__ __forceinline__ void jit_elems1(const JitArgs& a, const V* tile, sk_val_t* back, int t0,
+                                           int ne, const SkComb& comb, JitAcc<FIRST>& st) {
+  const Sweep2D& g = a.g;
+  for (int e = threadIdx.x; e < ne; e += SK_BLOCK) {
+    NB nb;
+    nb.c = tile + kJitKA + e;
+    nb.stride = 1;
+    nb.i = t0 + e + a.env.row0;  // global index
+    nb.j = 0;
+    nb.rows = a.env.rows;
+    nb.cols = 1;
+    nb.k = SK_K;
+    nb.eidx = (long long)(t0 + e) * a.env.pitch[0];
+    SkErr err;
+    sk_val_t nw;
+    sk_delta_t d;
+    if constexpr (FIRST) {
+      nw = sk_elemental_1(nb, a.env, err);
+      d = sk_delta_1(nw, nb.center(), err);
+    } else {
+      nw = sk_elemental_n(nb, a.env, err);
+      d = sk_delta_n(nw, nb.center(), err);
+    }
+    back[(long long)(t0 + e) * g.pitch] = nw;
+    if (err.code) jit_fail(a.L.st, (long long)nb.i, err.code);
+#ifdef SK_LOCAL_MAX
+    st.lmax = st.lany ? jit_lmax(st.lmax, d) : d;
+    st.lany = true;
+#else
+    st.acc = comb(st.acc, (double)d);
+#endif
+  }
+}
+
+template <class V, bool FIRST>
+__device__ __forceinline__ void jit_sweep1(const JitArgs& a, long long it, V* tiles, int* s_chunk,
+                                           double* sh, const SkComb& comb) {
+  const Sweep2D& g = a.g;
+  const long long fp = FIRST ? g.src_pitch : g.pitch;
+  const V* front = static_cast<const V*>(FIRST ? g.src : g.buf[(it - 1) & 1]) +
+                   (long long)g.halo_top * fp;
+  sk_val_t* back = static_cast<sk_val_t*>(g.buf[it & 1]) + (long long)g.halo_top * g.pitch;
+  const int n = g.rows;
+  const int rlo = -g.halo_top, rhi = n + g.halo_bottom;
+  const int row0 = a.env.row0, grows = a.env.rows;
+  const double neutral = comb.neutral(a.L.identity);
+  const int total = a.L.part_chunk[a.L.nparts];
+  for (int c = next_chunk(a.L, s_chunk); c < total; c = next_chunk(a.L, s_chunk)) {
+    int cb, r0, r1;
+    chunk_geom(a.L, g, c, &cb, &r0, &r1);
+    JitAcc<FIRST> st{neutral};
+#ifdef SK_LOCAL_MAX
+    st.lmax = 0;
+    st.lany = false;
+#endif
+    int buf = 0;
+    jit_stage1<V>(tiles, front, fp, r0, min(kJit1Elems, r1 - r0), rlo, rhi);
+    for (int t0 = r0; t0 < r1; t0 += kJit1Elems) {
+      const int ne = min(kJit1Elems, r1 - t0);
+      const bool more = t0 + kJit1Elems < r1;
+      if (more)
+        jit_stage1<V>(tiles + (buf ^ 1) * kJitTileElems, front, fp, t0 + kJit1Elems,
+                      min(kJit1Elems, r1 - t0 - kJit1Elems), rlo, rhi);
+      stage_wait_upto<V>(more ? 1 : 0);
+      __syncthreads();
+      const V* tile = tiles + buf * kJitTileElems;
+      const bool inner = t0 + row0 >= SK_K && t0 + ne - 1 + row0 + SK_K < grows;
+      if (inner) jit_elems1<FIRST, SkNb<V, true, 1>>(a, tile, back, t0, ne, comb, st);
+      else jit_elems1<FIRST, SkNb<V, false, 1>>(a, tile, back, t0, ne, comb, st);
+      __syncthreads();  // tile `buf` is free for the tile after next
+      buf ^= 1;
+    }
+    double acc = st.acc;
+#ifdef SK_LOCAL_MAX
+    if (st.lany) acc = comb(acc, (double)st.lmax);
+#endif
+    const double v = block_reduce_c<SK_BLOCK>(comb, neutral, acc, sh);
+    if (threadIdx.x == 0) a.L.partials[c] = v;
+  }
+}
+#endif  // SK_NDIM == 1
+
 }  // namespace sk
 
 extern "C" __global__ void __launch_bounds__(SK_BLOCK, SK_MINB) sk_jit_sweep(const __grid_constant__ sk::JitArgs a) {
@@ -288,8 +399,13 @@ extern "C" __global__ void __launch_bounds__(SK_BLOCK, SK_MINB) sk_jit_sweep(con
   long long it = loop_enter(a.L);
   if (it == 0) return;
   for (;;) {
+#if SK_NDIM == 1
+    if (it == 1) jit_sweep1<sk_in_t, true>(a, it, reinterpret_cast<sk_in_t*>(s_tile), &s_chunk, sh, comb);
+    else jit_sweep1<sk_val_t, false>(a, it, reinterpret_cast<sk_val_t*>(s_tile), &s_chunk, sh, comb);
+#else
     if (it == 1) jit_sweep<sk_in_t, true>(a, it, reinterpret_cast<sk_in_t*>(s_tile), &s_chunk, sh, comb);
     else jit_sweep<sk_val_t, false>(a, it, reinterpret_cast<sk_val_t*>(s_tile), &s_chunk, sh, comb);
+#endif
     if (!a.L.persistent) {
       loop_finalize<SK_BLOCK>(a.L, it, sh, comb);
       return;

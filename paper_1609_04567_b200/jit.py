@@ -1708,6 +1708,8 @@ def build_program(plan, grid, dims=None) -> Program:
         f"#define SK_PAD_EDGE {pad_edge}",
         f"#define SK_PAD_VALUE {pad_lit}",
         f"#define SK_NENV {len(env_types)}",
+        # rank-1 grids: contiguous element tiles (sk_jit_kernel.cuh jit_sweep1)
+        f"#define SK_NDIM {1 if win.ndim == 1 else 2}",
         # byte address of env element `eidx` of slot s (the sweep prefetches
         # a tile's env rows into L1 before computing it)
         "__device__ __forceinline__ const void* sk_env_elem(const SkEnv& e, int s, long long eidx) {",

@@ -567,6 +567,7 @@ class DeviceExecutor(Executor):
         ident = plan.op.identity
         p.identity = float(ident) if isinstance(ident, (int, float, bool, np.number)) else 0.0
         p.params[0] = float(prog.tile_rows)  # the program's SK_TH (rows per work tile)
+        p.params[3] = 1.0 if grid.ndim == 1 else 0.0  # rank 1: contiguous element tiles
         n = len(envs)
         eptr = (C.c_void_p * 4)(*[C.c_void_p(t.data_ptr()) for t in envs])
         epitch = (C.c_int64 * 4)(*[t.stride(0) for t in envs])

@@ -205,3 +205,49 @@ def test_plain_lambda_condition_runs_on_the_device():
                                         as_grid(g), env=as_grid(env), executor=ex)
     assert ex.launches == 1
     _check("jacobi_f64", out, rep)
+
+
+def _wide1d(nb, env):
+    """radius-2 rank-1 smoothing with ABSENT edges (many tiles of the 1D sweep)"""
+    c = nb.center
+    s = c
+    n = 1
+    for d in (-2, -1, 1, 2):
+        v = nb.at(d)
+        if v is not ABSENT_1D:
+            s = s + v
+            n += 1
+    (i,) = nb.center_index
+    return 0.25 * c + 0.75 * (s / n) + 0.001 * env.at(i)
+
+
+ABSENT_1D = J.ABSENT
+
+
+@pytest.mark.parametrize("n,P", [(10007, 1), (20011, 3)])
+def test_rank1_multi_tile_matches_oracle(n, P):
+    """Rank-1 grids run as contiguous element tiles (2048 + radius per tile):
+    several tiles and partitions against the sequential oracle."""
+    g = np.random.default_rng(21).random(n)
+    e = np.random.default_rng(22).random(n)
+    f = sk.ElementalFn(point=_wide1d, k=2)
+    out, rep = sk.parallel_loop("1:n" if P > 1 else "1:1", P, 2, f, sk.max_combinator(0.0),
+                                sk.stop_after(4), sk.Grid((n,), g), env=sk.Grid((n,), e),
+                                delta=sk.Delta(lambda a, b: abs(a - b)))
+
+    class _E:
+        def __init__(self, a):
+            self.a, self.dims = a, a.shape
+
+        def at(self, *idx):
+            return self.a[idx].item()
+
+        def in_range(self, *idx):
+            return 0 <= idx[0] < self.a.shape[0]
+
+    ref, it, val, ex = sequential_loop(_wide1d, 2, lambda a, b: a if b < a else b, 0.0,
+                                       lambda v, i, s: i >= 4, [float(x) for x in g],
+                                       env=_E(e), delta=lambda a, b: abs(a - b))
+    assert rep.iterations == it == 4
+    assert np.array_equal(out.to_array(), np.asarray(ref))
+    assert float(rep.final_reduce) == val
