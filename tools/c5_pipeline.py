@@ -18,7 +18,7 @@ base = [sk.Grid.from_array(O.salt_pepper(O.synthetic_frame(1080, 1920, i), 0.1, 
         for i in range(16)]
 frames = [base[i % 16] for i in range(nf)]
 video_restore_pipeline(frames[:4], width=2)  # warm up (library, clocks)
-for width in (8, 32):
+for width in [int(x) for x in (sys.argv[2].split(",") if len(sys.argv) > 2 else ["8", "32"])]:
     got = []
     torch.cuda.synchronize()
     t0 = time.perf_counter()
