@@ -133,18 +133,23 @@ __device__ __forceinline__ void stage_wait_upto(int pending) {
 }
 
 // env grids are read per element straight from global memory: a tile's env
-// elements (this thread's rows of it) are pulled into L1 before the tile is
-// computed, so the elemental's env loads hit instead of each waiting a DRAM
-// round trip in turn
-__device__ __forceinline__ void env_prefetch(const JitArgs& a, int t, int nr, int gj) {
-  if (gj >= a.g.cols) return;
-  constexpr int RS = SK_BLOCK / SK_TW;
-  const int ty = threadIdx.x / SK_TW;
+// rows are pulled into L1 before the tile is computed, one prefetch per
+// 128-byte line spread over the block (so the elemental's env loads hit
+// instead of each waiting a DRAM round trip in turn)
+__device__ __forceinline__ void env_prefetch(const JitArgs& a, int t0, int nr, int c0) {
 #pragma unroll
-  for (int s = 0; s < SK_NENV; ++s)
-    for (int lr = ty; lr < nr; lr += RS)
-      asm volatile("prefetch.global.L1 [%0];" ::"l"(
-          sk_env_elem(a.env, s, (long long)(t + lr) * a.env.pitch[0] + gj)));
+  for (int s = 0; s < SK_NENV; ++s) {
+    const char* e0 = static_cast<const char*>(sk_env_elem(a.env, s, 0));
+    const int esize = (int)(static_cast<const char*>(sk_env_elem(a.env, s, 1)) - e0);
+    const int lines = esize * SK_TW / 128;  // 128-byte lines per tile row
+    const int cmax = a.g.cols - c0;         // columns of this block inside the grid
+    for (int t = threadIdx.x; t < nr * lines; t += SK_BLOCK) {
+      const int row = t / lines, ln = t - row * lines;
+      if (ln * 128 / esize < cmax)
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(
+            e0 + ((long long)(t0 + row) * a.env.pitch[0] + c0) * esize + ln * 128));
+    }
+  }
 }
 
 // a thread's running reduce state across tiles
@@ -178,9 +183,6 @@ __device__ __forceinline__ void jit_rows(const JitArgs& a, const V* tile, sk_val
   const long long estep = (long long)RS * a.env.pitch[0];
   sk_val_t* bp = back + (long long)(t0 + ty) * g.pitch + gj;
   const long long bstep = (long long)RS * g.pitch;
-  // the tile's grid values are staged; its env elements are not: pull them
-  // into L1 first (measured faster than one tile ahead, or none)
-  env_prefetch(a, t0, nr, gj);
   for (int lr = ty; lr < nr; lr += RS) {
     SkErr err;
     sk_val_t nw;
@@ -244,6 +246,7 @@ __device__ __forceinline__ void jit_sweep(const JitArgs& a, long long it, V* til
       if (more)
         jit_stage<V>(tiles + (buf ^ 1) * kJitTileElems, front, fp, t0 + SK_TH,
                      min(SK_TH, r1 - t0 - SK_TH), c0, rlo, rhi, cols);
+      env_prefetch(a, t0, nr, c0);  // this tile's env rows (not staged)
       stage_wait_upto<V>(more ? 1 : 0);
       __syncthreads();
       const V* tile = tiles + buf * kJitTileElems;

@@ -1729,7 +1729,11 @@ def build_program(plan, grid, dims=None) -> Program:
 
 
 def tile_rows(k: int, esize: int) -> int:
-    """Rows per staged tile: 16, or 8 when two 16-row buffers of the window
-    (+ radius frame, 128 columns wide) would pass 40 KB of shared memory."""
+    """Rows per staged tile: the tallest of 32 / 16 / 8 whose two buffers of
+    the window (+ radius frame, 128 columns wide) fit 40 KB of shared memory
+    (taller tiles spread the per-tile staging and setup over more cells)."""
     ka = (k + 3) // 4 * 4
-    return 16 if 2 * (16 + 2 * k) * (128 + 2 * ka) * esize <= 40 * 1024 else 8
+    for th in (32, 16):
+        if 2 * (th + 2 * k) * (128 + 2 * ka) * esize <= 40 * 1024:
+            return th
+    return 8
