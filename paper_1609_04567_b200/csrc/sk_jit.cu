@@ -33,6 +33,7 @@ struct sk_jit {
   CUmodule mod[64] = {};
   CUfunction fn[64] = {};
   int occ[64] = {};
+  int smem[64] = {};  // dynamic shared memory bytes per launch
   int block = 256;
 };
 
@@ -91,6 +92,9 @@ struct Driver {
   decltype(&cuLaunchCooperativeKernel) launch_coop = nullptr;
   decltype(&cuOccupancyMaxActiveBlocksPerMultiprocessor) occupancy = nullptr;
   decltype(&cuGetErrorName) err = nullptr;
+  decltype(&cuModuleGetGlobal) global = nullptr;
+  decltype(&cuMemcpyDtoH) dtoh = nullptr;
+  decltype(&cuFuncSetAttribute) setattr = nullptr;
 };
 
 const Driver& driver() {
@@ -110,6 +114,9 @@ const Driver& driver() {
     ok &= get("cuLaunchCooperativeKernel", reinterpret_cast<void**>(&d.launch_coop));
     ok &= get("cuOccupancyMaxActiveBlocksPerMultiprocessor", reinterpret_cast<void**>(&d.occupancy));
     ok &= get("cuGetErrorName", reinterpret_cast<void**>(&d.err));
+    ok &= get("cuModuleGetGlobal", reinterpret_cast<void**>(&d.global));
+    ok &= get("cuMemcpyDtoH", reinterpret_cast<void**>(&d.dtoh));
+    ok &= get("cuFuncSetAttribute", reinterpret_cast<void**>(&d.setattr));
     d.ok = ok;
     cudaGetLastError();
   });
@@ -146,11 +153,28 @@ int jit_function(sk_jit* j, int dev, CUfunction* fn) {
       d.unload(m);
       return cu_fail(r, "cuModuleGetFunction(sk_jit_sweep)");
     }
+    // the tile buffers are dynamic shared memory; the program says how much
+    // (sk_jit_smem_bytes), which may pass the 48 KB default
+    int smem = 0;
+    CUdeviceptr gp = 0;
+    size_t gsz = 0;
+    if (d.global(&gp, &gsz, m, "sk_jit_smem_bytes") != CUDA_SUCCESS || gsz != sizeof(int) ||
+        d.dtoh(&smem, gp, sizeof(int)) != CUDA_SUCCESS) {
+      d.unload(m);
+      set_error("sk_jit: program lacks sk_jit_smem_bytes");
+      return SK_ERR_STATE;
+    }
+    r = d.setattr(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, smem);
+    if (r != CUDA_SUCCESS) {
+      d.unload(m);
+      return cu_fail(r, "cuFuncSetAttribute(user elemental shared memory)");
+    }
     int occ = 0;
-    if (d.occupancy(&occ, f, j->block, 0) != CUDA_SUCCESS || occ < 1) occ = 1;
+    if (d.occupancy(&occ, f, j->block, (size_t)smem) != CUDA_SUCCESS || occ < 1) occ = 1;
     j->mod[dev] = m;
     j->fn[dev] = f;
     j->occ[dev] = occ;
+    j->smem[dev] = smem;
   }
   *fn = j->fn[dev];
   return SK_OK;
@@ -245,9 +269,11 @@ int jit_launch(sk_run* r, const LoopCtl& L, cudaStream_t s) {
   if (L.persistent) {
     const int slots = device_sms(r->device) * j->occ[r->device];
     const int grid = r->grid < slots ? r->grid : slots;
-    cr = d.launch_coop(f, grid, 1, 1, r->block, 1, 1, 0, reinterpret_cast<CUstream>(s), params);
+    cr = d.launch_coop(f, grid, 1, 1, r->block, 1, 1, (unsigned)j->smem[r->device],
+                       reinterpret_cast<CUstream>(s), params);
   } else {
-    cr = d.launch(f, r->grid, 1, 1, r->block, 1, 1, 0, reinterpret_cast<CUstream>(s), params, nullptr);
+    cr = d.launch(f, r->grid, 1, 1, r->block, 1, 1, (unsigned)j->smem[r->device],
+                  reinterpret_cast<CUstream>(s), params, nullptr);
   }
   if (cr != CUDA_SUCCESS) return cu_fail(cr, "cuLaunchKernel(user elemental)");
   return SK_OK;

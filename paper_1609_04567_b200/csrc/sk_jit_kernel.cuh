@@ -393,11 +393,14 @@ __device__ __forceinline__ void jit_sweep1(const JitArgs& a, long long it, V* ti
 
 }  // namespace sk
 
+// dynamic shared memory per launch (the host reads it at module load)
+extern "C" __device__ const int sk_jit_smem_bytes = 2 * sk::kJitTileElems * sk::kJitElemMax;
+
 extern "C" __global__ void __launch_bounds__(SK_BLOCK, SK_MINB) sk_jit_sweep(const __grid_constant__ sk::JitArgs a) {
   using namespace sk;
   __shared__ double sh[SK_BLOCK / 32];
   __shared__ int s_chunk;
-  __shared__ __align__(16) unsigned char s_tile[2 * kJitTileElems * kJitElemMax];  // 2 tile buffers
+  extern __shared__ __align__(16) unsigned char s_tile[];  // 2 tile buffers (dynamic)
   const SkComb comb{};
   long long it = loop_enter(a.L);
   if (it == 0) return;

@@ -1730,10 +1730,12 @@ def build_program(plan, grid, dims=None) -> Program:
 
 def tile_rows(k: int, esize: int) -> int:
     """Rows per staged tile: the tallest of 32 / 16 / 8 whose two buffers of
-    the window (+ radius frame, 128 columns wide) fit 40 KB of shared memory
-    (taller tiles spread the per-tile staging and setup over more cells)."""
+    the window (+ radius frame, 128 columns wide) fit the shared-memory
+    budget (dynamic shared memory; taller tiles spread the per-tile staging
+    and setup over more cells, at the price of CTAs per SM)."""
     ka = (k + 3) // 4 * 4
+    budget = int(os.environ.get("SK_JIT_SMEM_KB", "40")) * 1024
     for th in (32, 16):
-        if 2 * (th + 2 * k) * (128 + 2 * ka) * esize <= 40 * 1024:
+        if 2 * (th + 2 * k) * (128 + 2 * ka) * esize <= budget:
             return th
     return 8
