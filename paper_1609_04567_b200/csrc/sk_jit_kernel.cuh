@@ -123,14 +123,54 @@ __device__ __forceinline__ void jit_stage(V* tile, const V* front, long long fp,
     asm volatile("cp.async.commit_group;\n" ::: "memory");
 }
 
+// cp.async groups one staged tile commits: the grid tile (4 / 8-byte
+// elements) and, when staged, env slot 0's tile
+template <class V>
+constexpr int kStageGroups = (sizeof(V) == 4 || sizeof(V) == 8 ? 1 : 0) + (SK_ENV0_STAGE ? 1 : 0);
+
 // wait until at most `pending` staged tiles are still in flight
 template <class V>
 __device__ __forceinline__ void stage_wait_upto(int pending) {
-  if constexpr (sizeof(V) == 4 || sizeof(V) == 8) {
+  if constexpr (kStageGroups<V> == 2) {
+    if (pending) asm volatile("cp.async.wait_group 2;\n" ::: "memory");
+    else asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  } else if constexpr (kStageGroups<V> == 1) {
     if (pending) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
     else asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   }
 }
+
+#if SK_ENV0_STAGE
+// env slot 0 of tile rows [t0, t0 + nr) x columns [c0, c0 + SK_TW) into a
+// SK_TH x SK_TW shared buffer (columns past the grid are not copied: no
+// thread reads them); one commit group
+__device__ __forceinline__ void env0_stage(sk_env0_t* et, const JitArgs& a, int t0, int nr, int c0) {
+  const sk_env0_t* p0 = static_cast<const sk_env0_t*>(a.env.p[0]) + (long long)t0 * a.env.pitch[0] + c0;
+  const long long ep = a.env.pitch[0];
+  constexpr int VE = 16 / sizeof(sk_env0_t);
+  const bool vec = c0 + SK_TW <= a.g.cols &&
+                   ((reinterpret_cast<unsigned long long>(a.env.p[0]) | (ep * sizeof(sk_env0_t))) & 15) == 0;
+  if (vec) {
+    constexpr int NV = SK_TW / VE;
+    for (int v = threadIdx.x; v < nr * NV; v += SK_BLOCK) {
+      const int r = v / NV, cv = v - r * NV;
+      const unsigned d = (unsigned)__cvta_generic_to_shared(et + r * SK_TW + cv * VE);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(p0 + r * ep + cv * VE));
+    }
+  } else {
+    const int cmax = a.g.cols - c0;
+    for (int v = threadIdx.x; v < nr * SK_TW; v += SK_BLOCK) {
+      const int r = v / SK_TW, c = v - r * SK_TW;
+      if (c < cmax) {
+        const unsigned d = (unsigned)__cvta_generic_to_shared(et + r * SK_TW + c);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(d), "l"(p0 + r * ep + c),
+                     "n"((int)sizeof(sk_env0_t)));
+      }
+    }
+  }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+#endif
 
 // env grids are read per element straight from global memory: a tile's env
 // rows are pulled into L1 before the tile is computed, one prefetch per
@@ -165,8 +205,9 @@ struct JitAcc {
 // One tile's rows for this thread: elemental + delta + reduce per element.
 // Per-element pointers advance by a fixed stride (no index arithmetic).
 template <bool FIRST, class NB, class V>
-__device__ __forceinline__ void jit_rows(const JitArgs& a, const V* tile, sk_val_t* back, int t0,
-                                         int nr, int gj, const SkComb& comb, JitAcc<FIRST>& st) {
+__device__ __forceinline__ void jit_rows(const JitArgs& a, const V* tile, const sk_env0_t* etile,
+                                         sk_val_t* back, int t0, int nr, int gj,
+                                         const SkComb& comb, JitAcc<FIRST>& st) {
   constexpr int RS = SK_BLOCK / SK_TW;  // rows between a thread's elements
   const int tx = threadIdx.x % SK_TW, ty = threadIdx.x / SK_TW;
   const Sweep2D& g = a.g;
@@ -180,6 +221,7 @@ __device__ __forceinline__ void jit_rows(const JitArgs& a, const V* tile, sk_val
   nb.cols = cols;
   nb.k = SK_K;
   nb.eidx = (long long)(t0 + ty) * a.env.pitch[0] + gj;  // env element of the centre
+  nb.ec = etile + ty * SK_TW + tx;  // (PRE) the staged env slot 0 element
   const long long estep = (long long)RS * a.env.pitch[0];
   sk_val_t* bp = back + (long long)(t0 + ty) * g.pitch + gj;
   const long long bstep = (long long)RS * g.pitch;
@@ -205,6 +247,7 @@ __device__ __forceinline__ void jit_rows(const JitArgs& a, const V* tile, sk_val
     nb.c += RS * kJitTWP;
     nb.i += RS;
     nb.eidx += estep;
+    nb.ec += RS * SK_TW;
     bp += bstep;
   }
 }
@@ -239,17 +282,30 @@ __device__ __forceinline__ void jit_sweep(const JitArgs& a, long long it, V* til
 #endif
     const int gj = c0 + tx;
     int buf = 0;
+    // env slot 0 tiles follow the two grid tile buffers
+    sk_env0_t* etiles = reinterpret_cast<sk_env0_t*>(
+        reinterpret_cast<unsigned char*>(tiles) + 2 * kJitTileElems * kJitElemMax);
+#if SK_ENV0_STAGE
+    env0_stage(etiles, a, r0, min(SK_TH, r1 - r0), c0);
+#endif
     jit_stage<V>(tiles, front, fp, r0, min(SK_TH, r1 - r0), c0, rlo, rhi, cols);
     for (int t0 = r0; t0 < r1; t0 += SK_TH) {
       const int nr = min(SK_TH, r1 - t0);
       const bool more = t0 + SK_TH < r1;
-      if (more)
+      if (more) {
+#if SK_ENV0_STAGE
+        env0_stage(etiles + (buf ^ 1) * SK_TH * SK_TW, a, t0 + SK_TH, min(SK_TH, r1 - t0 - SK_TH), c0);
+#endif
         jit_stage<V>(tiles + (buf ^ 1) * kJitTileElems, front, fp, t0 + SK_TH,
                      min(SK_TH, r1 - t0 - SK_TH), c0, rlo, rhi, cols);
+      }
+#if !SK_ENV0_STAGE
       env_prefetch(a, t0, nr, c0);  // this tile's env rows (not staged)
+#endif
       stage_wait_upto<V>(more ? 1 : 0);
       __syncthreads();
       const V* tile = tiles + buf * kJitTileElems;
+      const sk_env0_t* etile = etiles + buf * SK_TH * SK_TW;
       if (gj < cols) {
         // NB = SkNb<V, true> when all of this thread's windows in the tile
         // are on the grid: every ABSENT test compiles away
@@ -261,8 +317,13 @@ __device__ __forceinline__ void jit_sweep(const JitArgs& a, long long it, V* til
         st.lmax = lmax;
         st.lany = lany;
 #endif
-        if (inner) jit_rows<FIRST, SkNb<V, true, kJitTWP>>(a, tile, back, t0, nr, gj, comb, st);
-        else jit_rows<FIRST, SkNb<V, false, kJitTWP>>(a, tile, back, t0, nr, gj, comb, st);
+        constexpr bool PRE = SK_ENV0_STAGE != 0;
+        if (inner)
+          jit_rows<FIRST, SkNb<V, true, kJitTWP, sk_env0_t, PRE>>(a, tile, etile, back, t0, nr, gj,
+                                                                  comb, st);
+        else
+          jit_rows<FIRST, SkNb<V, false, kJitTWP, sk_env0_t, PRE>>(a, tile, etile, back, t0, nr,
+                                                                   gj, comb, st);
         acc = st.acc;
 #ifdef SK_LOCAL_MAX
         lmax = st.lmax;
@@ -394,7 +455,9 @@ __device__ __forceinline__ void jit_sweep1(const JitArgs& a, long long it, V* ti
 }  // namespace sk
 
 // dynamic shared memory per launch (the host reads it at module load)
-extern "C" __device__ const int sk_jit_smem_bytes = 2 * sk::kJitTileElems * sk::kJitElemMax;
+extern "C" __device__ const int sk_jit_smem_bytes =
+    2 * sk::kJitTileElems * sk::kJitElemMax +
+    (SK_ENV0_STAGE ? 2 * SK_TH * SK_TW * (int)sizeof(sk::sk_env0_t) : 0);
 
 extern "C" __global__ void __launch_bounds__(SK_BLOCK, SK_MINB) sk_jit_sweep(const __grid_constant__ sk::JitArgs a) {
   using namespace sk;

@@ -48,7 +48,9 @@ struct SkErr {
 // reference's `is not ABSENT`).  IN: the whole window is known to be on the
 // grid (interior tiles), so `ok` is the constant true and every ABSENT test
 // in the generated elemental folds away at compile time.
-template <class V, bool IN = false, int STRIDE = 0>
+struct SkEnv;
+
+template <class V, bool IN = false, int STRIDE = 0, class E0 = float, bool PRE = false>
 struct SkNb {
   const V* c;       // centre slot in the staged tile
   int stride;       // tile row stride (elements)
@@ -56,6 +58,7 @@ struct SkNb {
   int rows, cols;   // grid dims
   int k;            // radius
   long long eidx;   // element index of the centre in the env grids (all pitch == env.pitch[0])
+  const E0* ec;     // PRE: env slot 0 at the centre, staged in shared memory
   // STRIDE: the tile row stride as a compile-time constant (0: use `stride`)
   __device__ __forceinline__ V at(int di, int dj) const {
     return c[di * (STRIDE ? STRIDE : stride) + dj];
@@ -63,6 +66,9 @@ struct SkNb {
   // true when the whole window is on the grid (and, for row blocks, every
   // env row within the radius is resident): ABSENT / bounds tests fold away
   __device__ static constexpr bool inner() { return IN; }
+  // env.at(*nb.center_index): slot 0 from the staged env tile when PRE
+  template <class T>
+  __device__ __forceinline__ T centre_env(const SkEnv& env, int slot) const;
   __device__ __forceinline__ bool ok(int di, int dj) const {
     if constexpr (IN) return true;
     return (unsigned)(i + di) < (unsigned)rows && (unsigned)(j + dj) < (unsigned)cols;
@@ -95,6 +101,16 @@ struct SkEnv {
   // with its halo rows)
   __device__ __forceinline__ bool resident(long long i) const { return i >= lo && i < hi; }
 };
+
+template <class V, bool IN, int STRIDE, class E0, bool PRE>
+template <class T>
+__device__ __forceinline__ T SkNb<V, IN, STRIDE, E0, PRE>::centre_env(const SkEnv& env,
+                                                                     int slot) const {
+  if constexpr (PRE) {
+    if (slot == 0) return (T)*ec;
+  }
+  return env.at_centre<T>(slot, eidx);
+}
 
 // (i, j) within the radius of an interior window's centre: on the grid and
 // resident, no checks needed (false for border windows)

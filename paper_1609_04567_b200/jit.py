@@ -900,7 +900,7 @@ class Translator:
         cst, sem = self.win.env[slot]
         if _centre_offset(i.c, "i") == 0 and _centre_offset(j.c, "j") == 0:
             # the centre's own env element: on the grid and resident
-            return num(f"(({CTYPE[sem]})env.at_centre<{cst}>({slot}, nb.eidx))", sem)
+            return num(f"(({CTYPE[sem]})nb.template centre_env<{cst}>(env, {slot}))", sem)
         ii = self.fresh(INT, i.c)
         jj = self.fresh(INT, j.c)
         # Within the radius of the centre an env element is on the grid and
@@ -1696,7 +1696,14 @@ def build_program(plan, grid, dims=None) -> Program:
     else:
         pad_lit = _lit(pad, val_t if isinstance(pad, float) or val_t == F32 else INT) \
             if val_t != BOOL else _lit(bool(pad), BOOL)
-    th = tile_rows(k, max(np.dtype(in_dtype).itemsize, np.dtype(out_dtype).itemsize))
+    # env slot 0 staged in shared memory: measured faster for 4-byte grids and
+    # env (f32 Jacobi 16384^2: 0.75 -> 0.69 ms with 32-row tiles at 72 KB),
+    # slower for 8-byte ones (fewer CTAs per SM), which keep the L1 prefetch
+    esize = max(np.dtype(in_dtype).itemsize, np.dtype(out_dtype).itemsize)
+    env0_size = np.dtype(grid_dtype(env_grids[0])).itemsize if env_grids else 0
+    env0_stage = win.ndim == 2 and env0_size == 4 and esize == 4
+    th = tile_rows(k, esize, env0_size if env0_stage else 0,
+                   budget_kb=72 if env0_stage else 40)
     head = [
         '#include "sk_jit_prelude.cuh"',
         "namespace sk {",
@@ -1708,6 +1715,10 @@ def build_program(plan, grid, dims=None) -> Program:
         f"#define SK_PAD_EDGE {pad_edge}",
         f"#define SK_PAD_VALUE {pad_lit}",
         f"#define SK_NENV {len(env_types)}",
+        # env slot 0 is staged per tile in shared memory next to the grid
+        # tile (2D sweeps; 4- or 8-byte elements)
+        f"#define SK_ENV0_STAGE {1 if env0_stage else 0}",
+        f"typedef {env_types[0][0] if env_types else 'float'} sk_env0_t;",
         # rank-1 grids: contiguous element tiles (sk_jit_kernel.cuh jit_sweep1)
         f"#define SK_NDIM {1 if win.ndim == 1 else 2}",
         # byte address of env element `eidx` of slot s (the sweep prefetches
@@ -1728,14 +1739,16 @@ def build_program(plan, grid, dims=None) -> Program:
                    int_value=int_value, tile_rows=th)
 
 
-def tile_rows(k: int, esize: int) -> int:
+def tile_rows(k: int, esize: int, env0: int = 0, budget_kb: int = 40) -> int:
     """Rows per staged tile: the tallest of 32 / 16 / 8 whose two buffers of
-    the window (+ radius frame, 128 columns wide) fit the shared-memory
-    budget (dynamic shared memory; taller tiles spread the per-tile staging
-    and setup over more cells, at the price of CTAs per SM)."""
+    the window (+ radius frame, 128 columns wide) -- and of env slot 0's
+    tile, `env0` bytes per element, when it is staged -- fit the
+    shared-memory budget (dynamic shared memory; taller tiles spread the
+    per-tile staging and setup over more cells, at the price of CTAs per
+    SM)."""
     ka = (k + 3) // 4 * 4
-    budget = int(os.environ.get("SK_JIT_SMEM_KB", "40")) * 1024
+    budget = int(os.environ.get("SK_JIT_SMEM_KB", str(budget_kb))) * 1024
     for th in (32, 16):
-        if 2 * (th + 2 * k) * (128 + 2 * ka) * esize <= budget:
+        if 2 * (th + 2 * k) * (128 + 2 * ka) * esize + 2 * th * 128 * env0 <= budget:
             return th
     return 8

@@ -196,4 +196,4 @@ def test_interior_window_specialisation():
     plan = LoopPlan(fn=sk.ElementalFn(point=centre, k=1), k=1, op=sk.sum_combinator(0.0),
                     env=sk.Grid(e.shape, e))
     src = jit.build_program(plan, sk.Grid(g.shape, g)).source
-    assert "env.at_centre<double>(0, nb.eidx)" in src and "env.ok(" not in src
+    assert "nb.template centre_env<double>(env, 0)" in src and "env.ok(" not in src
