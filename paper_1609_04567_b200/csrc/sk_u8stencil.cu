@@ -361,7 +361,7 @@ __device__ __forceinline__ void sobel_round2(F2 n, unsigned& lo, unsigned& hi) {
 }
 
 #ifndef SK_SOBEL_MINB
-#define SK_SOBEL_MINB 5
+#define SK_SOBEL_MINB 4
 #endif
 #ifndef SK_SOBEL_UNROLL
 #define SK_SOBEL_UNROLL 2
