@@ -414,7 +414,10 @@ __global__ void __launch_bounds__(BLOCK, PAIRED ? SK_SOBEL_MINB : 1) sobel_sweep
   constexpr unsigned FULL = 0xffffffffu;
   __shared__ double sh[BLOCK / 32];
   // PAIRED: per-warp ring of RING input-row slots
-  constexpr int RING = 8, SLOT = 288;
+#ifndef SK_SOBEL_RING
+#define SK_SOBEL_RING 8
+#endif
+  constexpr int RING = SK_SOBEL_RING, SLOT = 288;  // RING: a power of two
   __shared__ __align__(128) unsigned char ring_mem[PAIRED ? (BLOCK / 32) * RING * SLOT : 16];
   unsigned K;  // 0x4B000000, opaque to the compiler (see lane_lo)
   asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(K) : "l"(a.magic));
