@@ -18,6 +18,8 @@
 // so sqrt(n) is never within 4.9e-4 of a rounding boundary k+0.5 for k <= 255,
 // and n >= 255.5^2 clips to 255), so the hardware sqrt.approx is exact here;
 // tests compare every pixel against the reference.
+#include <type_traits>
+
 #include "sk_internal.h"
 #include "sk_sweep.cuh"
 
@@ -615,7 +617,10 @@ __global__ void __launch_bounds__(BLOCK, PAIRED ? SK_SOBEL_MINB : 1) sobel_sweep
     F2 G[4], SA[4], SB[4], DA[4], DB[4];
     unsigned char* po = back + (long long)r0 * op + colx;
     const F2 two_c = f2_splat(2.0f);
-    auto step = [&](unsigned so, F2* Sold, F2* Dprev, F2* Dnew) {
+    // FULL (every column of the warp's strip inside the image -- all but the
+    // last column block): no byte masks, unconditional stores
+    auto step = [&](auto full, unsigned so, F2* Sold, F2* Dprev, F2* Dnew) {
+      constexpr bool FULL = decltype(full)::value;
       F2 S[4];
       take(so, S, Dnew);
       unsigned o[8];
@@ -631,8 +636,12 @@ __global__ void __launch_bounds__(BLOCK, PAIRED ? SK_SOBEL_MINB : 1) sobel_sweep
       const unsigned x23 = __vminu2(__byte_perm(o[2], o[3], 0x5410u), 0x00ff00ffu);
       const unsigned y01 = __vminu2(__byte_perm(o[4], o[5], 0x5410u), 0x00ff00ffu);
       const unsigned y23 = __vminu2(__byte_perm(o[6], o[7], 0x5410u), 0x00ff00ffu);
-      const unsigned ox = __byte_perm(x01, x23, 0x6420u) & mx;
-      const unsigned oy = __byte_perm(y01, y23, 0x6420u) & my;
+      unsigned ox = __byte_perm(x01, x23, 0x6420u);
+      unsigned oy = __byte_perm(y01, y23, 0x6420u);
+      if constexpr (!FULL) {
+        ox &= mx;
+        oy &= my;
+      }
       if (REDUCE == SK_REDUCE_MAX) {
         const unsigned m = __vmaxu4(ox, oy);
         const unsigned m2 = __vmaxu4(m, m >> 16);
@@ -641,8 +650,8 @@ __global__ void __launch_bounds__(BLOCK, PAIRED ? SK_SOBEL_MINB : 1) sobel_sweep
         acc = __dp4a(ox, 0x01010101u, acc);
         acc = __dp4a(oy, 0x01010101u, acc);
       }
-      if (nx > 0) *reinterpret_cast<unsigned*>(po) = ox;
-      if (ny > 0) *reinterpret_cast<unsigned*>(po + 128) = oy;
+      if (FULL || nx > 0) *reinterpret_cast<unsigned*>(po) = ox;
+      if (FULL || ny > 0) *reinterpret_cast<unsigned*>(po + 128) = oy;
       po += op;
     };
 #pragma unroll
@@ -652,13 +661,17 @@ __global__ void __launch_bounds__(BLOCK, PAIRED ? SK_SOBEL_MINB : 1) sobel_sweep
 #pragma unroll
     for (int k = 0; k < 4; ++k) G[k] = f2_fma(DB[k], two_c, DA[k]);
     // step i: S(i-2) is in SA for even i, SB for odd i; D(i-1) in DB / DA
-    int i = 2;
+    auto rows_loop = [&](auto full) {
+      int i = 2;
 #pragma unroll (kSobelUnroll)
-    for (; i + 2 <= n_in; i += 2) {
-      step((i & (RING - 1)) * SLOT, SA, DB, DA);
-      step(((i + 1) & (RING - 1)) * SLOT, SB, DA, DB);
-    }
-    if (i < n_in) step((i & (RING - 1)) * SLOT, SA, DB, DA);
+      for (; i + 2 <= n_in; i += 2) {
+        step(full, (i & (RING - 1)) * SLOT, SA, DB, DA);
+        step(full, ((i + 1) & (RING - 1)) * SLOT, SB, DA, DB);
+      }
+      if (i < n_in) step(full, (i & (RING - 1)) * SLOT, SA, DB, DA);
+    };
+    if (cols - cb * (32 * VEC) >= 32 * VEC) rows_loop(std::true_type{});
+    else rows_loop(std::false_type{});
     } else {
     unsigned S0[4], D0[4], S1[4], D1[4], S2[4], D2[4];
     {
