@@ -461,10 +461,16 @@ def c5(args, ClockSampler, measured_peaks, local=0, world=1, rank=0, width=32):
     # e2e: the reference's pipeline shape, host frames in / host frames out
     frames = [sk.Grid.from_array(distinct[i % len(distinct)]) for i in range(min(total, 256))]
     video_restore_pipeline(frames[:16], width=width, writer=lambda g: g.to_array())  # warm
-    got = []
-    t0 = time.perf_counter()
-    video_restore_pipeline(frames, width=width, writer=lambda g: got.append(g.to_array()))
-    e2e_s = time.perf_counter() - t0
+    # three passes, the median reported (the host side of the stream --
+    # fresh fp64 frames, 32 replica threads -- varies run to run)
+    passes = []
+    for _ in range(3):
+        got = []
+        t0 = time.perf_counter()
+        video_restore_pipeline(frames, width=width, writer=lambda g: got.append(g.to_array()))
+        passes.append(time.perf_counter() - t0)
+        del got
+    e2e_s = statistics.median(passes)
     line = _base(args, "frames/s (denoise)", "frames/s", total * world / sec, sec * 1e3, "f64",
                  f"C5 video denoise 1000 synthetic 1920x1080 frames, 10% noise "
                  f"({len(distinct)} distinct frames cycled), device farm batches of {B}",
@@ -482,9 +488,11 @@ def c5(args, ClockSampler, measured_peaks, local=0, world=1, rank=0, width=32):
     line.update({
         "gpu_launches": None,
         "e2e": {"value": len(frames) / e2e_s, "unit": "frames/s",
+                "passes_frames_per_s": [round(len(frames) / x, 1) for x in passes],
                 "h2d_bytes_per_step": len(frames) * 1080 * 1920,
                 "d2h_bytes_per_step": len(frames) * 1080 * 1920 * 8,
-                "mode": f"video_restore_pipeline(width={width}) over {len(frames)} host frames"},
+                "mode": f"median of 3 passes of video_restore_pipeline(width={width}) over "
+                        f"{len(frames)} host frames"},
         "roofline": restore_roofline(int(counts.sum()), t1),
         "cpu_baseline": cpu_line,
         "clocks": clk.summary(),
