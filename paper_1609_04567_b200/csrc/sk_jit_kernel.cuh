@@ -78,11 +78,18 @@ __device__ __forceinline__ void jit_stage(V* tile, const V* front, long long fp,
     if (rows_in && cols_in && aligned) {
       constexpr int VE = 16 / sizeof(V);
       constexpr int NV = kJitTWP / VE;  // vectors per tile row
-      for (int v = threadIdx.x; v < nrow * NV; v += SK_BLOCK) {
-        const int tr = v / NV, cv = v - tr * NV;
-        const unsigned d = (unsigned)__cvta_generic_to_shared(tile + tr * kJitTWP + cv * VE);
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d),
-                     "l"(p + (long long)tr * fp + cv * VE));
+      constexpr int NW = SK_BLOCK / 32;
+      // warp w copies rows w, w + NW, ...; its lanes cover the row's NV
+      // vectors (no index division; addresses advance by whole rows)
+      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+      const unsigned d0 = (unsigned)__cvta_generic_to_shared(tile + warp * kJitTWP);
+      const V* s0 = p + (long long)warp * fp;
+      for (int tr = warp; tr < nrow; tr += NW) {
+#pragma unroll
+        for (int cv = lane; cv < NV; cv += 32)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(
+                           d0 + (unsigned)(((tr - warp) * kJitTWP + cv * VE) * sizeof(V))),
+                       "l"(s0 + (long long)(tr - warp) * fp + cv * VE));
       }
       asm volatile("cp.async.commit_group;\n" ::: "memory");
       return;
