@@ -833,7 +833,7 @@ int geometry(int device, U8Fn fn, long long rows, long long cols, int nparts, co
       (long long)device_sms(device) * occupancy(reinterpret_cast<const void*>(fn), kBlock);
   *colblocks = (int)((cols + 32 * kVec - 1) / (32 * kVec));  // one warp per chunk
 #ifndef SK_U8_CHUNKS_PER_WARP
-#define SK_U8_CHUNKS_PER_WARP 8
+#define SK_U8_CHUNKS_PER_WARP 16
 #endif
   const long long want = slots * (kBlock / 32) * SK_U8_CHUNKS_PER_WARP;
   long long ch = (rows * (long long)*colblocks * frames + want - 1) / want;
