@@ -208,7 +208,7 @@ def run_ours(args):
     h_u0 = torch.zeros((n, n), dtype=torch.float32).pin_memory()
     h_f = torch.ones((n, n), dtype=torch.float32).pin_memory()
     h_out = torch.empty((n, n), dtype=torch.float32).pin_memory()
-    e2e_steps = max(1, min(args.steps, 3))
+    e2e_steps = max(2, min(args.steps, 5))
     ex2 = sk.DeviceExecutor(1)
     # Pipelined like a stream of solves: step k+1's inputs go up on a copy
     # stream while step k solves, and step k's result comes down on another
