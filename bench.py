@@ -126,6 +126,31 @@ def cpu_reference(n_cells_target: float, steps: int):
 
 # ----------------------------------------------------------------------------- GPU arm
 
+C4_FINAL = 8.118152618408203e-05  # reference C1 / oracle C4 final max|delta| (36 iterations)
+
+
+def golden_prod(name):
+    p = os.path.join(ROOT, "tests", "golden", "golden_prod.json")
+    with open(p) as fh:
+        return json.load(fh).get(name)
+
+
+def sha256_of(t):
+    import hashlib
+
+    return hashlib.sha256(t.contiguous().cpu().numpy().tobytes()).hexdigest()
+
+
+def check_c4_result(n, rep, out):
+    """Fail the bench unless the measured solve is the reference's: 36
+    iterations, final max|delta| bit-equal, and (at 32768^2) the output grid's
+    SHA-256 equal to the pinned oracle's (make_golden_prod.py)."""
+    assert rep.iterations == 36 and not rep.exhausted, rep
+    assert rep.final_reduce == C4_FINAL, rep.final_reduce
+    g = golden_prod("prod_C4_f32_max_unit_%d" % n)
+    if g is not None:
+        assert sha256_of(out.tensor()) == g["sha"], "C4 output grid differs from the oracle"
+
 
 def run_workload(args):
     """--workload c1|c2|c3|c5 (bench_workloads.py); c4 is run_ours below."""
@@ -136,11 +161,16 @@ def run_workload(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    dev, shared = rank_device(local, world)
+    torch.cuda.set_device(dev)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    local = dev
     fn = getattr(W, args.workload)
     if args.workload in ("c2", "c5"):
         line = fn(args, ClockSampler, measured_peaks, local=local, world=world, rank=rank)
@@ -163,9 +193,9 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
     if world > 1:
         return run_distributed(args, world, rank, local)
+    torch.cuda.set_device(local)
     n = args.n
     cfg = HelmholtzConfig(rows=n, cols=n)
     kern = helmholtz_kernel(cfg)
@@ -194,6 +224,7 @@ def run_ours(args):
             out, rep = solve(ex)
             kernel_ms += ex.last_kernel_time[0]
             kernel_n += ex.last_kernel_time[1]
+            out_last = out
             del out
         stop.record()
         torch.cuda.synchronize()
@@ -201,8 +232,10 @@ def run_ours(args):
     cells = float(n) * n * rep.iterations
     value = cells / (ms / 1e3)
 
-    # parity on the benchmark config itself: iterations and final reduce
-    assert rep.iterations == 36 and not rep.exhausted, rep
+    # parity on the benchmark config itself: iterations, final reduce and
+    # the output grid against the pinned oracle (tests/golden/golden_prod.json)
+    check_c4_result(n, rep, out_last)
+    del out_last
 
     # ---- e2e through the public API from pinned host buffers
     h_u0 = torch.zeros((n, n), dtype=torch.float32).pin_memory()
@@ -240,6 +273,7 @@ def run_ours(args):
         o, r2 = sk.loop_stencil_reduce_d(1, kern, sk.abs_change(), sk.max_combinator(0.0), cond,
                                          sk.Grid.from_tensor(du), env=sk.Grid.from_tensor(df),
                                          executor=ex2)
+        assert r2.iterations == rep.iterations and r2.final_reduce == rep.final_reduce, r2
         ot = o.tensor()
         down_s.wait_stream(cur)
         with torch.cuda.stream(down_s):
@@ -296,12 +330,212 @@ def run_ours(args):
     print(json.dumps(line))
 
 
-def run_distributed(args, world, rank, local):
-    from paper_1609_04567_b200 import distributed as D
+def _free_port():
+    import socket
 
-    line = D.bench_weak_scaling(args, world, rank, local, ClockSampler, measured_peaks)
-    if rank == 0 and line is not None:
-        print(json.dumps(line))
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def launch_command(n: int, argv, port: int):
+    """The torchrun command `bench.py --gpus N` re-executes itself under when
+    it is started without WORLD_SIZE (one rank per GPU, rendezvous on
+    127.0.0.1)."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+            f"--nproc-per-node={n}", "--master-addr=127.0.0.1", f"--master-port={port}",
+            os.path.abspath(__file__), *argv]
+
+
+def rank_device(local: int, world: int):
+    """(cuda index, shared): one GPU per rank; with fewer GPUs than ranks
+    (a dry run on one GPU) ranks share devices round-robin."""
+    import torch
+
+    ndev = max(torch.cuda.device_count(), 1)
+    return local % ndev, ndev < world
+
+
+def peer_copy_gbs(src_dev: int, dst_dev: int, nbytes: int = 1 << 28, reps: int = 10):
+    """GPU->GPU copy bandwidth over the peer link (NVLink on a B200 node),
+    CUDA events on the source device; None when the two are one device."""
+    import torch
+
+    if src_dev == dst_dev:
+        return None
+    a = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{src_dev}")
+    b = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{dst_dev}")
+    with torch.cuda.device(src_dev):
+        b.copy_(a)
+        torch.cuda.synchronize(src_dev)
+        torch.cuda.synchronize(dst_dev)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(reps):
+            b.copy_(a, non_blocking=True)
+        e.record()
+        torch.cuda.synchronize(src_dev)
+        torch.cuda.synchronize(dst_dev)
+    return nbytes * reps / (s.elapsed_time(e) / 1e3) / 1e9
+
+
+def run_distributed(args, world, rank, local):
+    """C4 over N ranks (one per GPU): row blocks of the global grid with one
+    halo row per neighbour per iteration and the rank-ordered MAX fold of
+    the partials (distributed.DeviceBlock).  --scaling weak: every rank a
+    32768 x 32768 block of a (32768 N) x 32768 grid; strong: the global
+    32768^2 grid split by the reference's _split_ranges (partition.py:187-195).
+    Timing is on the device, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1609_04567_b200 import distributed as D
+    from paper_1609_04567_b200.partition import _split_ranges
+
+    dev, shared = rank_device(local, world)
+    torch.cuda.set_device(dev)
+    # ranks sharing one GPU cannot use NCCL (one communicator per device):
+    # the dry run rendezvous over gloo, the halo / partial path is the same
+    backend = "gloo" if shared else "nccl"
+    if not dist.is_initialized():
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group("gloo")
+    n = args.n
+    strong = args.scaling == "strong"
+    rows = (lambda r: r[1] - r[0])(_split_ranges(n, world)[rank]) if strong else n
+    transport = args.transport
+    consts = (1.0, 1.0, 5.0, 0.0, 1.0)
+    cond = D.make_cond("lt", TOL, 0.0, 10_000)
+    u0 = torch.zeros((rows, n), dtype=torch.float32, device="cuda")
+    f = torch.ones((rows, n), dtype=torch.float32, device="cuda")
+
+    def solve(timing=False, a=u0, b=f):
+        blk = D.DeviceBlock(a, b, consts, rank=rank, world=world, timing=timing,
+                            transport=transport)
+        res = D.run_block_loop(blk, cond)
+        kt = blk.kernel_time() if timing else (0.0, 0)
+        nl = blk.launches()
+        return blk, res, kt, nl
+
+    def max_over_ranks(x):
+        t = torch.tensor([x], dtype=torch.float64, device="cuda" if backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def timed(fn, steps):
+        torch.cuda.synchronize()
+        dist.barrier()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        acc = fn(steps)
+        e.record()
+        torch.cuda.synchronize()
+        dist.barrier()
+        return max_over_ranks(s.elapsed_time(e)), acc
+
+    for _ in range(args.warmup):
+        blk, res, _, _ = solve()
+        blk.close()
+    # 1) production path: device-decided stop, no per-sweep events
+    def prod_steps(k):
+        out = {"launches": 0, "res": None}
+        for _ in range(k):
+            blk, res, _, nl = solve()
+            out["launches"] += nl
+            out["res"] = (res.iterations, res.final_reduce, res.exhausted)
+            blk.close()
+        return out
+
+    with ClockSampler(dev) as clk:
+        total_ms, acc = timed(prod_steps, args.steps)
+    ms = total_ms / args.steps
+    iters, final, exhausted = acc["res"]
+    assert iters == 36 and not exhausted and final == C4_FINAL, acc["res"]
+
+    # 2) the same solves with per-sweep CUDA events (roofline denominator)
+    def timing_steps(k):
+        kms, kn = 0.0, 0
+        for _ in range(k):
+            blk, res, kt, _ = solve(timing=True)
+            kms += kt[0]
+            kn += kt[1]
+            blk.close()
+        return kms / max(kn, 1), kn
+
+    _, (avg_kernel_ms, kn) = timed(timing_steps, max(1, min(args.steps, 3)))
+    avg_kernel_ms = max_over_ranks(avg_kernel_ms)
+    cells_rank = float(rows) * n * iters
+    cells = float(n) * n * iters * (1 if strong else world)
+
+    # 3) e2e: every rank's block from pinned host memory, its rows back
+    h_u0 = torch.zeros((rows, n), dtype=torch.float32).pin_memory()
+    h_f = torch.ones((rows, n), dtype=torch.float32).pin_memory()
+    h_out = torch.empty((rows, n), dtype=torch.float32).pin_memory()
+
+    def e2e_steps(k):
+        for _ in range(k):
+            du0 = h_u0.to("cuda", non_blocking=True)
+            df = h_f.to("cuda", non_blocking=True)
+            blk, r2, _, _ = solve(a=du0, b=df)
+            h_out.copy_(r2.out, non_blocking=True)
+            torch.cuda.synchronize()
+            assert (r2.iterations, r2.final_reduce) == (iters, final)
+            blk.close()
+
+    e2e_n = max(1, min(args.steps, 3))
+    e2e_total, _ = timed(e2e_steps, e2e_n)
+    e2e_ms = e2e_total / e2e_n
+
+    nvlink = peer_copy_gbs(dev, rank_device(1, world)[0]) if rank == 0 and world > 1 else None
+    peak, peak_kind = measured_peaks()
+    alg = BYTES_PER_CELL["f32"] * float(rows) * n
+    achieved = alg / (avg_kernel_ms / 1e3) / 1e9
+    row_bytes = 4 * n
+    halo_iter = 2 * (world - 1) * row_bytes  # each interior boundary: one row each way
+    if rank != 0:
+        return
+    line = {
+        "metric": "stencil cell-updates/s", "value": cells / (ms / 1e3),
+        "unit": "cell-updates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong" if strong else "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (rhs=1, u0=0)",
+        "config": {"workload": (f"C4 Helmholtz/Jacobi {n}x{n} fp32 split over {world} ranks"
+                                if strong else
+                                f"C4 Helmholtz/Jacobi ({n}*{world})x{n} fp32 (32768^2 per GPU)")
+                   + ", MAX|delta|<1e-4",
+                   "rows_per_rank": rows, "cols": n, "iterations_per_step": iters,
+                   "final_reduce": final, "parallelism": f"row blocks x{world}, " + (
+                       "halo rows + partials stored by the sweep kernel into peer memory, "
+                       "stream waits on peer flags, device-side rank-ordered combine"
+                       if transport == "peer" else
+                       "NCCL halo rows + all-gather, device-side rank-ordered combine"),
+                   "transport": transport, "backend": backend,
+                   "shared_gpu": shared,
+                   "l2": "inputs >= 4.3 GB/array > 126 MB L2 (no flush needed)"},
+        "gpu_launches": acc["launches"],
+        "e2e": {"value": cells / (e2e_ms / 1e3), "unit": "cell-updates/s",
+                "h2d_bytes_per_step": 2 * 4 * rows * n * world,
+                "d2h_bytes_per_step": 4 * rows * n * world, "ms_per_step": e2e_ms,
+                "mode": "per rank: pinned H2D of its u0/f rows, the solve, D2H of its rows; "
+                        "max over ranks"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "kernel": "helmholtz_sweep<float> (+ fused peer halo stores), max over ranks",
+                     "alg_bytes_per_launch": alg, "avg_kernel_ms": avg_kernel_ms,
+                     "kernel_launches_timed": kn, "peak_source": peak_kind},
+        "halo": {"bytes_per_iteration": halo_iter,
+                 "avg_gbs_over_solve": halo_iter * iters / (ms / 1e3) / 1e9,
+                 "peer_copy_gbs_rank0_to_1": nvlink,
+                 "note": "halo rows are stored by the sweep kernel (overlapped with it); the "
+                         "link figure is a 256 MiB device-to-device copy between ranks 0 and 1; "
+                         "ncu recipe for the stores themselves in profiles/README.md"},
+        "cells_per_rank_per_step": cells_rank,
+        "cpu_baseline": None,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line))
 
 
 def run_reference(args):
@@ -346,7 +580,17 @@ def main():
                          "kernel (default) or by NCCL send/recv + all-gather")
     ap.add_argument("--workload", default="c4", choices=["c1", "c2", "c3", "c4", "c5"],
                     help="BASELINE.json config (default c4: the cell-updates/s headline)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="C4 with N>1: 32768^2 per GPU (weak) or one 32768^2 grid split over "
+                         "the ranks (strong)")
     args = ap.parse_args()
+    world_env = os.environ.get("WORLD_SIZE")
+    if world_env is None and args.gpus > 1:
+        # one rank per GPU: re-run this command under torchrun
+        sys.exit(subprocess.call(launch_command(args.gpus, sys.argv[1:], _free_port())))
+    if world_env is not None and int(world_env) != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world_env}; launch one rank "
+                 "per GPU (or omit WORLD_SIZE and let bench.py start torchrun itself)")
     if args.impl == "reference":
         run_reference(args)
     elif args.workload != "c4":

@@ -375,112 +375,6 @@ def run_block_loop(block, cond, batch: int = 4) -> BlockResult:
     return BlockResult(iterations=it, final_reduce=val, exhausted=ex, out=out)
 
 
-# ---------------------------------------------------------------- bench driver
-
-
-def bench_weak_scaling(args, world: int, rank: int, local: int, ClockSampler, measured_peaks):
-    """C4 weak scaling: every rank a 32768 x 32768 fp32 block of a (32768*P) x
-    32768 grid; returns rank 0's JSON line (None on other ranks)."""
-    import torch
-
-    dist = _dist()
-    if not dist.is_initialized():
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    torch.cuda.set_device(local)
-    n = args.n
-    transport = getattr(args, "transport", "peer")
-    consts = (1.0, 1.0, 5.0, 0.0, 1.0)
-    cond = make_cond("lt", 1e-4, 0.0, 10_000)
-    u0 = torch.zeros((n, n), dtype=torch.float32, device="cuda")
-    f = torch.ones((n, n), dtype=torch.float32, device="cuda")
-
-    def solve(timing=False):
-        blk = DeviceBlock(u0, f, consts, rank=rank, world=world, timing=timing,
-                          transport=transport)
-        res = run_block_loop(blk, cond)
-        kt = blk.kernel_time() if timing else (0.0, 0)
-        nl = blk.launches()
-        blk.close()
-        return res, kt, nl
-
-    for _ in range(args.warmup):
-        res, _, _ = solve()
-    torch.cuda.synchronize()
-    dist.barrier()
-    kms, kn, launches = 0.0, 0, 0
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        torch.cuda.synchronize()
-        dist.barrier()
-        s.record()
-        for _ in range(args.steps):
-            res, kt, nl = solve(timing=True)
-            kms += kt[0]
-            kn += kt[1]
-            launches += nl
-            del res
-        e.record()
-        torch.cuda.synchronize()
-        dist.barrier()
-    ms = torch.tensor([s.elapsed_time(e) / args.steps], dtype=torch.float64, device="cuda")
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    ms = float(ms.item())
-    res, _, _ = solve()
-    iters = res.iterations
-    cells = float(world) * n * n * iters
-    # e2e: every rank's block from pinned host memory and its result back,
-    # copies inside the timed region (max over ranks)
-    h_u0 = torch.zeros((n, n), dtype=torch.float32).pin_memory()
-    h_f = torch.ones((n, n), dtype=torch.float32).pin_memory()
-    h_out = torch.empty((n, n), dtype=torch.float32).pin_memory()
-    torch.cuda.synchronize()
-    dist.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    du0 = h_u0.to("cuda", non_blocking=True)
-    df = h_f.to("cuda", non_blocking=True)
-    blk = DeviceBlock(du0, df, consts, rank=rank, world=world, transport=transport)
-    r2 = run_block_loop(blk, cond)
-    h_out.copy_(r2.out, non_blocking=True)
-    e1.record()
-    torch.cuda.synchronize()
-    blk.close()
-    del du0, df
-    e2e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
-    dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
-    e2e_ms = float(e2e_ms.item())
-    peak, peak_kind = measured_peaks()
-    avg = kms / max(kn, 1)
-    alg = 12.0 * n * n
-    if rank != 0:
-        return None
-    return {
-        "metric": "stencil cell-updates/s", "value": cells / (ms / 1e3),
-        "unit": "cell-updates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f32", "data": "synthetic (rhs=1, u0=0)",
-        "config": {"workload": f"C4 Helmholtz/Jacobi ({n}*{world})x{n} fp32, MAX|delta|<1e-4",
-                   "rows_per_gpu": n, "cols": n, "iterations_per_step": iters,
-                   "final_reduce": res.final_reduce, "parallelism": f"row blocks x{world}, " + (
-                       "halo rows + partials stored by the sweep kernel into peer memory, "
-                       "stream waits on peer flags, device-side rank-ordered combine"
-                       if transport == "peer" else
-                       "NCCL halo rows + all-gather, device-side rank-ordered combine"),
-                   "transport": transport,
-                   "l2": "inputs 4.3 GB/array > 126 MB L2 (no flush needed)"},
-        "gpu_launches": launches,
-        "e2e": {"value": cells / (e2e_ms / 1e3), "unit": "cell-updates/s",
-                "h2d_bytes_per_step": 2 * 4 * n * n * world, "d2h_bytes_per_step": 4 * n * n * world,
-                "ms_per_step": e2e_ms},
-        "roofline": {"bound": "hbm", "achieved": alg / (avg / 1e3) / 1e9, "peak": peak,
-                     "unit": "GB/s", "frac": alg / (avg / 1e3) / 1e9 / peak, "traffic": None,
-                     "kernel": "helmholtz_sweep<float> (rank 0)", "avg_kernel_ms": avg,
-                     "peak_source": peak_kind},
-        "cpu_baseline": None,
-        "clocks": clk.summary(),
-    }
-
-
 # ---------------------------------------------------------------- any elemental
 
 

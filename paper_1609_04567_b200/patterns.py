@@ -11,7 +11,7 @@ runtime calls per element or per block.  Here an ElementalFn may carry a
 and its dtype-rounded constants; without one, its Python `point` function
 (and the plan's Combinator / Delta callables) are translated and compiled
 for the device at run time (jit.py).  Sum / max combinators and abs /
-square deltas are recognised (declared `kind`, or by probing the callable)
+square deltas are recognised (declared `kind`, or an exact AST match)
 and map onto the engine's reduce / delta enums.  Anything that cannot be
 compiled is rejected with DeviceUnsupported -- there is no host path.
 """
@@ -88,7 +88,7 @@ def _radius(f, k: Optional[int]) -> int:
 @dataclass(frozen=True)
 class Combinator:
     """Associative combiner with identity (patterns.py:85-107).  `kind`
-    ('sum' | 'max') is the device reduce; None means "probe fn"."""
+    ('sum' | 'max') is the device reduce; None means "look at fn's source"."""
 
     fn: Callable[[Any, Any], Any]
     identity: Any
@@ -108,7 +108,7 @@ class Combinator:
 @dataclass(frozen=True)
 class Delta:
     """Per-element change measure (patterns.py:110-122).  `kind`
-    ('abs' | 'square') is the device delta; None means "probe fn"."""
+    ('abs' | 'square') is the device delta; None means "look at fn's source"."""
 
     fn: Callable[[Any, Any], Any]
     on_arrays: Optional[Callable] = None
@@ -119,26 +119,125 @@ class Delta:
 
 
 # ---------------------------------------------------------------- recognition
+#
+# A user Combinator / Delta maps onto the engine's SUM / MAX reduce and
+# |new-old| / (new-old)**2 delta enums only when it says so (`kind`) or when
+# its source IS one of those expressions (checked on the AST, names resolved
+# to the builtins).  Anything else -- including functions that agree with a
+# built-in on many inputs but not on all -- is compiled as written (jit.py)
+# or, for the hand-written kernels, rejected with DeviceUnsupported.  No
+# classification by sampling: a near-miss would silently diverge from the
+# reference's fold of op.fn (patterns.py:85-122, loop.py:163-191).
 
-_PAIRS = ((1.5, 2.25), (2.25, 1.5), (-3.0, 0.5), (0.0, 7.0), (5.0, 3.0), (-2.0, -9.5))
 
+def _lambda_expr(fn):
+    """(param names, returned expression) of a one-expression function, or None."""
+    import ast
 
-def _probe(fn, expect) -> bool:
     try:
-        return all(fn(a, b) == expect(a, b) for a, b in _PAIRS)
+        from .jit import _func_node
+
+        node = _func_node(fn)
+    except Exception:
+        return None
+    a = node.args
+    if a.vararg or a.kwarg or a.kwonlyargs or a.defaults or len(a.args) != 2:
+        return None
+    if isinstance(node, ast.Lambda):
+        body = node.body
+    else:
+        stmts = [st for st in node.body
+                 if not (isinstance(st, ast.Expr) and isinstance(st.value, ast.Constant))]
+        if len(stmts) != 1 or not isinstance(stmts[0], ast.Return) or stmts[0].value is None:
+            return None
+        body = stmts[0].value
+    return [x.arg for x in a.args], body
+
+
+def _resolves_to(fn, name: str, target) -> bool:
+    """`name` inside fn means the builtin / module object `target`."""
+    import builtins
+    import inspect
+
+    try:
+        cv = inspect.getclosurevars(fn)
     except Exception:
         return False
+    for scope in (cv.nonlocals, cv.globals):
+        if name in scope:
+            return scope[name] is target
+    return getattr(builtins, name, None) is target
+
+
+def _is_name(node, name) -> bool:
+    import ast
+
+    return isinstance(node, ast.Name) and node.id == name
+
+
+def _is_diff(node, x, y) -> bool:
+    import ast
+
+    return (isinstance(node, ast.BinOp) and isinstance(node.op, ast.Sub)
+            and _is_name(node.left, x) and _is_name(node.right, y))
+
+
+def _ast_combinator(fn) -> Optional[str]:
+    import ast
+
+    le = _lambda_expr(fn)
+    if le is None:
+        return None
+    (a, b), e = le
+    if isinstance(e, ast.BinOp) and isinstance(e.op, ast.Add):  # a + b / b + a
+        if {getattr(e.left, "id", None), getattr(e.right, "id", None)} == {a, b} \
+                and isinstance(e.left, ast.Name) and isinstance(e.right, ast.Name):
+            return "sum"
+    if isinstance(e, ast.IfExp) and _is_name(e.body, a) and _is_name(e.orelse, b) \
+            and isinstance(e.test, ast.Compare) and len(e.test.ops) == 1:
+        t, op, r = e.test.left, e.test.ops[0], e.test.comparators[0]
+        # the reference's max: `a if b < a else b` (patterns.py:205-211), or `a if a > b else b`
+        if (isinstance(op, ast.Lt) and _is_name(t, b) and _is_name(r, a)) or \
+                (isinstance(op, ast.Gt) and _is_name(t, a) and _is_name(r, b)):
+            return "max"
+    if isinstance(e, ast.Call) and isinstance(e.func, ast.Name) and not e.keywords \
+            and len(e.args) == 2 and _is_name(e.args[0], a) and _is_name(e.args[1], b) \
+            and _resolves_to(fn, e.func.id, max):
+        return "max"
+    return None
+
+
+def _ast_delta(fn) -> Optional[str]:
+    import ast
+
+    le = _lambda_expr(fn)
+    if le is None:
+        return None
+    (n, o), e = le
+    diff = lambda d: _is_diff(d, n, o) or _is_diff(d, o, n)  # noqa: E731
+    if isinstance(e, ast.Call) and not e.keywords and len(e.args) == 1 and diff(e.args[0]):
+        f = e.func
+        if isinstance(f, ast.Name) and _resolves_to(fn, f.id, abs):
+            return "abs"
+    if isinstance(e, ast.BinOp) and isinstance(e.op, ast.Pow) and diff(e.left) \
+            and isinstance(e.right, ast.Constant) and type(e.right.value) is int \
+            and e.right.value == 2:
+        return "square"
+    return None
 
 
 def combinator_kind(op: Combinator) -> str:
-    """'sum' or 'max' for the device reduce, else DeviceUnsupported."""
+    """'sum' or 'max' for the device reduce, else DeviceUnsupported (the
+    JIT then compiles op.fn itself)."""
     if getattr(op, "kind", None) is not None:
         return op.kind
-    if _probe(op.fn, lambda a, b: a + b):
-        return "sum"
-    if _probe(op.fn, lambda a, b: a if b < a else b):
-        return "max"
-    raise DeviceUnsupported("combinator is neither a sum nor a max; no device reduce for it")
+    import operator
+
+    k = "sum" if op.fn is operator.add else "max" if op.fn is max else _ast_combinator(op.fn)
+    if k is None:
+        raise DeviceUnsupported("combinator is not exactly `a + b` or `a if b < a else b`; "
+                                "no built-in device reduce for it")
+    return k
 
 
 def delta_kind(d: Optional[Delta]) -> str:
@@ -147,11 +246,11 @@ def delta_kind(d: Optional[Delta]) -> str:
         return "none"
     if getattr(d, "kind", None) is not None:
         return d.kind
-    if _probe(d.fn, lambda n, o: abs(n - o)):
-        return "abs"
-    if _probe(d.fn, lambda n, o: (n - o) ** 2):
-        return "square"
-    raise DeviceUnsupported("delta is neither |new-old| nor (new-old)**2; no device delta for it")
+    k = _ast_delta(d.fn)
+    if k is None:
+        raise DeviceUnsupported("delta is not exactly `abs(new - old)` or `(new - old) ** 2`; "
+                                "no built-in device delta for it")
+    return k
 
 
 def abs_change() -> Delta:

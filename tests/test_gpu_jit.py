@@ -251,3 +251,60 @@ def test_rank1_multi_tile_matches_oracle(n, P):
     assert rep.iterations == it == 4
     assert np.array_equal(out.to_array(), np.asarray(ref))
     assert float(rep.final_reduce) == val
+
+
+def _near_sum(a, b):
+    return a + b if b < 50 else a  # == a + b on small partials only
+
+
+def _near_abs(n, o):
+    return abs(n - o) if abs(n - o) < 100 else 0.0
+
+
+def test_near_miss_combinator_and_delta_compile_as_written():
+    """A combinator / delta that agree with SUM / |new-old| on small inputs
+    but not everywhere: before round 2 they were classified by sampling and
+    ran as the built-in reduce; now they are compiled as written, and the
+    device matches the reference's sequential fold of op.fn
+    (loop.py:163-191, partition.py:642-646) exactly."""
+    def pt(nb, env):
+        s = 0.0
+        for v in nb.values():
+            s += v
+        return s * 0.25 + 7.0
+
+    rng = np.random.default_rng(5)
+    a = rng.random((67, 301)) * 200.0
+    for P in (1, 3):
+        op = sk.Combinator(_near_sum, 0.0)
+        delta = sk.Delta(_near_abs)
+        out, rep = sk.parallel_loop("1:n" if P > 1 else "1:1", P, 1, sk.ElementalFn(pt, 1), op,
+                                    sk.stop_after(4), as_grid(a), delta=delta)
+        rows, it, val, ex = sequential_loop(pt, 1, _near_sum, 0.0, lambda v, i, s: i >= 4,
+                                            a.tolist(), delta=_near_abs, partitions=P)
+        assert rep.iterations == it == 4
+        assert rep.final_reduce == val, (P, rep.final_reduce, val)
+        assert np.array_equal(out.to_array(), np.asarray(rows))
+        # the plain SUM of |delta| differs: the near-miss really is exercised
+        plain = sk.parallel_loop("1:n" if P > 1 else "1:1", P, 1, sk.ElementalFn(pt, 1),
+                                 sk.sum_combinator(0.0), sk.stop_after(4), as_grid(a),
+                                 delta=sk.abs_change())[1].final_reduce
+        assert plain != val
+
+
+def test_builtin_kernel_rejects_unrecognised_reduce():
+    """The hand-written kernels only have the SUM / MAX reduce and abs /
+    square deltas: anything else is refused loudly, never approximated."""
+    from paper_1609_04567_b200.apps import HelmholtzConfig, helmholtz_kernel
+
+    rhs = np.ones((40, 40), np.float32)
+    with pytest.raises(sk.DeviceUnsupported):
+        sk.parallel_loop("1:1", 1, 1, helmholtz_kernel(HelmholtzConfig(40, 40)),
+                         sk.Combinator(_near_sum, 0.0), sk.Condition.below(1e-4),
+                         sk.Grid(rhs.shape, np.zeros_like(rhs)), env=sk.Grid(rhs.shape, rhs),
+                         delta=sk.abs_change())
+    with pytest.raises(sk.DeviceUnsupported):
+        sk.parallel_loop("1:1", 1, 1, helmholtz_kernel(HelmholtzConfig(40, 40)),
+                         sk.max_combinator(0.0), sk.Condition.below(1e-4),
+                         sk.Grid(rhs.shape, np.zeros_like(rhs)), env=sk.Grid(rhs.shape, rhs),
+                         delta=sk.Delta(_near_abs))

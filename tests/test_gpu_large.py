@@ -99,3 +99,27 @@ def test_c3_denoise_4096_full_size():
     assert sha(a) == m["sha"]
     assert sha(np.clip(np.rint(a), 0, 255).astype(np.uint8)) == m["sha_u8"]
     assert rep.final_reduce == pytest.approx(m["final_reduce"], rel=1e-12)
+
+
+def test_c2_sobel_frames_batched_2048(golden_large):
+    """The C2 bench kernel itself: `sobel_frames` (the batched, paired
+    full-width-strip instantiation of sobel_sweep) over a stack of 2048^2
+    frames with a 16-byte pitch, each frame against the reference's SHA-256
+    and pixel sum (apps/sobel.py:47-66, :73-74)."""
+    import torch
+
+    from paper_1609_04567_b200.apps import sobel_frames
+
+    seeds = (0, 42, 43, 43, 0, 42, 42, 0)
+    imgs = {s: np.random.default_rng(s).integers(0, 256, (2048, 2048)).astype(np.uint8)
+            for s in set(seeds)}
+    frames = torch.from_numpy(np.stack([imgs[s] for s in seeds])).cuda()
+    for rep in range(2):  # second call reuses the per-stream chunk counters
+        out, sums = sobel_frames(frames)
+        torch.cuda.synchronize()
+        o = out.cpu().numpy()
+        s = sums.cpu().numpy()
+        for i, seed in enumerate(seeds):
+            m = golden_large.meta[f"C2_sobel_rng{seed}_2048"]
+            assert int(s[i]) == m["final_reduce"], (rep, i, seed)
+            assert sha(o[i]) == m["sha"], (rep, i, seed)

@@ -110,6 +110,60 @@ def test_combinator_and_delta_recognition():
         delta_kind(sk.Delta(lambda n, o: n - o))
 
 
+def _shadow_abs(x):
+    return 0.0
+
+
+@pytest.mark.parametrize("fn", [
+    lambda a, b: a + b if b < 50 else a,       # agrees with a + b on small values only
+    lambda a, b: min(a + b, 100.0),
+    lambda a, b: a + b + 0.0 * a,
+    lambda a, b: a - b,
+    lambda a, b: b if b < a else a,            # min, not max
+    lambda a, b: a if b <= a else b,
+])
+def test_near_miss_combinators_are_not_builtin_reduces(fn):
+    """no classification by sampling -- a function that
+    matches SUM / MAX on probe pairs but not everywhere must not run as the
+    built-in reduce (the JIT compiles it instead)."""
+    with pytest.raises(DeviceUnsupported):
+        combinator_kind(sk.Combinator(fn, 0.0))
+
+
+@pytest.mark.parametrize("fn", [
+    lambda n, o: abs(n - o) if abs(n - o) < 100 else 0.0,
+    lambda n, o: min(abs(n - o), 10.0),
+    lambda n, o: (n - o) ** 3,
+    lambda n, o: abs(n + o),
+    lambda n, o: _shadow_abs(n - o),
+])
+def test_near_miss_deltas_are_not_builtin_deltas(fn):
+    with pytest.raises(DeviceUnsupported):
+        delta_kind(sk.Delta(fn))
+
+
+def test_exact_forms_and_shadowed_names():
+    import operator
+
+    assert combinator_kind(sk.Combinator(operator.add, 0)) == "sum"
+    assert combinator_kind(sk.Combinator(lambda x, y: y + x, 0)) == "sum"
+    assert combinator_kind(sk.Combinator(lambda a, b: a if a > b else b, 0.0)) == "max"
+
+    def mx(a, b):
+        """docstring is fine"""
+        return a if b < a else b
+
+    assert combinator_kind(sk.Combinator(mx, 0.0)) == "max"
+    assert delta_kind(sk.Delta(lambda new, old: abs(old - new))) == "abs"
+    assert delta_kind(sk.Delta(lambda new, old: (old - new) ** 2)) == "square"
+
+
+def test_shadowed_abs_is_not_the_builtin():
+    abs = _shadow_abs  # noqa: A001 -- a local `abs` that is not the builtin
+    with pytest.raises(DeviceUnsupported):
+        delta_kind(sk.Delta(lambda n, o: abs(n - o)))
+
+
 @pytest.mark.parametrize("cond", [sk.Condition.below(1e-4), sk.Condition.rms_below(1e-6, 256),
                                   sk.Condition.mean_below(0.02, 1234), sk.stop_after(7)])
 def test_device_conditions_equal_their_python_predicates(cond):
