@@ -342,6 +342,9 @@ def launch_command(n: int, argv, port: int):
     """The torchrun command `bench.py --gpus N` re-executes itself under when
     it is started without WORLD_SIZE (one rank per GPU, rendezvous on
     127.0.0.1)."""
+    # torchrun's own parser takes abbreviations: `--n` would read as one of
+    # its options, so the grid size travels as --size
+    argv = ["--size" + a[3:] if a == "--n" or a.startswith("--n=") else a for a in argv]
     return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
             f"--nproc-per-node={n}", "--master-addr=127.0.0.1", f"--master-port={port}",
             os.path.abspath(__file__), *argv]
@@ -574,7 +577,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=32768)
+    ap.add_argument("--n", "--size", dest="n", type=int, default=32768)
     ap.add_argument("--transport", default="peer", choices=["peer", "collective"],
                     help="C4 with N>1: halo rows + partials by peer stores from the sweep "
                          "kernel (default) or by NCCL send/recv + all-gather")

@@ -282,17 +282,19 @@ def salt_pepper(img: Grid, level: float, seed: int = 42):
 
 
 class _RestoreBatcher:
-    """Coalesces the restore farm's frames into device batches.
+    """Coalesces the restore farm's frames on ONE GPU into device batches.
 
-    Every farm replica still handles one frame at a time (the reference's
-    ordered farm, apps/denoise.py:338-356); what the replicas hand in
+    Every farm lane still hands in one frame at a time (the reference's
+    ordered farm, apps/denoise.py:338-356); what the lanes of one GPU hand in
     concurrently is restored together by `restore_frames` -- one persistent
     launch in which every frame runs its own loop to its own stop, each
     bit-identical to restoring it alone.  A batch is closed when it is full,
-    or when no further frame arrives within `linger_s`."""
+    or when no further frame arrives within `linger_s`.  The batch waits for
+    each submitting lane's stream (its upload) and the lane waits for the
+    batch's completion event, so no host synchronisation sits between them."""
 
     def __init__(self, cfg: RestoreConfig, max_batch: int, linger_s: float = 2e-4,
-                 detect: bool = False):
+                 detect: bool = False, device: Optional[int] = None):
         import torch
 
         self.cfg = cfg
@@ -302,14 +304,16 @@ class _RestoreBatcher:
         self.pending = []
         self.closed = False
         self.detect = detect  # run the detector on each batch first (masks not given)
-        self.device = torch.cuda.current_device()
-        self.stream = torch.cuda.Stream()
+        self.device = torch.cuda.current_device() if device is None else device
+        self.stream = torch.cuda.Stream(device=self.device)
         self.thread = threading.Thread(target=self._run, daemon=True)
         self.thread.start()
 
-    def submit(self, frame, mask):
-        """frame / mask: [H, W] uint8 CUDA tensors; returns (out, report)."""
-        slot = {"done": threading.Event()}
+    def submit(self, frame, mask, after=None):
+        """frame / mask: [H, W] uint8 tensors on this batcher's GPU, ready
+        after the event `after` (None: already complete); returns
+        (out, report, done_event)."""
+        slot = {"done": threading.Event(), "after": after}
         with self.cv:
             if self.closed:
                 raise RuntimeError("restore batcher is closed")
@@ -341,22 +345,27 @@ class _RestoreBatcher:
     def _run(self):
         import torch
 
-        torch.cuda.set_device(self.device)  # the thread restores on its creator's GPU
+        torch.cuda.set_device(self.device)
         while True:
             batch = self._take()
             if batch is None:
                 return
             try:
                 with torch.cuda.stream(self.stream):
+                    for _f, _m, slot in batch:
+                        if slot["after"] is not None:
+                            self.stream.wait_event(slot["after"])
                     frames = torch.stack([b[0] for b in batch])
                     if self.detect:
                         masks, _ = amf_frames(frames, self.cfg.amf_wmax, stream=self.stream)
                     else:
                         masks = torch.stack([b[1] for b in batch])
                     outs, reps = restore_frames(frames, masks, self.cfg, stream=self.stream)
+                    done = torch.cuda.Event()
+                    done.record(self.stream)
                 for (_f, _m, slot), o, r in zip(batch, outs, reps):
                     g = Grid.from_tensor(o, logical_dtype=np.float64)
-                    slot["result"] = (g, r)
+                    slot["result"] = (g, r, done)
                     slot["done"].set()
             except Exception as e:  # the batch's frames all fail with it
                 for _f, _m, slot in batch:
@@ -373,92 +382,91 @@ class _RestoreBatcher:
 def video_restore_pipeline(frames: Iterable, *, width: int = 1, partitions: int = 1,
                            mode=DeploymentMode.ONE_TO_ONE, cfg: Optional[RestoreConfig] = None,
                            writer: Optional[Callable] = None, loader: Optional[Callable] = None,
-                           mask_writer: Optional[Callable] = None) -> StreamReport:
+                           mask_writer: Optional[Callable] = None,
+                           devices: Optional[list] = None) -> StreamReport:
     """read -> detect -> ordered_farm(restore, width) -> write
-    (apps/denoise.py:307-368).
+    (apps/denoise.py:307-368), over one GPU or several.
 
-    1:1 deployment: the detect stage uploads each frame once (uint8) and
-    runs the detector on the device; the `width` restore replicas hand their
-    frames to one batcher that restores whatever is in flight together in a
-    single persistent launch (a device-side farm of loops, restore_frames).
-    1:n deployment: each replica runs restore_regularize over `partitions`
-    row blocks of its frame."""
+    `devices` (default: the caller's GPU): the restore farm's `width` lanes
+    are spread round-robin over these GPUs (streams.ordered_farm), each lane
+    with its own CUDA stream; frames keep stream order end to end.
+
+    1:1 deployment: each lane uploads its frame (uint8) on its own stream and
+    hands it to its GPU's batcher, which detects and restores whatever that
+    GPU's lanes have in flight together in a single persistent launch (a
+    device-side farm of loops, restore_frames).  With a `mask_writer` the
+    detector runs per frame in the detect stage instead, so masks are written
+    in stream order.  1:n deployment: each lane runs restore_regularize over
+    `partitions` row blocks of its frame on its GPU."""
     import torch
 
     from ..partition import _u8_from
+    from ..streams import current_lane
 
     mode = DeploymentMode.parse(mode)
     if mode is DeploymentMode.ONE_TO_N and partitions < 2:
         raise GridError("1:n deployment needs at least 2 partitions")
     eff = partitions if mode is DeploymentMode.ONE_TO_N else 1
     cfg = cfg or RestoreConfig()
-
-    read = Stage(loader or (lambda f: f), name="read")
-    detect_group = WorkerGroup(1)
+    N.require_cuda()
+    if devices is None:
+        devices = [torch.cuda.current_device()]
+    devices = [int(getattr(d, "index", d)) for d in devices]
     batched = eff == 1
-    # without a mask writer the detector runs inside the restore batches (one
-    # AMF launch per batch, on the batcher's stream); with one, per frame in
-    # the detect stage so the masks are written in stream order
     fused_detect = batched and mask_writer is None
-    batcher = _RestoreBatcher(cfg, width, detect=fused_detect) if batched else None
+    per_dev = -(-width // len(devices))
+    batchers = ({d: _RestoreBatcher(cfg, per_dev, detect=fused_detect, device=d)
+                 for d in dict.fromkeys(devices)} if batched else {})
 
     def detect_fn(img: Grid):
-        # one batched-detector launch on the stage's stream (no run object:
-        # detection is a single stencil pass), then hand the frame and its
-        # mask to the restore farm
         if img.ndim != 2:
             raise GridError("detection expects a 2D image")
+        if fused_detect:
+            return img, None  # the restore lane uploads it; its batcher detects
+        lane = current_lane()
         if not batched:
-            mask = _detect_frame(img, cfg.amf_wmax, detect_group.stream)
+            mask = _detect_frame(img, cfg.amf_wmax, lane.stream)
             if mask_writer is not None:
                 mask_writer(mask)
             return img, mask
-        if fused_detect:
-            # the detector runs inside the restore batches; the upload happens
-            # in the restore replicas (in parallel) rather than in this stage
-            return img, None
-        st = detect_group.stream
-        dev = torch.device("cuda", torch.cuda.current_device())
-        with torch.cuda.stream(st):
-            t = _u8_from(img, "amf", 0, 255, dev)
-            masks, _ = amf_frames(t.reshape(1, *img.dims), cfg.amf_wmax, stream=st)
-        st.synchronize()
+        dev = torch.device("cuda", lane.device)
+        t = _u8_from(img, "amf", 0, 255, dev)
+        masks, _ = amf_frames(t.reshape(1, *img.dims), cfg.amf_wmax, stream=lane.stream)
         if mask_writer is not None:
+            lane.stream.synchronize()
             mg = Grid.from_tensor(masks[0], logical_dtype=np.int64)
             mg.value_range = (0, 1)
             mask_writer(mg)
         return t, masks[0]
 
-    detect = Stage(detect_fn, name="detect")
-
     def make_restorer():
+        lane = current_lane()
+        dev = torch.device("cuda", lane.device)
         grp = None if batched else WorkerGroup(eff)
-        streams = []
-
-        def upload_stream():  # one per replica, created on first use
-            if not streams:
-                streams.append(torch.cuda.Stream())
-            return streams[0]
 
         class _Restorer:
             def __call__(self, pair):
                 img, mask = pair
                 if batched:
-                    if isinstance(img, Grid):  # fused detect: upload here
-                        if img.ndim != 2:
-                            raise GridError("detection expects a 2D image")
-                        dev = torch.device("cuda", torch.cuda.current_device())
-                        with torch.cuda.stream(upload_stream()):
-                            img = _u8_from(img, "amf", 0, 255, dev)
-                            torch.cuda.current_stream().synchronize()
-                    out, _rep = batcher.submit(img, mask)
+                    # on the lane's stream (current): the frame's upload, and
+                    # the mask's move when detect ran on another GPU
+                    if isinstance(img, Grid):
+                        img = _u8_from(img, "amf", 0, 255, dev)
+                    elif img.device != dev:
+                        img = img.to(dev, non_blocking=True)
+                    if mask is not None and mask.device != dev:
+                        mask = mask.to(dev, non_blocking=True)
+                    up = torch.cuda.Event()
+                    up.record(lane.stream)
+                    out, _rep, done = batchers[lane.device].submit(img, mask, after=up)
+                    lane.stream.wait_event(done)
                 else:
                     out, _rep = restore_regularize(
                         img, mask, cfg, partitions=eff,
                         mode=mode if eff > 1 else DeploymentMode.ONE_TO_ONE, group=grp)
                 if writer is not None:
-                    # read the frame back here, in parallel across replicas;
-                    # the ordered writer's to_array() then takes it over
+                    # read the frame back here, in parallel across lanes; the
+                    # ordered writer's to_array() then takes it over
                     out.prefetch_host()
                 return out
 
@@ -468,6 +476,8 @@ def video_restore_pipeline(frames: Iterable, *, width: int = 1, partitions: int 
 
         return _Restorer()
 
+    read = Stage(loader or (lambda f: f), name="read")
+    detect = Stage(detect_fn, name="detect")
     restore = Stage(factory=make_restorer, name="restore")
     if writer is None:
         write = Stage(lambda g: g, name="write")
@@ -477,10 +487,9 @@ def video_restore_pipeline(frames: Iterable, *, width: int = 1, partitions: int 
             return g
 
         write = Stage(write_fn, name="write")
-    top = pipeline(read, detect, ordered_farm(restore, width), write)
+    top = pipeline(read, detect, ordered_farm(restore, width, devices=devices), write)
     try:
         return run_stream(frames, top, sink=lambda _item: None)
     finally:
-        detect_group.close()
-        if batcher is not None:
-            batcher.close()
+        for b in batchers.values():
+            b.close()

@@ -28,6 +28,13 @@ def test_launch_command_is_one_rank_per_gpu():
     assert "--master-addr=127.0.0.1" in cmd and "--master-port=29555" in cmd
     assert cmd[-4:] == ["--gpus", "8", "--steps", "3"]
     assert cmd[-5].endswith("bench.py")
+    # torchrun's own parser must hand every bench flag to the script
+    from torch.distributed.run import get_args_parser
+
+    cmd = bench.launch_command(2, ["--gpus", "2", "--n", "2048", "--steps", "2"], 29555)
+    ns = get_args_parser().parse_args(cmd[3:])
+    assert ns.nproc_per_node == "2" and ns.training_script.endswith("bench.py")
+    assert ns.training_script_args == ["--gpus", "2", "--size", "2048", "--steps", "2"]
 
 
 def test_gpus_must_match_world_size():
