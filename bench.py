@@ -506,7 +506,7 @@ def run_distributed(args, world, rank, local):
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (rhs=1, u0=0)",
         "config": {"workload": (f"C4 Helmholtz/Jacobi {n}x{n} fp32 split over {world} ranks"
                                 if strong else
-                                f"C4 Helmholtz/Jacobi ({n}*{world})x{n} fp32 (32768^2 per GPU)")
+                                f"C4 Helmholtz/Jacobi ({n}*{world})x{n} fp32 ({n}^2 per GPU)")
                    + ", MAX|delta|<1e-4",
                    "rows_per_rank": rows, "cols": n, "iterations_per_step": iters,
                    "final_reduce": final, "parallelism": f"row blocks x{world}, " + (

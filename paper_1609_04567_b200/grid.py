@@ -138,6 +138,10 @@ class Grid:
         a = np.asarray(arr)
         if a.ndim not in (1, 2):
             raise GridError(f"array rank must be 1 or 2, got {a.ndim}")
+        if a.dtype.kind == "f" and a.dtype != np.float64:
+            # the reference stores arr.tolist() (grid.py:100-107): Python
+            # floats, so every computation on the grid is fp64
+            return cls(a.shape, a.astype(np.float64))
         return cls(a.shape, a.copy())
 
     @classmethod
@@ -285,7 +289,11 @@ class Grid:
             if self._src != "list":
                 self._t = t
         if device is not None and t.device != torch.device(device):
-            t = t.to(device, non_blocking=False)
+            dev = torch.device(device)
+            if t.device.type == "cpu" and dev.type == "cuda" and not t.is_pinned():
+                t = _to_device(t.numpy(), dev)  # pageable host memory: staged
+            else:
+                t = t.to(device, non_blocking=False)
             if self._src != "list":
                 self._t = t
         if dtype is not None and t.dtype != dtype:
@@ -331,67 +339,148 @@ class Grid:
         self.value_range = None
 
 
-_PIN_LOCK = None
-_PIN_POOL: dict = {}
-
-
 _COPY_POOL = None
+_STAGE_LOCK = None
+_STAGE_FREE: list = []
+_CHUNK = 32 << 20  # bytes per pinned staging chunk
+_NSTAGE = 3        # chunks in flight per transfer
 
 
-def _par_copy(src: np.ndarray) -> np.ndarray:
-    """Fresh copy of a large host array with 8 threads: the cost is mostly
-    first-touch page faults of the new memory, which parallelise (numpy
-    releases the GIL in copyto)."""
+def _copy_pool():
     global _COPY_POOL
-    out = np.empty_like(src)
-    if src.nbytes < (4 << 20):
-        np.copyto(out, src)
-        return out
     if _COPY_POOL is None:
         from concurrent.futures import ThreadPoolExecutor
 
         _COPY_POOL = ThreadPoolExecutor(8, thread_name_prefix="sk-hostcopy")
-    n, k = src.size, 8
+    return _COPY_POOL
+
+
+def _host_copy(dst: np.ndarray, src: np.ndarray) -> None:
+    """dst[:] = src (1-D uint8 views) with 8 threads: large copies are bound
+    by first-touch page faults of fresh memory, which parallelise (numpy
+    releases the GIL in copyto)."""
+    n = src.size
+    if n < (4 << 20):
+        np.copyto(dst, src)
+        return
+    k = 8
     step = -(-n // k)
-    a, b = src.reshape(-1), out.reshape(-1)
-    list(_COPY_POOL.map(lambda i: np.copyto(b[i * step:(i + 1) * step], a[i * step:(i + 1) * step]),
-                        range(k)))
+    list(_copy_pool().map(
+        lambda i: np.copyto(dst[i * step:(i + 1) * step], src[i * step:(i + 1) * step]),
+        range(k)))
+
+
+def _par_copy(src: np.ndarray) -> np.ndarray:
+    out = np.empty_like(src)
+    _host_copy(out.reshape(-1).view(np.uint8), src.reshape(-1).view(np.uint8))
+    return out
+
+
+class _Stage:
+    """_NSTAGE pinned host chunks + one event each: a transfer of any size
+    streams through them, the host copy of chunk k overlapping the DMA of
+    chunk k+1 (pageable <-> pinned <-> device)."""
+
+    def __init__(self):
+        torch = _torch()
+        self.bufs = [torch.empty(_CHUNK, dtype=torch.uint8, pin_memory=True)
+                     for _ in range(_NSTAGE)]
+        self.views = [b.numpy() for b in self.bufs]
+        self.events = [None] * _NSTAGE
+
+
+def _stage_get() -> _Stage:
+    import threading
+
+    global _STAGE_LOCK
+    if _STAGE_LOCK is None:
+        _STAGE_LOCK = threading.Lock()
+    with _STAGE_LOCK:
+        if _STAGE_FREE:
+            return _STAGE_FREE.pop()
+    return _Stage()
+
+
+def _stage_put(st: _Stage) -> None:
+    with _STAGE_LOCK:
+        _STAGE_FREE.append(st)
+
+
+def _to_device(a: np.ndarray, device):
+    """Host array -> new device tensor.  Large arrays stream through pinned
+    chunks on the current stream (pageable memory crosses PCIe at a fraction
+    of the pinned rate); the call returns once the data is on the device."""
+    torch = _torch()
+    a = np.ascontiguousarray(a)
+    if a.nbytes < (8 << 20):
+        return torch.from_numpy(a).to(device)
+    out = torch.empty(a.shape, dtype=torch.from_numpy(a[:0]).dtype, device=device)
+    src = a.reshape(-1).view(np.uint8)
+    dst = out.view(-1).view(torch.uint8)
+    stream = torch.cuda.current_stream(out.device)
+    st = _stage_get()
+    try:
+        for k, off in enumerate(range(0, src.size, _CHUNK)):
+            j = k % _NSTAGE
+            m = min(_CHUNK, src.size - off)
+            if st.events[j] is not None:
+                st.events[j].synchronize()  # chunk k - _NSTAGE has left this buffer
+            _host_copy(st.views[j][:m], src[off:off + m])
+            dst[off:off + m].copy_(st.bufs[j][:m], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+            st.events[j] = ev
+        for ev in st.events:
+            if ev is not None:
+                ev.synchronize()
+    finally:
+        st.events = [None] * _NSTAGE
+        _stage_put(st)
     return out
 
 
 def _to_host(t) -> np.ndarray:
-    """Device tensor -> fresh numpy array through a pooled pinned staging
-    buffer (pageable copies run at a fraction of PCIe bandwidth)."""
-    import threading
-
+    """Device tensor -> fresh numpy array.  Large tensors stream through
+    pinned chunks: the DMA of chunk k+1.. runs while chunk k is copied out
+    into the fresh array."""
     torch = _torch()
     if not t.is_cuda or t.numel() * t.element_size() < (1 << 20):
         return t.detach().cpu().numpy()
     if os.environ.get("SK_D2H", "pinned") == "direct":
-        # the driver's own staged copy straight into the fresh array (0.9 ms
-        # per 16.6 MB frame alone, but slower than pinned staging when many
-        # threads copy at once)
+        # the driver's own staged copy straight into the fresh array
         out = np.empty(tuple(t.shape), dtype=_numpy_dtype_of(t.dtype))
         src = t.detach() if t.is_contiguous() else t.detach().contiguous()
         torch.from_numpy(out).copy_(src)
         return out
-    global _PIN_LOCK
-    if _PIN_LOCK is None:
-        _PIN_LOCK = threading.Lock()
-    key = (t.dtype, t.numel())
-    with _PIN_LOCK:
-        free = _PIN_POOL.setdefault(key, [])
-        buf = free.pop() if free else None
-    if buf is None:
-        buf = torch.empty(t.numel(), dtype=t.dtype, pin_memory=True)
+    out = np.empty(tuple(t.shape), dtype=_numpy_dtype_of(t.dtype))
+    src = (t.detach() if t.is_contiguous() else t.detach().contiguous()).reshape(-1)
+    src = src.view(torch.uint8)
+    dst = out.reshape(-1).view(np.uint8)
+    stream = torch.cuda.current_stream(t.device)
+    st = _stage_get()
+    offs = list(range(0, dst.size, _CHUNK))
     try:
-        src = t.detach().reshape(-1) if t.is_contiguous() else t.detach().contiguous().reshape(-1)
-        buf.copy_(src, non_blocking=True)
-        torch.cuda.current_stream(t.device).synchronize()
-        return _par_copy(buf.numpy())
+        def issue(k):
+            j = k % _NSTAGE
+            m = min(_CHUNK, dst.size - offs[k])
+            st.bufs[j][:m].copy_(src[offs[k]:offs[k] + m], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+            st.events[j] = ev
+
+        for k in range(min(_NSTAGE, len(offs))):
+            issue(k)
+        for k in range(len(offs)):
+            j = k % _NSTAGE
+            m = min(_CHUNK, dst.size - offs[k])
+            st.events[j].synchronize()
+            _host_copy(dst[offs[k]:offs[k] + m], st.views[j][:m])
+            if k + _NSTAGE < len(offs):
+                issue(k + _NSTAGE)
     finally:
-        with _PIN_LOCK:
-            _PIN_POOL[key].append(buf)
+        st.events = [None] * _NSTAGE
+        _stage_put(st)
+    return out
 
 
 def _numpy_dtype_of(tdtype):

@@ -754,7 +754,7 @@ class DeviceExecutor(Executor):
             out = out.reshape(run.dims)
         led = model_ledger(run.dims, run.P, run.plan.k, it)
         g = Grid.from_tensor(out, logical_dtype=run.out_dtype)
-        g.value_range = _OUT_RANGE.get(getattr(run.plan.fn.device, "name", None))
+        g.value_range = _OUT_RANGE.get(getattr(getattr(run.plan.fn, "device", None), "name", None))
         return g, led
 
     def abort(self, run: _DevRun) -> None:

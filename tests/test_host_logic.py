@@ -252,3 +252,18 @@ def test_adapts_reference_plan_objects():
     plan, grid = _adapt(ref_plan, ref_grid)
     assert plan.fn is ours and isinstance(grid, sk.Grid) and isinstance(plan.env, sk.Grid)
     assert combinator_kind(plan.op) == "sum"
+
+
+def test_from_array_widens_floats_like_the_reference():
+    """the reference's Grid.from_array stores
+    arr.tolist() -- Python floats -- so a float32 array computes in fp64;
+    Grid(dims, float32 elements) and from_tensor keep float32."""
+    import torch
+
+    a = np.arange(6, dtype=np.float32).reshape(2, 3) / 3
+    g = sk.Grid.from_array(a)
+    assert g.storage_dtype() == np.float64
+    assert np.array_equal(g.to_array(), a.astype(np.float64))
+    assert sk.Grid(a.shape, a).storage_dtype() == np.float32
+    assert sk.Grid.from_tensor(torch.from_numpy(a)).storage_dtype() == np.float32
+    assert sk.Grid.from_array(np.arange(4, dtype=np.uint8)).storage_dtype() == np.uint8
