@@ -38,7 +38,10 @@ def _worker(rank, world, port, name, q):
         lo, hi = _split_ranges(g.shape[0], world)[rank]
 
         def blk(a):
-            return sk.Grid.from_array(np.ascontiguousarray(a[lo:hi]))
+            # Grid(dims, array) keeps the element dtype (the fixture's f32 grid
+            # was built from np.float32 values); from_array widens like the reference
+            b = np.ascontiguousarray(a[lo:hi])
+            return sk.Grid(b.shape, b)
 
         benv = None if env is None else (tuple(blk(e) for e in env) if isinstance(env, tuple)
                                          else blk(env))
