@@ -25,6 +25,7 @@ SOURCES = [
     "sk_helmholtz.cu",
     "sk_verify.cu",
     "sk_u8stencil.cu",
+    "sk_sobel_tma.cu",
     "sk_amf.cu",
     "sk_restore.cu",
     "sk_dispatch.cu",

@@ -71,6 +71,13 @@ cudaError_t launch_kernel(void (*fn)(A), int grid, int block, const A& args, cud
   return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(fn), grid, block, params, 0, s);
 }
 
+// Batched Sobel through the TMA row ring (sk_sobel_tma.cu); SK_ERR_UNSUPPORTED
+// when the geometry does not fit it (rows wider than 2048 bytes, unaligned
+// pitches), in which case sobel_frames runs the generic batched sweep.
+int sobel_frames_tma(const uint8_t* in, long long in_pitch, long long in_fs, uint8_t* out,
+                     long long out_pitch, long long out_fs, int frames, long long rows,
+                     long long cols, long long* sums, cudaStream_t s);
+
 // mismatches of div_const vs IEEE division over all safe fp32 numerators
 // (cached per divisor; -1 if the check could not run)
 long long verify_div_f32(float b, cudaStream_t s);

@@ -1,0 +1,580 @@
+// Batched Sobel (stream mode) with the input rows streamed into shared memory
+// by the Tensor Memory Accelerator.
+//
+// Reference: Sobel block kernel apps/sobel.py:47-66 (point :33-44, border rule
+// :53-56, magnitude rounding :60-64); per-frame pixel sum apps/sobel.py:73-74.
+//
+// HBM-bound: 2 B/pixel (read 1 + write 1).  The arithmetic is the paired-fp32
+// form of sk_u8stencil.cu's sobel_sweep (exact integer features under a 2^15
+// bias, sqrt.approx + a magic add for rint, one u16x2 clip per two pixels);
+// what changes is how bytes reach the warps:
+//
+//  * A CTA owns a contiguous run of OUTPUT rows of the batch (frame-major, so
+//    a run covers parts of 1-3 frames); every CTA gets the same number of
+//    rows, so there is no work counter and no tail imbalance beyond one row.
+//  * A producer warp (one elected lane) streams the run's input rows -- each
+//    frame segment [a, b) needs rows a-1 .. b -- into a ring of STAGES stages
+//    of SR full-width rows with cp.async.bulk.tensor (a 4-D tensor map
+//    {IB, W/IB, rows, frames} whose box is SR whole rows, so a stage lands as
+//    SR dense rows of W bytes; rows outside the frame are zero-filled by the
+//    TMA unit and only feed border pixels).  Completion is an mbarrier
+//    transaction count; the consumer warps release a stage through a second
+//    mbarrier.  No consumer lane issues a copy or computes a global address
+//    for its input.
+//  * Consumer warp w owns columns 256w .. 256w+255 of every row; lane j owns
+//    the 8 contiguous pixels 8j .. 8j+7, held as four pairs (p_t, p_t+4), so
+//    a row costs one 8-byte shared load plus two neighbour bytes, and the
+//    result is one 8-byte store.
+//  * Border pixels follow the reference's centre-substitution rule without a
+//    global re-read: image rows 0 / rows-1 come out of the main path exactly
+//    (rows outside the frame arrive as zeros and S of the missing row is
+//    replaced by 4x the centre row), and columns 0 / cols-1 are recomputed
+//    per stage from the ring by the producer warp once the consumers release
+//    the stage (the buffer before it is refilled only after that, so the
+//    rows above a stage are still resident); consumer warps do identical
+//    work, so none of them drags the ring.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdint>
+#include <cstdlib>
+#include <mutex>
+
+#include "sk_internal.h"
+
+namespace sk {
+
+
+namespace sobel_tma {
+
+constexpr int NW = 8;  // consumer warps: 8 x 256 columns = rows up to 2048 bytes
+constexpr int BLOCK = (NW + 1) * 32;
+constexpr int FRONT = 128;  // guard before the ring (TMA destinations are 128-byte aligned)
+constexpr int BACK = 256;   // guard after it (lanes past the row width read here)
+constexpr int kMaxWidth = NW * 256;
+
+struct Args {
+  unsigned char* out;
+  const unsigned char* in;  // the border pass reads the frames directly
+  long long in_pitch, in_fs, out_pitch, out_fs;
+  long long* sums;
+  long long total;  // frames * rows output rows
+  int rows, cols;
+  int ws;   // bytes per ring row (the box width), multiple of 16, <= 2048
+  int nwa;  // consumer warps that own columns
+  const unsigned* k2;  // -> 0x47000000 (see below)
+  unsigned hint;       // mbarrier wait: suspend-time hint in ns (0: poll)
+};
+
+// 0x47000000 = the exponent word of 2^15.  Loaded from memory, which ptxas
+// cannot fold: with it as an immediate, every PRMT would need its selector
+// re-materialised into a register (the sk_u8stencil.cu note on lane_lo).
+__device__ const unsigned kK2 = 0x47000000u;
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned a, unsigned n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned a, unsigned parity, unsigned hint) {
+  unsigned done;
+  if (hint) {
+    do {
+      asm volatile(
+          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, 0, p; }"
+          : "=r"(done)
+          : "r"(a), "r"(parity), "r"(hint)
+          : "memory");
+    } while (!done);
+  } else {
+    do {
+      asm volatile(
+          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+          : "=r"(done)
+          : "r"(a), "r"(parity)
+          : "memory");
+    } while (!done);
+  }
+}
+__device__ __forceinline__ void mbar_arrive(unsigned a) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned a, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(unsigned dst, const CUtensorMap* tm, int c0, int c1,
+                                            int c2, int c3, unsigned bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
+      : "memory");
+}
+
+using F2 = float2;
+__device__ __forceinline__ F2 f2(float lo, float hi) { return make_float2(lo, hi); }
+__device__ __forceinline__ F2 add2(F2 a, F2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ F2 sub2(F2 a, F2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+__device__ __forceinline__ F2 mul2(F2 a, F2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ F2 fma2(F2 a, F2 b, F2 c) { return __ffma2_rn(a, b, c); }
+
+// byte k of w -> the exact float 2^15 + byte (K2 = 0x47000000, exponent word of 2^15)
+template <int k>
+__device__ __forceinline__ float bf(unsigned w, unsigned K2) {
+  return __uint_as_float(__byte_perm(w, K2, 0x7604u | (k << 4)));
+}
+
+// the next segment of a CTA's run: output rows [a, b) of frame f
+struct Seg {
+  long long g;  // global output row of the segment start
+  int f, a, b;
+};
+__device__ __forceinline__ bool next_seg(Seg& s, long long g1, int rows) {
+  if (s.g >= g1) return false;
+  s.f = (int)(s.g / rows);
+  s.a = (int)(s.g - (long long)s.f * rows);
+  const long long left = g1 - s.g;
+  s.b = left < rows - s.a ? s.a + (int)left : rows;
+  s.g += s.b - s.a;
+  return true;
+}
+
+// SR input rows per stage (even: the feature register sets alternate per
+// row), STAGES ring stages, MINB CTAs per SM; COPY: the consumers only move
+// the centre rows (a pipeline-throughput probe, not Sobel)
+template <int SR, int STAGES, int MINB, bool COPY>
+__global__ void __launch_bounds__(BLOCK, MINB)
+    sobel_tma_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ Args A) {
+  extern __shared__ __align__(128) unsigned char dyn[];
+  // 128-byte aligned ring base (dynamic shared memory is only 16-byte aligned)
+  const unsigned raw = smem_u32(dyn);
+  const unsigned base = (raw + 127u) & ~127u;
+  const int ws = A.ws;
+  const unsigned stage_bytes = (unsigned)(SR * ws);
+  const unsigned ring = base + FRONT;
+  const unsigned bars = ring + STAGES * stage_bytes + BACK;  // full[STAGES], empty[STAGES]
+  auto full = [&](int s) { return bars + 8u * s; };
+  auto empty = [&](int s) { return bars + 8u * (STAGES + s); };
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full(s), 1);
+      mbar_init(empty(s), (unsigned)A.nwa);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const long long g0 = A.total * blockIdx.x / gridDim.x;
+  const long long g1 = A.total * (blockIdx.x + 1) / gridDim.x;
+  const int rows = A.rows, cols = A.cols;
+
+  if (warp == NW) {  // ------------------------------------------------ producer
+    // Lane 0 streams the stages; the warp also recomputes the border columns
+    // 0 / cols-1 of each stage's output rows once the consumers are done
+    // with it (their main-path values there are excluded from their sums),
+    // and only then refills the buffer of the stage before it: a stage's
+    // first outputs and border pixels read the last rows of the previous one.
+    if (lane == 0)
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm)) : "memory");
+    Seg is{g0, 0, 0, 0};  // issue iterator
+    int is_k = 0, is_nst = 0;
+    bool is_more = true;
+    unsigned qi = 0;
+    auto issue_next = [&]() {
+      if (!is_more) return;
+      if (is_k == is_nst) {
+        if (!next_seg(is, g1, rows)) {
+          is_more = false;
+          return;
+        }
+        is_k = 0;
+        is_nst = (is.b - is.a + 2 + SR - 1) / SR;
+      }
+      if (lane == 0) {
+        const int s = (int)(qi % STAGES);
+        mbar_expect_tx(full(s), stage_bytes);
+        tma_load_4d(ring + s * stage_bytes, &tm, 0, 0, is.a - 1 + SR * is_k, is.f, full(s));
+      }
+      ++is_k;
+      ++qi;
+    };
+    for (int i = 0; i < STAGES; ++i) issue_next();
+    if (COPY) {
+      unsigned q = 0;
+      while (is_more || q < qi) {
+        if (q >= qi) break;
+        mbar_wait(empty(q % STAGES), (q / STAGES) & 1, A.hint);
+        ++q;
+        issue_next();
+      }
+      return;
+    }
+    const int t = lane & 15;
+    const bool right = lane >= 16;
+    const int c = right ? cols - 1 : 0;
+    const bool mine = t < SR && (!right || cols > 1);
+    unsigned q = 0;
+    Seg sg{g0, 0, 0, 0};
+    while (next_seg(sg, g1, rows)) {
+      const int a = sg.a, n_in = sg.b - sg.a + 2;
+      const int nst = (n_in + SR - 1) / SR;
+      unsigned char* const back = A.out + (long long)sg.f * A.out_fs;
+      unsigned acc = 0;
+      for (int k = 0; k < nst; ++k, ++q) {
+        mbar_wait(empty(q % STAGES), (q / STAGES) & 1, A.hint);
+        const unsigned sb = ring + (q % STAGES) * stage_bytes;
+        const unsigned pb = ring + ((q + STAGES - 1) % STAGES) * stage_bytes;
+        const int i = SR * k + t;  // input row of this lane's output row r = a + i - 2
+        if (mine && i >= 2 && i < n_in) {
+          const int r = a + i - 2;
+          auto rowp = [&](int d) -> unsigned {  // ring address of image row r + d
+            const int ii = i - 1 + d;           // input row, in stage k or k - 1
+            return (ii >= SR * k ? sb : pb) + (unsigned)((ii - SR * (ii / SR)) * ws);
+          };
+          auto ld = [&](unsigned pp) {
+            unsigned v;
+            asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(pp) : "memory");
+            return (int)v;
+          };
+          const unsigned pu = rowp(-1), pc = rowp(0), pd = rowp(1);
+          const int ctr = ld(pc + c);
+          const bool uok = r > 0, dok = r + 1 < rows, lok = c > 0, rok = c + 1 < cols;
+          const int nw = (uok && lok) ? ld(pu + c - 1) : ctr, n = uok ? ld(pu + c) : ctr;
+          const int ne = (uok && rok) ? ld(pu + c + 1) : ctr;
+          const int w = lok ? ld(pc + c - 1) : ctr, e = rok ? ld(pc + c + 1) : ctr;
+          const int sw = (dok && lok) ? ld(pd + c - 1) : ctr, so = dok ? ld(pd + c) : ctr;
+          const int se = (dok && rok) ? ld(pd + c + 1) : ctr;
+          const int gx = -nw + ne - 2 * w + 2 * e - sw + se;
+          const int gy = -nw - 2 * n - ne + sw + 2 * so + se;
+          float sq;
+          asm("sqrt.approx.f32 %0, %1;" : "=f"(sq) : "f"((float)(gx * gx + gy * gy)));
+          const int m = __float2int_rn(sq);
+          const unsigned v = (unsigned)(m > 255 ? 255 : m);
+          back[(long long)r * A.out_pitch + c] = (unsigned char)v;
+          acc += v;
+        }
+        __syncwarp();
+        if (q >= 1) issue_next();  // refills the buffer of stage q - 1
+      }
+      const unsigned tot = __reduce_add_sync(0xffffffffu, acc);
+      if (lane == 0 && tot)
+        atomicAdd(reinterpret_cast<unsigned long long*>(&A.sums[sg.f]), (unsigned long long)tot);
+    }
+    return;
+  }
+  if (warp >= A.nwa) return;
+
+  // -------------------------------------------------------------- consumers
+  unsigned K2;
+  asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(K2) : "l"(A.k2));
+  const int col = warp * 256 + lane * 8;
+  const int nvalid = cols - col;
+  const bool active = nvalid > 0;
+  const int wl = (cols - 1) >> 8;  // the warp that owns column cols-1
+  // bytes of this lane's 8 that the main path sums: inside the image and not
+  // on a border column (the producer warp recomputes those)
+  unsigned long long m64 =
+      nvalid >= 8 ? ~0ull : (nvalid <= 0 ? 0ull : (~0ull >> (64 - 8 * nvalid)));
+  if (col == 0) m64 &= ~0xffull;
+  if (nvalid >= 1 && nvalid <= 8) m64 &= ~(0xffull << (8 * (nvalid - 1)));
+  const unsigned mlo = (unsigned)m64, mhi = (unsigned)(m64 >> 32);
+  // unmasked rows: every pixel of the warp's strip inside the image, no border column
+  const bool plain_warp = cols >= warp * 256 + 256 && warp != 0 && warp != wl;
+  const unsigned lofs = (unsigned)col;  // this lane's byte offset in a ring row
+  const F2 two = f2(2.0f, 2.0f), four = f2(4.0f, 4.0f), magic = f2(12582912.0f, 12582912.0f);
+
+  F2 G[4], SA[4], SB[4], DA[4], DB[4];
+  unsigned acc = 0;
+  unsigned char* po = nullptr;
+
+  // the lane's four pairs Q_t = (p_t, p_t+4) of the ring row at p, times 4
+  auto quad4 = [&](unsigned p, F2* S) {
+    unsigned wx, wy;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(wx), "=r"(wy) : "r"(p) : "memory");
+    S[0] = mul2(f2(bf<0>(wx, K2), bf<0>(wy, K2)), four);
+    S[1] = mul2(f2(bf<1>(wx, K2), bf<1>(wy, K2)), four);
+    S[2] = mul2(f2(bf<2>(wx, K2), bf<2>(wy, K2)), four);
+    S[3] = mul2(f2(bf<3>(wx, K2), bf<3>(wy, K2)), four);
+  };
+  // features of the ring row at shared address p: S = L + 2Q + R, D = R - L
+  auto take = [&](unsigned p, F2* S, F2* D) {
+    unsigned wx, wy, xl, xr;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(wx), "=r"(wy) : "r"(p) : "memory");
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(xl) : "r"(p - 1) : "memory");
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(xr) : "r"(p + 8) : "memory");
+    const F2 Q0 = f2(bf<0>(wx, K2), bf<0>(wy, K2));
+    const F2 Q1 = f2(bf<1>(wx, K2), bf<1>(wy, K2));
+    const F2 Q2 = f2(bf<2>(wx, K2), bf<2>(wy, K2));
+    const F2 Q3 = f2(bf<3>(wx, K2), bf<3>(wy, K2));
+    const F2 L0 = f2(bf<0>(xl, K2), bf<3>(wx, K2));  // (p_-1, p_3)
+    const F2 R3 = f2(bf<0>(wy, K2), bf<0>(xr, K2));  // (p_4, p_8)
+    S[0] = fma2(Q0, two, add2(L0, Q1));
+    S[1] = fma2(Q1, two, add2(Q0, Q2));
+    S[2] = fma2(Q2, two, add2(Q1, Q3));
+    S[3] = fma2(Q3, two, add2(Q2, R3));
+    D[0] = sub2(Q1, L0);
+    D[1] = sub2(Q2, Q0);
+    D[2] = sub2(Q3, Q1);
+    D[3] = sub2(R3, Q2);
+  };
+  // input row at p -> the output row above it: gx = G + D(new), gy = S(new) - S(old).
+  // Image rows 0 / rows-1 need no fix-up: rows outside the frame arrive as
+  // zeros (D = 0, which is the reference's gx there), and S of the missing
+  // row is replaced by 4 Q of the centre row (the reference's gy there):
+  // SA at the top (below), S(new) = 4 Q(row above) at the bottom (`pbot`).
+  auto step = [&](auto masked_t, auto hot_t, unsigned p, F2* Sold, F2* Dprev, F2* Dnew,
+                  unsigned pbot) {
+    constexpr bool MASKED = decltype(masked_t)::value;
+    constexpr bool HOT = decltype(hot_t)::value;
+    F2 S[4];
+    take(p, S, Dnew);
+    if (!HOT && pbot) quad4(pbot, S);
+    unsigned o[8];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const F2 gx = add2(G[k], Dnew[k]);
+      const F2 gy = sub2(S[k], Sold[k]);
+      const F2 n = fma2(gx, gx, mul2(gy, gy));
+      float x = n.x, y = n.y;
+      asm("sqrt.approx.ftz.f32 %0, %0;" : "+f"(x));
+      asm("sqrt.approx.ftz.f32 %0, %0;" : "+f"(y));
+      const F2 r = add2(f2(x, y), magic);  // rint(sqrt(n)) in the low 16 bits
+      o[k] = __float_as_uint(r.x);
+      o[k + 4] = __float_as_uint(r.y);
+      G[k] = fma2(Dnew[k], two, Dprev[k]);
+      Sold[k] = S[k];
+    }
+    const unsigned x01 = __vminu2(__byte_perm(o[0], o[1], 0x5410u), 0x00ff00ffu);
+    const unsigned x23 = __vminu2(__byte_perm(o[2], o[3], 0x5410u), 0x00ff00ffu);
+    const unsigned y01 = __vminu2(__byte_perm(o[4], o[5], 0x5410u), 0x00ff00ffu);
+    const unsigned y23 = __vminu2(__byte_perm(o[6], o[7], 0x5410u), 0x00ff00ffu);
+    unsigned lo = __byte_perm(x01, x23, 0x6420u);
+    unsigned hi = __byte_perm(y01, y23, 0x6420u);
+    if constexpr (MASKED) {
+      lo &= mlo;
+      hi &= mhi;
+    }
+    acc = __dp4a(lo, 0x01010101u, acc);
+    acc = __dp4a(hi, 0x01010101u, acc);
+    if (!MASKED || active) *reinterpret_cast<uint2*>(po) = make_uint2(lo, hi);
+    po += A.out_pitch;
+  };
+
+  unsigned q = 0;
+  Seg sg{g0, 0, 0, 0};
+  while (next_seg(sg, g1, rows)) {
+    const int a = sg.a, b = sg.b, f = sg.f;
+    const int n_in = b - a + 2;
+    const int nst = (n_in + SR - 1) / SR;
+    const bool top = a == 0, bottom = b == rows;
+    unsigned char* const back = A.out + (long long)f * A.out_fs;
+    po = back + (long long)a * A.out_pitch + col;
+    acc = 0;
+    unsigned prev_sb = 0;  // ring buffer of the previous stage (not refilled before this one is done)
+    // stage k holds input rows i = SR*k + j (image row a - 1 + i), j < SR
+    auto stage = [&](auto hot_t, auto masked_t, unsigned sb, int k) {
+      // HOT: a full stage that is neither the segment's first nor its last
+      // (no row special cases); MASKED: the warp has border-column or
+      // off-image pixels (byte masks on the sum and the store)
+      constexpr bool HOT = decltype(hot_t)::value;
+      constexpr bool MASKED = decltype(masked_t)::value;
+      const int jn = n_in - SR * k;
+#pragma unroll
+      for (int j = 0; j < SR; ++j) {
+        if (!HOT && j >= jn) break;
+        const unsigned p = sb + (unsigned)(j * ws) + lofs;
+        if constexpr (COPY) {
+          if (k == 0 && j < 2) continue;
+          unsigned wx, wy;
+          asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(wx), "=r"(wy) : "r"(p) : "memory");
+          if (active) *reinterpret_cast<uint2*>(po) = make_uint2(wx, wy);
+          po += A.out_pitch;
+          continue;
+        }
+        if (!HOT && k == 0 && j == 0) {
+          take(p, SA, DA);
+          if (top) quad4(p + ws, SA);
+        } else if (!HOT && k == 0 && j == 1) {
+          take(p, SB, DB);
+#pragma unroll
+          for (int t = 0; t < 4; ++t) G[t] = fma2(DB[t], two, DA[t]);
+        } else {
+          const unsigned pb = (!HOT && bottom && j == jn - 1)
+                                  ? (j > 0 ? p - ws : prev_sb + (SR - 1) * ws + lofs)
+                                  : 0u;
+          if (j & 1) step(masked_t, hot_t, p, SB, DA, DB, pb);
+          else step(masked_t, hot_t, p, SA, DB, DA, pb);
+        }
+      }
+    };
+    for (int k = 0; k < nst; ++k, ++q) {
+      const int s = (int)(q % STAGES);
+      mbar_wait(full(s), (q / STAGES) & 1, A.hint);
+      const unsigned sb = ring + s * stage_bytes;
+      if (k > 0 && SR * (k + 1) < n_in) {
+        if (plain_warp) stage(std::true_type{}, std::false_type{}, sb, k);
+        else stage(std::true_type{}, std::true_type{}, sb, k);
+      } else {
+        stage(std::false_type{}, std::true_type{}, sb, k);
+      }
+      // release: the row stores precede the arrive (the producer warp then
+      // overwrites the border columns of these rows)
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty(s));
+      prev_sb = sb;
+    }
+    const unsigned tot = __reduce_add_sync(0xffffffffu, acc);
+    if (lane == 0 && tot)
+      atomicAdd(reinterpret_cast<unsigned long long*>(&A.sums[f]), (unsigned long long)tot);
+  }
+}
+
+// driver entry point for tensor-map encoding (no libcuda link)
+PFN_cuTensorMapEncodeTiled_v12000 encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &f, 12000, cudaEnableDefault,
+                                         &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  });
+  return fn;
+}
+
+bool disabled() {
+  static const bool v = [] {
+    const char* e = getenv("SK_SOBEL_TMA");
+    return e && e[0] == '0';
+  }();
+  return v;
+}
+
+size_t smem_bytes(int ws, int sr, int stages) {
+  return 128 + FRONT + (size_t)stages * sr * ws + BACK + 16 * stages;
+}
+
+using KFn = void (*)(const CUtensorMap, const Args);
+struct Cfg {
+  int sr, stages, minb;
+  bool copy;
+  KFn fn;
+};
+// measured configurations (SK_TMA_CFG=<index> selects one; 0 is the default)
+const Cfg kCfgs[] = {
+    {8, 6, 2, false, sobel_tma_kernel<8, 6, 2, false>},
+    {4, 12, 2, false, sobel_tma_kernel<4, 12, 2, false>},
+    {16, 3, 2, false, sobel_tma_kernel<16, 3, 2, false>},
+    {8, 4, 3, false, sobel_tma_kernel<8, 4, 3, false>},
+    {4, 8, 3, false, sobel_tma_kernel<4, 8, 3, false>},
+    {8, 12, 1, false, sobel_tma_kernel<8, 12, 1, false>},
+    {8, 6, 2, true, sobel_tma_kernel<8, 6, 2, true>},
+    {4, 8, 3, true, sobel_tma_kernel<4, 8, 3, true>},
+};
+
+const Cfg& cfg() {
+  static const int i = [] {
+    const char* e = getenv("SK_TMA_CFG");
+    const int n = (int)(sizeof(kCfgs) / sizeof(kCfgs[0]));
+    const int v = e ? atoi(e) : 0;
+    return v >= 0 && v < n ? v : 0;
+  }();
+  return kCfgs[i];
+}
+
+unsigned hint_ns() {
+  static const unsigned v = [] {
+    const char* e = getenv("SK_TMA_HINT");
+    return e ? (unsigned)strtoul(e, nullptr, 10) : 0u;
+  }();
+  return v;
+}
+
+}  // namespace sobel_tma
+
+// Returns SK_OK after enqueueing the TMA kernel, or SK_ERR_UNSUPPORTED when the
+// geometry does not fit it (the caller then runs the generic batched sweep).
+int sobel_frames_tma(const uint8_t* in, long long in_pitch, long long in_fs, uint8_t* out,
+                     long long out_pitch, long long out_fs, int frames, long long rows,
+                     long long cols, long long* sums, cudaStream_t s) {
+  using namespace sobel_tma;
+  if (disabled()) return SK_ERR_UNSUPPORTED;
+  if (frames == 1) in_fs = rows * in_pitch;
+  if (in_pitch % 16 || in_fs % 16 || (reinterpret_cast<uintptr_t>(in) & 15) || rows >= (1ll << 31) ||
+      frames < 1 || in_fs < rows * in_pitch)
+    return SK_ERR_UNSUPPORTED;
+  // inner box block: the widest of 256..16 bytes whose whole blocks stay inside a row's pitch
+  long long ib = 256;
+  while (ib > 16 && (cols + ib - 1) / ib * ib > in_pitch) ib >>= 1;
+  const long long ws = (cols + ib - 1) / ib * ib;
+  if (ws > kMaxWidth || ws > in_pitch) return SK_ERR_UNSUPPORTED;
+  auto enc = encoder();
+  if (!enc) return SK_ERR_UNSUPPORTED;
+
+  CUtensorMap tm;
+  cuuint64_t dims[4] = {(cuuint64_t)ib, (cuuint64_t)(ws / ib), (cuuint64_t)rows, (cuuint64_t)frames};
+  cuuint64_t strides[3] = {(cuuint64_t)ib, (cuuint64_t)in_pitch, (cuuint64_t)in_fs};
+  const Cfg& C = cfg();
+  cuuint32_t box[4] = {(cuuint32_t)ib, (cuuint32_t)(ws / ib), (cuuint32_t)C.sr, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult cr = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<uint8_t*>(in), dims, strides,
+                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) return SK_ERR_UNSUPPORTED;
+
+  int dev = 0;
+  SK_CUDA(cudaGetDevice(&dev));
+  static const unsigned* k2ptr[64] = {};
+  const int dslot = dev < 64 ? dev : 63;
+  const size_t smem = smem_bytes((int)ws, C.sr, C.stages);
+  static std::mutex mu;
+  static size_t attr_set[64][8] = {};
+  const int ci = (int)(&C - kCfgs);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    const int d = dev < 64 ? dev : 63;
+    if (!k2ptr[d]) {
+      void* p = nullptr;
+      SK_CUDA(cudaGetSymbolAddress(&p, kK2));
+      k2ptr[d] = static_cast<const unsigned*>(p);
+    }
+    if (attr_set[d][ci] < smem) {
+      SK_CUDA(cudaFuncSetAttribute(C.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr_set[d][ci] = smem;
+    }
+  }
+  int per_sm = 0;
+  SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, C.fn, BLOCK, smem));
+  if (per_sm < 1) return SK_ERR_UNSUPPORTED;
+  Args a{};
+  a.out = out;
+  a.in = in;
+  a.in_pitch = in_pitch;
+  a.in_fs = in_fs;
+  a.out_pitch = out_pitch;
+  a.out_fs = out_fs;
+  a.sums = sums;
+  a.total = (long long)frames * rows;
+  a.rows = (int)rows;
+  a.cols = (int)cols;
+  a.ws = (int)ws;
+  a.nwa = (int)((cols + 255) / 256);
+  a.k2 = k2ptr[dslot];
+  a.hint = hint_ns();
+  long long grid = (long long)device_sms(dev) * per_sm;
+  const long long min_rows = 16;  // at least a couple of stages per CTA
+  if (grid > (a.total + min_rows - 1) / min_rows) grid = (a.total + min_rows - 1) / min_rows;
+  if (grid < 1) grid = 1;
+  SK_CUDA(cudaMemsetAsync(sums, 0, sizeof(long long) * frames, s));
+  C.fn<<<(int)grid, BLOCK, smem, s>>>(tm, a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "sobel_frames (TMA) launch");
+  return SK_OK;
+}
+
+}  // namespace sk

@@ -922,6 +922,11 @@ int sobel_frames(const uint8_t* in, long long in_pitch, long long in_fs, uint8_t
     set_error("sk_sobel_frames: bad arguments (pitches/strides/pointers must be 8-byte aligned)");
     return SK_ERR_ARG;
   }
+  {
+    const int rc = sobel_frames_tma(in, in_pitch, in_fs, out, out_pitch, out_fs, frames, rows, cols,
+                                    sums, s);
+    if (rc != SK_ERR_UNSUPPORTED) return rc;
+  }
   int dev = 0;
   SK_CUDA(cudaGetDevice(&dev));
   const bool al16 = in_pitch % 16 == 0 && in_fs % 16 == 0 && in_pitch < (1ll << 31) &&
