@@ -288,8 +288,10 @@ def c2(args, ClockSampler, measured_peaks, local=0, world=1, rank=0):
         "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
                      "frac": ach / peak, "traffic": _traffic("sobel_2048_per_frame", B),
                      "avg_kernel_ms": kms,
-                     "kernel": f"sobel_sweep batched ({B} frames/launch), 2 B/pixel",
-                     "note": "issue-bound: f32x2 features, exact per-pixel sqrt/round path (profiles/r01e_ncu_sobel.json)",
+                     "kernel": f"sobel_tma_kernel ({B} frames/launch; TMA row ring), 2 B/pixel",
+                     "note": "issue/FMA-pipe bound: f32x2 features, exact per-pixel sqrt/round "
+                             "(profiles/r02_ncu_sobel_tma.json; the same ring as a pure copy "
+                             "streams 5.9 TB/s)",
                      "peak_source": pk},
         "cpu_baseline": None if cpu is None else
         {"value": cpu, "unit": "frames/s", "cores": cores, "kind": "port", "sample": sample},

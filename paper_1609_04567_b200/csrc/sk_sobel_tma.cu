@@ -21,10 +21,10 @@
 //    transaction count; the consumer warps release a stage through a second
 //    mbarrier.  No consumer lane issues a copy or computes a global address
 //    for its input.
-//  * Consumer warp w owns columns 256w .. 256w+255 of every row; lane j owns
-//    the 8 contiguous pixels 8j .. 8j+7, held as four pairs (p_t, p_t+4), so
-//    a row costs one 8-byte shared load plus two neighbour bytes, and the
-//    result is one 8-byte store.
+//  * Consumer warp w owns columns 32V w .. 32V w + 32V-1 of every row; lane j
+//    owns the V contiguous pixels Vj .. Vj+V-1 (V = 8 or 4), held as V/2
+//    pairs (p_t, p_t+V/2), so a row costs one V-byte shared load plus two
+//    neighbour bytes, and the result is one V-byte store.
 //  * Border pixels follow the reference's centre-substitution rule without a
 //    global re-read: image rows 0 / rows-1 come out of the main path exactly
 //    (rows outside the frame arrive as zeros and S of the missing row is
@@ -47,11 +47,10 @@ namespace sk {
 
 namespace sobel_tma {
 
-constexpr int NW = 8;  // consumer warps: 8 x 256 columns = rows up to 2048 bytes
-constexpr int BLOCK = (NW + 1) * 32;
+constexpr int kRowMax = 2048;  // bytes per ring row: the consumer warps span it
 constexpr int FRONT = 128;  // guard before the ring (TMA destinations are 128-byte aligned)
 constexpr int BACK = 256;   // guard after it (lanes past the row width read here)
-constexpr int kMaxWidth = NW * 256;
+constexpr int kMaxWidth = kRowMax;
 
 struct Args {
   unsigned char* out;
@@ -97,6 +96,15 @@ __device__ __forceinline__ void mbar_wait(unsigned a, unsigned parity, unsigned 
     } while (!done);
   }
 }
+__device__ __forceinline__ bool mbar_test(unsigned a, unsigned parity) {
+  unsigned done;
+  asm volatile(
+      "{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+      : "=r"(done)
+      : "r"(a), "r"(parity)
+      : "memory");
+  return done != 0;
+}
 __device__ __forceinline__ void mbar_arrive(unsigned a) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
 }
@@ -120,6 +128,12 @@ __device__ __forceinline__ F2 sub2(F2 a, F2 b) { return __fadd2_rn(a, make_float
 __device__ __forceinline__ F2 mul2(F2 a, F2 b) { return __fmul2_rn(a, b); }
 __device__ __forceinline__ F2 fma2(F2 a, F2 b, F2 c) { return __ffma2_rn(a, b, c); }
 
+template <int k>
+__device__ __forceinline__ float bf_opaque(unsigned w, unsigned K2) {
+  unsigned r;
+  asm volatile("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(w), "r"(K2), "n"(0x7604 | (k << 4)));
+  return __uint_as_float(r);
+}
 // byte k of w -> the exact float 2^15 + byte (K2 = 0x47000000, exponent word of 2^15)
 template <int k>
 __device__ __forceinline__ float bf(unsigned w, unsigned K2) {
@@ -144,14 +158,26 @@ __device__ __forceinline__ bool next_seg(Seg& s, long long g1, int rows) {
 // SR input rows per stage (even: the feature register sets alternate per
 // row), STAGES ring stages, MINB CTAs per SM; COPY: the consumers only move
 // the centre rows (a pipeline-throughput probe, not Sobel)
-template <int SR, int STAGES, int MINB, bool COPY>
-__global__ void __launch_bounds__(BLOCK, MINB)
+// VEC pixels per lane (8: one 8-byte load/store per row; 4: twice the warps
+// at half the registers); NW = 2048 / (32 VEC) consumer warps + 1 producer
+template <int VEC>
+constexpr int block_of() {
+  return (kRowMax / (32 * VEC) + 1) * 32;
+}
+// WIDE: ring rows and output rows are exactly kRowMax bytes (compile-time
+// shared and global row offsets, no per-row address arithmetic)
+template <int SR, int STAGES, int MINB, bool COPY, int VEC, bool WIDE>
+__global__ void __launch_bounds__(block_of<VEC>(), MINB)
     sobel_tma_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ Args A) {
+  constexpr int NW = kRowMax / (32 * VEC);
+  constexpr int NP = VEC / 2;       // pixel pairs per lane: (p_t, p_t+NP)
+  constexpr int WCOLS = 32 * VEC;   // columns per consumer warp
   extern __shared__ __align__(128) unsigned char dyn[];
   // 128-byte aligned ring base (dynamic shared memory is only 16-byte aligned)
   const unsigned raw = smem_u32(dyn);
   const unsigned base = (raw + 127u) & ~127u;
-  const int ws = A.ws;
+  const int ws = WIDE ? kRowMax : A.ws;
+  const long long opitch = WIDE ? (long long)kRowMax : A.out_pitch;
   const unsigned stage_bytes = (unsigned)(SR * ws);
   const unsigned ring = base + FRONT;
   const unsigned bars = ring + STAGES * stage_bytes + BACK;  // full[STAGES], empty[STAGES]
@@ -270,55 +296,71 @@ __global__ void __launch_bounds__(BLOCK, MINB)
   // -------------------------------------------------------------- consumers
   unsigned K2;
   asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(K2) : "l"(A.k2));
-  const int col = warp * 256 + lane * 8;
+  const int col = warp * WCOLS + lane * VEC;
   const int nvalid = cols - col;
   const bool active = nvalid > 0;
-  const int wl = (cols - 1) >> 8;  // the warp that owns column cols-1
-  // bytes of this lane's 8 that the main path sums: inside the image and not
-  // on a border column (the producer warp recomputes those)
+  const int wl = (cols - 1) / WCOLS;  // the warp that owns column cols-1
+  // bytes of this lane's VEC that the main path sums: inside the image and
+  // not on a border column (the producer warp recomputes those)
   unsigned long long m64 =
       nvalid >= 8 ? ~0ull : (nvalid <= 0 ? 0ull : (~0ull >> (64 - 8 * nvalid)));
   if (col == 0) m64 &= ~0xffull;
-  if (nvalid >= 1 && nvalid <= 8) m64 &= ~(0xffull << (8 * (nvalid - 1)));
+  if (nvalid >= 1 && nvalid <= VEC) m64 &= ~(0xffull << (8 * (nvalid - 1)));
   const unsigned mlo = (unsigned)m64, mhi = (unsigned)(m64 >> 32);
   // unmasked rows: every pixel of the warp's strip inside the image, no border column
-  const bool plain_warp = cols >= warp * 256 + 256 && warp != 0 && warp != wl;
+  const bool plain_warp = cols >= warp * WCOLS + WCOLS && warp != 0 && warp != wl;
   const unsigned lofs = (unsigned)col;  // this lane's byte offset in a ring row
   const F2 two = f2(2.0f, 2.0f), four = f2(4.0f, 4.0f), magic = f2(12582912.0f, 12582912.0f);
 
-  F2 G[4], SA[4], SB[4], DA[4], DB[4];
+  F2 G[NP], SA[NP], SB[NP], DA[NP], DB[NP];
   unsigned acc = 0;
   unsigned char* po = nullptr;
 
-  // the lane's four pairs Q_t = (p_t, p_t+4) of the ring row at p, times 4
+  // the lane's pairs Q_t = (p_t, p_t+NP) of the ring row at p
+  auto pairs = [&](unsigned p, F2* Q, unsigned& wlo, unsigned& whi) {
+    if constexpr (VEC == 8) {
+      unsigned wx, wy;
+      asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(wx), "=r"(wy) : "r"(p) : "memory");
+      wlo = wx;
+      whi = wy;
+      Q[0] = f2(bf<0>(wx, K2), bf<0>(wy, K2));
+      Q[1] = f2(bf<1>(wx, K2), bf<1>(wy, K2));
+      Q[2] = f2(bf<2>(wx, K2), bf<2>(wy, K2));
+      Q[3] = f2(bf<3>(wx, K2), bf<3>(wy, K2));
+    } else {
+      unsigned w;
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w) : "r"(p) : "memory");
+      wlo = whi = w;
+      Q[0] = f2(bf<0>(w, K2), bf<2>(w, K2));
+      Q[1] = f2(bf<1>(w, K2), bf<3>(w, K2));
+    }
+  };
+  // 4 Q of the ring row at p (the S of a missing row above / below the frame)
   auto quad4 = [&](unsigned p, F2* S) {
-    unsigned wx, wy;
-    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(wx), "=r"(wy) : "r"(p) : "memory");
-    S[0] = mul2(f2(bf<0>(wx, K2), bf<0>(wy, K2)), four);
-    S[1] = mul2(f2(bf<1>(wx, K2), bf<1>(wy, K2)), four);
-    S[2] = mul2(f2(bf<2>(wx, K2), bf<2>(wy, K2)), four);
-    S[3] = mul2(f2(bf<3>(wx, K2), bf<3>(wy, K2)), four);
+    unsigned wlo, whi;
+    pairs(p, S, wlo, whi);
+#pragma unroll
+    for (int t = 0; t < NP; ++t) S[t] = mul2(S[t], four);
   };
   // features of the ring row at shared address p: S = L + 2Q + R, D = R - L
   auto take = [&](unsigned p, F2* S, F2* D) {
-    unsigned wx, wy, xl, xr;
-    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(wx), "=r"(wy) : "r"(p) : "memory");
+    unsigned xl, xr, wlo, whi;
+    F2 Q[NP];
+    pairs(p, Q, wlo, whi);
     asm volatile("ld.shared.u8 %0, [%1];" : "=r"(xl) : "r"(p - 1) : "memory");
-    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(xr) : "r"(p + 8) : "memory");
-    const F2 Q0 = f2(bf<0>(wx, K2), bf<0>(wy, K2));
-    const F2 Q1 = f2(bf<1>(wx, K2), bf<1>(wy, K2));
-    const F2 Q2 = f2(bf<2>(wx, K2), bf<2>(wy, K2));
-    const F2 Q3 = f2(bf<3>(wx, K2), bf<3>(wy, K2));
-    const F2 L0 = f2(bf<0>(xl, K2), bf<3>(wx, K2));  // (p_-1, p_3)
-    const F2 R3 = f2(bf<0>(wy, K2), bf<0>(xr, K2));  // (p_4, p_8)
-    S[0] = fma2(Q0, two, add2(L0, Q1));
-    S[1] = fma2(Q1, two, add2(Q0, Q2));
-    S[2] = fma2(Q2, two, add2(Q1, Q3));
-    S[3] = fma2(Q3, two, add2(Q2, R3));
-    D[0] = sub2(Q1, L0);
-    D[1] = sub2(Q2, Q0);
-    D[2] = sub2(Q3, Q1);
-    D[3] = sub2(R3, Q2);
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(xr) : "r"(p + VEC) : "memory");
+    // (p_-1, p_NP-1) and (p_NP, p_VEC); the shared pixels are converted again
+    // (an opaque PRMT on the ALU pipe) rather than copied into the pair (a
+    // move on the FMA pipe, which the paired arithmetic already saturates)
+    const F2 L0 = f2(bf<0>(xl, K2), bf_opaque<VEC == 8 ? 3 : 1>(wlo, K2));
+    const F2 RN = f2(bf_opaque<VEC == 8 ? 0 : 2>(whi, K2), bf<0>(xr, K2));
+#pragma unroll
+    for (int t = 0; t < NP; ++t) {
+      const F2 L = t == 0 ? L0 : Q[t - 1];
+      const F2 R = t == NP - 1 ? RN : Q[t + 1];
+      S[t] = fma2(Q[t], two, add2(L, R));
+      D[t] = sub2(R, L);
+    }
   };
   // input row at p -> the output row above it: gx = G + D(new), gy = S(new) - S(old).
   // Image rows 0 / rows-1 need no fix-up: rows outside the frame arrive as
@@ -326,44 +368,48 @@ __global__ void __launch_bounds__(BLOCK, MINB)
   // row is replaced by 4 Q of the centre row (the reference's gy there):
   // SA at the top (below), S(new) = 4 Q(row above) at the bottom (`pbot`).
   auto step = [&](auto masked_t, auto hot_t, unsigned p, F2* Sold, F2* Dprev, F2* Dnew,
-                  unsigned pbot) {
+                  unsigned pbot, unsigned char* q) {
     constexpr bool MASKED = decltype(masked_t)::value;
     constexpr bool HOT = decltype(hot_t)::value;
-    F2 S[4];
+    F2 S[NP];
     take(p, S, Dnew);
     if (!HOT && pbot) quad4(pbot, S);
-    unsigned o[8];
+    unsigned o[VEC];  // o[k]: pixel k, rint(sqrt(n)) in the low 16 bits
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < NP; ++k) {
       const F2 gx = add2(G[k], Dnew[k]);
       const F2 gy = sub2(S[k], Sold[k]);
       const F2 n = fma2(gx, gx, mul2(gy, gy));
       float x = n.x, y = n.y;
       asm("sqrt.approx.ftz.f32 %0, %0;" : "+f"(x));
       asm("sqrt.approx.ftz.f32 %0, %0;" : "+f"(y));
-      const F2 r = add2(f2(x, y), magic);  // rint(sqrt(n)) in the low 16 bits
+      const F2 r = add2(f2(x, y), magic);
       o[k] = __float_as_uint(r.x);
-      o[k + 4] = __float_as_uint(r.y);
+      o[k + NP] = __float_as_uint(r.y);
       G[k] = fma2(Dnew[k], two, Dprev[k]);
       Sold[k] = S[k];
     }
-    const unsigned x01 = __vminu2(__byte_perm(o[0], o[1], 0x5410u), 0x00ff00ffu);
-    const unsigned x23 = __vminu2(__byte_perm(o[2], o[3], 0x5410u), 0x00ff00ffu);
-    const unsigned y01 = __vminu2(__byte_perm(o[4], o[5], 0x5410u), 0x00ff00ffu);
-    const unsigned y23 = __vminu2(__byte_perm(o[6], o[7], 0x5410u), 0x00ff00ffu);
-    unsigned lo = __byte_perm(x01, x23, 0x6420u);
-    unsigned hi = __byte_perm(y01, y23, 0x6420u);
-    if constexpr (MASKED) {
-      lo &= mlo;
-      hi &= mhi;
+    unsigned wd[VEC / 4];
+#pragma unroll
+    for (int h = 0; h < VEC / 4; ++h) {
+      const unsigned x01 = __vminu2(__byte_perm(o[4 * h], o[4 * h + 1], 0x5410u), 0x00ff00ffu);
+      const unsigned x23 = __vminu2(__byte_perm(o[4 * h + 2], o[4 * h + 3], 0x5410u), 0x00ff00ffu);
+      wd[h] = __byte_perm(x01, x23, 0x6420u);
     }
-    acc = __dp4a(lo, 0x01010101u, acc);
-    acc = __dp4a(hi, 0x01010101u, acc);
-    if (!MASKED || active) *reinterpret_cast<uint2*>(po) = make_uint2(lo, hi);
-    po += A.out_pitch;
+    if constexpr (MASKED) {
+      wd[0] &= mlo;
+      if constexpr (VEC == 8) wd[1] &= mhi;
+    }
+#pragma unroll
+    for (int h = 0; h < VEC / 4; ++h) acc = __dp4a(wd[h], 0x01010101u, acc);
+    if (!MASKED || active) {
+      if constexpr (VEC == 8) *reinterpret_cast<uint2*>(q) = make_uint2(wd[0], wd[1]);
+      else *reinterpret_cast<unsigned*>(q) = wd[0];
+    }
   };
 
-  unsigned q = 0;
+  int cs = 0;         // ring stage of the next row block
+  unsigned cph = 0;   // its full-barrier phase parity
   Seg sg{g0, 0, 0, 0};
   while (next_seg(sg, g1, rows)) {
     const int a = sg.a, b = sg.b, f = sg.f;
@@ -371,7 +417,7 @@ __global__ void __launch_bounds__(BLOCK, MINB)
     const int nst = (n_in + SR - 1) / SR;
     const bool top = a == 0, bottom = b == rows;
     unsigned char* const back = A.out + (long long)f * A.out_fs;
-    po = back + (long long)a * A.out_pitch + col;
+    po = back + (long long)a * opitch + col;
     acc = 0;
     unsigned prev_sb = 0;  // ring buffer of the previous stage (not refilled before this one is done)
     // stage k holds input rows i = SR*k + j (image row a - 1 + i), j < SR
@@ -390,8 +436,8 @@ __global__ void __launch_bounds__(BLOCK, MINB)
           if (k == 0 && j < 2) continue;
           unsigned wx, wy;
           asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(wx), "=r"(wy) : "r"(p) : "memory");
-          if (active) *reinterpret_cast<uint2*>(po) = make_uint2(wx, wy);
-          po += A.out_pitch;
+          if (active) *reinterpret_cast<uint2*>(po) = make_uint2(wx, wy);  // (VEC 8 probe)
+          po += opitch;
           continue;
         }
         if (!HOT && k == 0 && j == 0) {
@@ -400,31 +446,38 @@ __global__ void __launch_bounds__(BLOCK, MINB)
         } else if (!HOT && k == 0 && j == 1) {
           take(p, SB, DB);
 #pragma unroll
-          for (int t = 0; t < 4; ++t) G[t] = fma2(DB[t], two, DA[t]);
+          for (int t = 0; t < NP; ++t) G[t] = fma2(DB[t], two, DA[t]);
         } else {
           const unsigned pb = (!HOT && bottom && j == jn - 1)
                                   ? (j > 0 ? p - ws : prev_sb + (SR - 1) * ws + lofs)
                                   : 0u;
-          if (j & 1) step(masked_t, hot_t, p, SB, DA, DB, pb);
-          else step(masked_t, hot_t, p, SA, DB, DA, pb);
+          // HOT stages write rows po + j * pitch (po advances after the stage)
+          unsigned char* const q = HOT ? po + j * opitch : po;
+          if (j & 1) step(masked_t, hot_t, p, SB, DA, DB, pb, q);
+          else step(masked_t, hot_t, p, SA, DB, DA, pb, q);
+          if (!HOT) po += opitch;
         }
       }
     };
-    for (int k = 0; k < nst; ++k, ++q) {
-      const int s = (int)(q % STAGES);
-      mbar_wait(full(s), (q / STAGES) & 1, A.hint);
-      const unsigned sb = ring + s * stage_bytes;
+    for (int k = 0; k < nst; ++k) {
+      mbar_wait(full(cs), cph, A.hint);
+      const unsigned sb = ring + cs * stage_bytes;
+      const int ns = cs + 1 == STAGES ? 0 : cs + 1;
+      const unsigned nph = ns == 0 ? cph ^ 1u : cph;
       if (k > 0 && SR * (k + 1) < n_in) {
         if (plain_warp) stage(std::true_type{}, std::false_type{}, sb, k);
         else stage(std::true_type{}, std::true_type{}, sb, k);
+        po += SR * opitch;
       } else {
         stage(std::false_type{}, std::true_type{}, sb, k);
       }
       // release: the row stores precede the arrive (the producer warp then
       // overwrites the border columns of these rows)
       __syncwarp();
-      if (lane == 0) mbar_arrive(empty(s));
+      if (lane == 0) mbar_arrive(empty(cs));
       prev_sb = sb;
+      cs = ns;
+      cph = nph;
     }
     const unsigned tot = __reduce_add_sync(0xffffffffu, acc);
     if (lane == 0 && tot)
@@ -463,19 +516,20 @@ using KFn = void (*)(const CUtensorMap, const Args);
 struct Cfg {
   int sr, stages, minb;
   bool copy;
-  KFn fn;
+  int vec;
+  KFn fn, fn_wide;
 };
 // measured configurations (SK_TMA_CFG=<index> selects one; 0 is the default)
+#define SK_TMA_CFG_ROW(sr, st, mb, cp, v) \
+  {sr, st, mb, cp, v, sobel_tma_kernel<sr, st, mb, cp, v, false>, sobel_tma_kernel<sr, st, mb, cp, v, true>}
 const Cfg kCfgs[] = {
-    {8, 6, 2, false, sobel_tma_kernel<8, 6, 2, false>},
-    {4, 12, 2, false, sobel_tma_kernel<4, 12, 2, false>},
-    {16, 3, 2, false, sobel_tma_kernel<16, 3, 2, false>},
-    {8, 4, 3, false, sobel_tma_kernel<8, 4, 3, false>},
-    {4, 8, 3, false, sobel_tma_kernel<4, 8, 3, false>},
-    {8, 12, 1, false, sobel_tma_kernel<8, 12, 1, false>},
-    {8, 6, 2, true, sobel_tma_kernel<8, 6, 2, true>},
-    {4, 8, 3, true, sobel_tma_kernel<4, 8, 3, true>},
+    SK_TMA_CFG_ROW(8, 6, 2, false, 8),   // default: 1.03 ms per 512 C2 frames
+    SK_TMA_CFG_ROW(4, 12, 2, false, 8),  // finer stages: 1.15 ms
+    SK_TMA_CFG_ROW(8, 6, 2, false, 4),   // 4 pixels per lane, 2x warps: 1.20 ms
+    SK_TMA_CFG_ROW(8, 12, 1, false, 8),  // one CTA per SM, 12 stages: 1.10 ms
+    SK_TMA_CFG_ROW(8, 6, 2, true, 8),    // copy probe (not Sobel): 0.73 ms = 5.9 TB/s
 };
+#undef SK_TMA_CFG_ROW
 
 const Cfg& cfg() {
   static const int i = [] {
@@ -533,8 +587,11 @@ int sobel_frames_tma(const uint8_t* in, long long in_pitch, long long in_fs, uin
   const int dslot = dev < 64 ? dev : 63;
   const size_t smem = smem_bytes((int)ws, C.sr, C.stages);
   static std::mutex mu;
-  static size_t attr_set[64][8] = {};
-  const int ci = (int)(&C - kCfgs);
+  static size_t attr_set[64][16] = {};
+  // rows of exactly 2048 bytes in and out: the compile-time-pitch kernel
+  const bool wide = ws == kRowMax && out_pitch == kRowMax;
+  const KFn fn = wide ? C.fn_wide : C.fn;
+  const int ci = 2 * (int)(&C - kCfgs) + (wide ? 1 : 0);
   {
     std::lock_guard<std::mutex> lk(mu);
     const int d = dev < 64 ? dev : 63;
@@ -544,12 +601,13 @@ int sobel_frames_tma(const uint8_t* in, long long in_pitch, long long in_fs, uin
       k2ptr[d] = static_cast<const unsigned*>(p);
     }
     if (attr_set[d][ci] < smem) {
-      SK_CUDA(cudaFuncSetAttribute(C.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      SK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       attr_set[d][ci] = smem;
     }
   }
   int per_sm = 0;
-  SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, C.fn, BLOCK, smem));
+  const int block = (kRowMax / (32 * C.vec) + 1) * 32;
+  SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, block, smem));
   if (per_sm < 1) return SK_ERR_UNSUPPORTED;
   Args a{};
   a.out = out;
@@ -563,7 +621,7 @@ int sobel_frames_tma(const uint8_t* in, long long in_pitch, long long in_fs, uin
   a.rows = (int)rows;
   a.cols = (int)cols;
   a.ws = (int)ws;
-  a.nwa = (int)((cols + 255) / 256);
+  a.nwa = (int)((cols + 32 * C.vec - 1) / (32 * C.vec));
   a.k2 = k2ptr[dslot];
   a.hint = hint_ns();
   long long grid = (long long)device_sms(dev) * per_sm;
@@ -571,7 +629,7 @@ int sobel_frames_tma(const uint8_t* in, long long in_pitch, long long in_fs, uin
   if (grid > (a.total + min_rows - 1) / min_rows) grid = (a.total + min_rows - 1) / min_rows;
   if (grid < 1) grid = 1;
   SK_CUDA(cudaMemsetAsync(sums, 0, sizeof(long long) * frames, s));
-  C.fn<<<(int)grid, BLOCK, smem, s>>>(tm, a);
+  fn<<<(int)grid, block, smem, s>>>(tm, a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "sobel_frames (TMA) launch");
   return SK_OK;

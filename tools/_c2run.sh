@@ -1,2 +1,4 @@
-timeout 600 python -m pytest tests/test_gpu_sobel_tma.py tests/test_gpu_large.py -k "sobel" tests/test_gpu_apps.py -q -x -p no:cacheprovider 2>&1 | tail -2
-for c in 0 1 5 6; do SK_TMA_CFG=$c python tools/sobel_sweep.py; done
+timeout 600 python -m pytest tests/test_gpu_sobel_tma.py tests/test_gpu_large.py tests/test_gpu_apps.py -q -x -p no:cacheprovider 2>&1 | tail -2
+timeout 300 python bench.py --workload c2 --steps 5 --warmup 3 > gpurun_out/r02_bench_c2.json 2> gpurun_out/r02_bench_c2.err; tail -c 600 gpurun_out/r02_bench_c2.json
+FRAMES=512 timeout 600 ncu --set full --clock-control none --import-source on -k regex:sobel_tma -s 1 -c 1 -o gpurun_out/r02_sobel_tma python tools/sobel_sweep.py > gpurun_out/ncu_c2.log 2>&1; tail -1 gpurun_out/ncu_c2.log
+cuobjdump -sass paper_1609_04567_b200/_lib/libstencilkit_b200.so | grep -c UTMALDG
