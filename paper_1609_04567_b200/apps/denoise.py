@@ -15,6 +15,7 @@ W restoration loops are in flight on the GPU at once.
 
 from __future__ import annotations
 
+import os
 import threading
 import time
 
@@ -30,7 +31,8 @@ from ..grid import Grid, GridError
 from ..loop import Condition, DeviceCond, stop_after
 from ..partition import DeploymentMode, WorkerGroup, parallel_loop
 from ..patterns import Combinator, DeviceKernel, DeviceUnsupported, ElementalFn, abs_change
-from ..streams import Stage, StreamReport, ordered_farm, pipeline, run_stream
+from ..streams import (Stage, StageStats, StreamError, StreamReport, ordered_farm, pipeline,
+                       run_stream)
 
 _SEARCH_STEPS = math.ceil(math.log((255.0 - 0.0) / 0.25) / math.log(1.5))  # 18, as the reference
 
@@ -267,18 +269,48 @@ def restore_frames(frames, masks, cfg: Optional[RestoreConfig] = None, stream=No
 # ---------------------------------------------------------------- inputs, video
 
 
+def salt_pepper_array(a: np.ndarray, level: float, seed: int = 42):
+    """numpy form of `salt_pepper` (same PCG64 stream): (noisy, hit) arrays."""
+    if not 0 <= level <= 1:
+        raise GridError(f"noise level must be in [0, 1], got {level}")
+    rng = np.random.default_rng(seed)
+    hit = rng.random(a.shape) < level
+    salt = rng.random(a.shape) < 0.5
+    return np.where(hit, np.where(salt, 255, 0), a), hit
+
+
 def salt_pepper(img: Grid, level: float, seed: int = 42):
     """Corrupt a fraction of pixels to 0/255 with numpy's PCG64, exactly as the
     reference (apps/denoise.py:295-304); returns (noisy, mask).  Host-side
     input synthesis: identical streams of random numbers require numpy."""
-    if not 0 <= level <= 1:
-        raise GridError(f"noise level must be in [0, 1], got {level}")
-    rng = np.random.default_rng(seed)
-    a = img.to_array()
-    hit = rng.random(a.shape) < level
-    salt = rng.random(a.shape) < 0.5
-    noisy = np.where(hit, np.where(salt, 255, 0), a)
+    noisy, hit = salt_pepper_array(img.to_array(), level, seed)
     return Grid.from_array(noisy), Grid.from_array(hit.astype(np.int64))
+
+
+class _HostRing:
+    """Pinned host frames the restore lanes read results back into (the
+    `host_buffers` mode of video_restore_pipeline): a frame's buffer returns
+    to the pool when the writer is done with it, so steady state allocates
+    nothing and every device->host copy is one DMA into pinned memory.  The
+    pool grows on demand (never blocks: out-of-order completions waiting for
+    the ordered writer hold buffers too)."""
+
+    def __init__(self):
+        self.lock = threading.Lock()
+        self.free = []
+
+    def get(self, shape, dtype):
+        import torch
+
+        with self.lock:
+            for i, t in enumerate(self.free):
+                if tuple(t.shape) == tuple(shape) and t.dtype == dtype:
+                    return self.free.pop(i)
+        return torch.empty(tuple(shape), dtype=dtype, pin_memory=True)
+
+    def put(self, t):
+        with self.lock:
+            self.free.append(t)
 
 
 class _RestoreBatcher:
@@ -379,11 +411,189 @@ class _RestoreBatcher:
         self.thread.join(timeout=30)
 
 
+def _host_u8(img):
+    """A frame for the batched farm: a uint8 torch tensor (host or device),
+    range-checked like amf_detect's input (no copy for uint8 tensors)."""
+    import torch
+
+    from ..partition import _u8_from
+
+    if not isinstance(img, Grid):
+        raise GridError(f"frames must be grids, got {type(img).__name__}")
+    if img.ndim != 2:
+        raise GridError("detection expects a 2D image")
+    t0 = img._t if img._src == "t" else None
+    if t0 is not None and t0.dtype == torch.uint8:
+        return t0
+    if img.is_device:
+        return _u8_from(img, "amf", 0, 255, img._t.device)
+    return _u8_from(img, "amf", 0, 255, torch.device("cpu"))
+
+
+def _batched_restore_stream(frames, cfg, writer, loader, devices, host_buffers,
+                            batch) -> StreamReport:
+    """read -> detect -> ordered_farm(restore) -> write for the 1:1 case with
+    fused detection, farmed at batch granularity: a feeder thread reads and
+    validates frames and groups up to `batch` consecutive same-shape frames;
+    two workers per GPU each upload a batch on their own stream, detect it
+    (amf_frames) and restore it (restore_frames: every frame its own loop in
+    one persistent launch) while the other worker's batch is read back and
+    the next one uploaded; the calling thread hands the frames to `writer`
+    in stream order.  Same report contract as run_stream: a frame whose
+    read / detection input / restore / write fails is a failure of that item
+    only; a failing source raises StreamError after the run drains."""
+    import queue
+
+    import torch
+
+    started = time.perf_counter()
+    rep = StreamReport()
+    names = ("read", "detect", "restore", "write")
+    stats = {n: StageStats(n) for n in names}
+    lock = threading.Lock()
+    ring = _HostRing() if (host_buffers and writer is not None) else None
+    jobs = queue.Queue(maxsize=2 * len(devices))
+    done = {}  # batch index -> list of (seq, grid or None, error or None)
+    cv = threading.Condition()
+    fed = [0]
+    source_error = [None]
+    nbatches = [None]
+
+    def busy(name, dt, n=1):
+        with lock:
+            stats[name].items += n
+            stats[name].busy_s += dt
+
+    def feeder():
+        bi, cur, shape = 0, [], None
+
+        def flush():
+            nonlocal bi, cur, shape
+            if cur:
+                jobs.put((bi, cur))
+                bi += 1
+            cur, shape = [], None
+
+        try:
+            for seq, item in enumerate(frames):
+                fed[0] = seq + 1
+                t0 = time.perf_counter()
+                try:
+                    img = loader(item) if loader is not None else item
+                    busy("read", time.perf_counter() - t0)
+                    t = _host_u8(img)
+                    entry = (seq, t, None)
+                except Exception as e:  # poisons this frame only
+                    entry = (seq, None, e)
+                if entry[1] is not None and shape is not None and tuple(entry[1].shape) != shape:
+                    flush()
+                if entry[1] is not None:
+                    shape = tuple(entry[1].shape)
+                cur.append(entry)
+                if len(cur) >= batch:
+                    flush()
+        except Exception as e:
+            source_error[0] = e
+        finally:
+            flush()
+            with cv:
+                nbatches[0] = bi
+                cv.notify_all()
+            for _ in range(2 * len(devices)):
+                jobs.put(None)
+
+    def worker(dev):
+        torch.cuda.set_device(dev)
+        stream = torch.cuda.Stream(device=dev)
+        while True:
+            job = jobs.get()
+            if job is None:
+                return
+            bi, entries = job
+            res = [(seq, None, err) for seq, _t, err in entries if err is not None]
+            good = [(seq, t) for seq, t, err in entries if err is None]
+            if good:
+                t0 = time.perf_counter()
+                try:
+                    with torch.cuda.stream(stream):
+                        H, W = good[0][1].shape
+                        d = torch.empty((len(good), H, W), dtype=torch.uint8, device=dev)
+                        for i, (_seq, t) in enumerate(good):
+                            d[i].copy_(t, non_blocking=True)
+                        masks, _ = amf_frames(d, cfg.amf_wmax, stream=stream)
+                        t1 = time.perf_counter()
+                        outs, _reps = restore_frames(d, masks, cfg, stream=stream)
+                        t2 = time.perf_counter()
+                        grids = []
+                        for o in outs:
+                            if ring is not None:
+                                h = ring.get(o.shape, o.dtype)
+                                h.copy_(o, non_blocking=True)
+                                g = Grid.from_tensor(h, logical_dtype=np.float64)
+                                grids.append((g, h))
+                            else:
+                                grids.append((Grid.from_tensor(o, logical_dtype=np.float64), None))
+                        stream.synchronize()
+                    if ring is None and writer is not None:
+                        for g, _h in grids:
+                            g.prefetch_host()
+                    busy("detect", t1 - t0, len(good))
+                    busy("restore", t2 - t1, len(good))
+                    res += [(seq, g, None, h) for (seq, _t), (g, h) in zip(good, grids)]
+                except Exception as e:  # the batch's frames all fail with it
+                    res += [(seq, None, e) for seq, _t in good]
+            res.sort(key=lambda r: r[0])
+            with cv:
+                done[bi] = res
+                cv.notify_all()
+
+    threads = [threading.Thread(target=feeder, daemon=True)]
+    for d in devices:
+        threads += [threading.Thread(target=worker, args=(d,), daemon=True) for _ in range(2)]
+    for t in threads:
+        t.start()
+    nxt = 0
+    while True:
+        with cv:
+            while nxt not in done and not (nbatches[0] is not None and nxt >= nbatches[0]):
+                cv.wait()
+            if nxt not in done:
+                break
+            res = done.pop(nxt)
+        nxt += 1
+        for r in res:
+            seq, g, err = r[0], r[1], r[2]
+            if err is not None:
+                rep.failures.append((seq, err))
+                continue
+            t0 = time.perf_counter()
+            try:
+                if writer is not None:
+                    writer(g)
+                rep.items_out += 1
+            except Exception as e:  # a failing write poisons its frame only
+                rep.failures.append((seq, e))
+            finally:
+                busy("write", time.perf_counter() - t0)
+                if len(r) > 3 and r[3] is not None:
+                    ring.put(r[3])
+    for t in threads:
+        t.join()
+    rep.items_in = fed[0]
+    rep.wall_s = time.perf_counter() - started
+    rep.stages = [stats[n] for n in names]
+    if source_error[0] is not None:
+        e = source_error[0]
+        raise StreamError(f"stream source failed: {e!r}") from e
+    return rep
+
+
 def video_restore_pipeline(frames: Iterable, *, width: int = 1, partitions: int = 1,
                            mode=DeploymentMode.ONE_TO_ONE, cfg: Optional[RestoreConfig] = None,
                            writer: Optional[Callable] = None, loader: Optional[Callable] = None,
                            mask_writer: Optional[Callable] = None,
-                           devices: Optional[list] = None) -> StreamReport:
+                           devices: Optional[list] = None,
+                           host_buffers: bool = False) -> StreamReport:
     """read -> detect -> ordered_farm(restore, width) -> write
     (apps/denoise.py:307-368), over one GPU or several.
 
@@ -397,7 +607,14 @@ def video_restore_pipeline(frames: Iterable, *, width: int = 1, partitions: int 
     device-side farm of loops, restore_frames).  With a `mask_writer` the
     detector runs per frame in the detect stage instead, so masks are written
     in stream order.  1:n deployment: each lane runs restore_regularize over
-    `partitions` row blocks of its frame on its GPU."""
+    `partitions` row blocks of its frame on its GPU.
+
+    `host_buffers=True` (with a `writer`): each restored frame is read back by
+    one DMA into a recycled pinned host frame and handed to the writer as a
+    host Grid over it (`g.tensor()` is that pinned tensor, no copy); the
+    buffer is reused once the writer returns, so a writer that keeps a frame
+    must copy it (`g.to_array()`).  Default: every frame is a fresh grid, as
+    in the reference."""
     import torch
 
     from ..partition import _u8_from
@@ -414,9 +631,20 @@ def video_restore_pipeline(frames: Iterable, *, width: int = 1, partitions: int 
     devices = [int(getattr(d, "index", d)) for d in devices]
     batched = eff == 1
     fused_detect = batched and mask_writer is None
+    if fused_detect and not os.environ.get("SK_LANE_FARM"):
+        # the farm at batch granularity: the device-side farm of loops
+        # (restore_frames) fed by two workers per GPU, frames written in order
+        per_dev = -(-width // len(devices))
+        cap = int(os.environ.get("SK_BATCH_CAP", "0")) or max(1, min(64, -(-per_dev // 2)))
+        return _batched_restore_stream(frames, cfg, writer, loader, devices, host_buffers, cap)
     per_dev = -(-width // len(devices))
-    batchers = ({d: _RestoreBatcher(cfg, per_dev, detect=fused_detect, device=d)
+    # a GPU's lanes fill two batches: one restores while the other's frames
+    # are read back and the next frames uploaded (SK_BATCH_CAP overrides)
+    cap = int(os.environ.get("SK_BATCH_CAP", "0")) or max(1, -(-per_dev // 2))
+    batchers = ({d: _RestoreBatcher(cfg, cap, detect=fused_detect, device=d)
                  for d in dict.fromkeys(devices)} if batched else {})
+    ring = _HostRing() if (host_buffers and writer is not None) else None
+    held, held_lock = {}, threading.Lock()  # id(grid handed on) -> its pinned frame
 
     def detect_fn(img: Grid):
         if img.ndim != 2:
@@ -464,6 +692,16 @@ def video_restore_pipeline(frames: Iterable, *, width: int = 1, partitions: int 
                     out, _rep = restore_regularize(
                         img, mask, cfg, partitions=eff,
                         mode=mode if eff > 1 else DeploymentMode.ONE_TO_ONE, group=grp)
+                if ring is not None:
+                    # one DMA into a recycled pinned frame, on the lane's stream
+                    t = out.tensor()
+                    h = ring.get(t.shape, t.dtype)
+                    h.copy_(t, non_blocking=True)
+                    lane.stream.synchronize()
+                    g = Grid.from_tensor(h, logical_dtype=np.float64)
+                    with held_lock:
+                        held[id(g)] = h
+                    return g
                 if writer is not None:
                     # read the frame back here, in parallel across lanes; the
                     # ordered writer's to_array() then takes it over
@@ -484,6 +722,11 @@ def video_restore_pipeline(frames: Iterable, *, width: int = 1, partitions: int 
     else:
         def write_fn(g):
             writer(g)
+            if ring is not None:  # the writer is done with the pinned frame
+                with held_lock:
+                    h = held.pop(id(g), None)
+                if h is not None:
+                    ring.put(h)
             return g
 
         write = Stage(write_fn, name="write")

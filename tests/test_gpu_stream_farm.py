@@ -119,3 +119,77 @@ def test_video_pipeline_mask_writer_and_1n():
                            writer=lambda g: got.append(g.to_array()))
     for i in range(2):
         assert sha(got[i]) == meta[str(i)]["sha"]
+
+
+def test_video_pipeline_host_buffers_recycle_pinned_frames():
+    """host_buffers=True: results arrive by DMA in recycled pinned host frames
+    (pinned uint8 frames in); each frame, copied by the writer while it owns
+    the buffer, is the reference's (golden_c5 SHA-256), in stream order."""
+    import torch
+
+    meta = json.load(open(GOLD))["frames"]
+    from paper_1609_04567_b200.apps import video_restore_pipeline
+
+    k = 12
+    host = torch.from_numpy(np.stack([c5_frame(i).astype(np.uint8) for i in range(k)])).pin_memory()
+    frames = [sk.Grid.from_tensor(host[i]) for i in range(k)]
+    got, ptrs = [], set()
+
+    def writer(g):
+        t = g.tensor()
+        assert t.is_pinned() and not t.is_cuda
+        ptrs.add(t.data_ptr())
+        got.append(g.to_array())
+
+    video_restore_pipeline(frames, width=3, writer=writer, host_buffers=True)
+    assert len(got) == k
+    for i in range(k):
+        assert sha(got[i]) == meta[str(i)]["sha"], i
+    assert len(ptrs) < k  # buffers were reused
+
+
+def test_video_pipeline_batched_farm_failures_shapes_loader(monkeypatch):
+    """The batch-granular farm (default for 1:1 with fused detection) keeps
+    the stream contract of the lane farm (SK_LANE_FARM=1): stream order,
+    a bad frame (pixel out of range), a failing loader call and a failing
+    write poison only their own item, shape changes split batches, and
+    items_in == items_out + len(failures)."""
+    from paper_1609_04567_b200.apps import salt_pepper, video_restore_pipeline
+
+    def frame(i, h, w):
+        r = np.arange(h)[:, None]
+        c = np.arange(w)[None, :]
+        return salt_pepper(sk.Grid.from_array(((r * 3 + c * 2 + i) % 200 + 20).astype(np.int64)),
+                           0.2, seed=70 + i)[0]
+
+    src = [frame(0, 40, 50), frame(1, 40, 50), "bad-load", frame(3, 30, 20),
+           sk.Grid.from_array(np.full((40, 50), 300, dtype=np.int64)), frame(5, 40, 50),
+           frame(6, 40, 50), frame(7, 30, 20)]
+
+    def loader(x):
+        if isinstance(x, str):
+            raise ValueError("cannot load")
+        return x
+
+    results = {}
+    for lane_farm in ("", "1"):
+        if lane_farm:
+            monkeypatch.setenv("SK_LANE_FARM", "1")
+        else:
+            monkeypatch.delenv("SK_LANE_FARM", raising=False)
+        got = []
+
+        def writer(g):
+            if len(got) == 3:
+                got.append(None)
+                raise RuntimeError("disk full")
+            got.append(g.to_array())
+
+        rep = video_restore_pipeline(src, width=4, loader=loader, writer=writer)
+        assert rep.items_in == 8 and rep.items_in == rep.items_out + len(rep.failures)
+        results[lane_farm] = (got, sorted(s for s, _e in rep.failures))
+    (g0, f0), (g1, f1) = results[""], results["1"]
+    assert f0 == f1 == [2, 4, 5]  # the load, the out-of-range frame, the failed write
+    assert len(g0) == len(g1)
+    for a, b in zip(g0, g1):
+        assert (a is None and b is None) or np.array_equal(a, b)
