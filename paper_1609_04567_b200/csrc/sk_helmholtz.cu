@@ -611,8 +611,11 @@ __global__ void __launch_bounds__(BLOCK, 1) helm_resident(const __grid_constant_
     u[r] = (active && r < R) ? ldgN<T, VEC>(src + (long long)(r0 + r) * g.src_pitch + col) : zeroN<T, VEC>();
     if (active && r < R) {
       const VecN<T, VEC> fv = ldgN<T, VEC>(env + (long long)(r0 + r) * g.env_pitch + col);
+      // only the row's own columns: s_f rows are `cols` long, so a lane's
+      // vector tail past the last column would land on the next row's head
 #pragma unroll
-      for (int e = 0; e < VEC; ++e) s_f[r * cols + col + e] = fv.v[e];
+      for (int e = 0; e < VEC; ++e)
+        if (e < nvalid) s_f[r * cols + col + e] = fv.v[e];
     }
   }
   VecN<T, VEC> up = (active && !(r0 == 0 && top_zero)) ? ldgN<T, VEC>(src + (long long)(r0 - 1) * g.src_pitch + col)

@@ -78,7 +78,8 @@ class Grid:
     ints do.
     """
 
-    __slots__ = ("dims", "_list", "_arr", "_t", "_ldtype", "_src", "value_range", "_fresh")
+    __slots__ = ("dims", "_list", "_arr", "_t", "_ldtype", "_src", "value_range", "_fresh",
+                 "_pending")
 
     def __init__(self, dims: Sequence[int], data: Sequence[Any]):
         dims = _check_dims(dims)
@@ -251,13 +252,60 @@ class Grid:
                 self._arr = np.asarray(self._list).reshape(self.dims)
         return self._arr
 
-    def prefetch_host(self) -> None:
-        """Read a device grid back now (on the calling thread), so the next
-        to_array() hands over that fresh array instead of copying then --
-        stream replicas call this so the D2H copies of many frames run in
-        parallel rather than in the ordered writer.  No effect on host grids."""
-        if self._src == "t" and self._arr is None and self._t is not None and self._t.is_cuda:
+    def prefetch_host(self, out: np.ndarray = None) -> None:
+        """Read a device grid back ahead of to_array().
+
+        Without `out`: now, on the calling thread (stream replicas call this
+        so the D2H copies of many frames run in parallel rather than in the
+        ordered writer).  With `out` (a host array of the grid's shape and
+        dtype, ideally over pinned memory): asynchronously, one DMA on a copy
+        stream ordered after the work that produced the grid; the next
+        to_array() waits for it and returns `out`.  No effect on host grids."""
+        if not (self._src == "t" and self._arr is None and self._t is not None and self._t.is_cuda):
+            return
+        if out is None:
             self._fresh = self.to_array()
+            return
+        torch = _torch()
+        t = self._t
+        if tuple(out.shape) != tuple(self.dims) or out.dtype != _numpy_dtype_of(t.dtype):
+            raise GridError(f"prefetch_host: out must be {self.dims} {_numpy_dtype_of(t.dtype)}")
+        cs = _copy_stream(t.device, "down")
+        cs.wait_stream(torch.cuda.current_stream(t.device))
+        with torch.cuda.stream(cs):
+            torch.from_numpy(out).copy_(t if t.is_contiguous() else t.contiguous(),
+                                        non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(cs)
+        t.record_stream(cs)
+        self._fresh = (out, ev)
+
+    def prefetch_device(self, device="cuda") -> "Grid":
+        """Start uploading a host grid to `device` now, asynchronously, on a
+        copy stream; the kernels that consume the grid later wait for the
+        copy on their own stream (no host synchronisation).  A host grid over
+        a pinned tensor is one DMA; other host storage streams through the
+        pinned staging chunks.  Returns self."""
+        torch = _torch()
+        dev = torch.device(device)
+        if dev.type != "cuda" or self.is_device or getattr(self, "_pending", None) is not None:
+            return self
+        if self._src == "t" and self._t is not None and self._t.is_pinned():
+            src = self._t.contiguous()
+        else:
+            a = self._host()
+            if a.dtype == object:
+                raise GridError("grid elements are not numeric")
+            src = torch.from_numpy(np.ascontiguousarray(a))
+            if src.numel() * src.element_size() >= (8 << 20):
+                src = src.pin_memory()  # one pinned copy, then the DMA is asynchronous
+        cs = _copy_stream(dev, "up")
+        with torch.cuda.stream(cs):
+            d = src.to(dev, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(cs)
+        self._pending = (d, ev, src)
+        return self
 
     def to_array(self, dtype=None) -> np.ndarray:
         """Fresh host numpy array of the elements (grid.py:158-162)."""
@@ -265,6 +313,11 @@ class Grid:
         if fresh is not None:
             # a prefetched copy nobody else holds: hand it over (once)
             self._fresh = None
+            if isinstance(fresh, tuple):  # asynchronous read into the caller's array
+                fresh, ev = fresh
+                ev.synchronize()
+            if self._ldtype is not None and fresh.dtype != self._ldtype:
+                return fresh.astype(self._ldtype if dtype is None else dtype)
             return fresh.astype(dtype) if dtype is not None else fresh
         if self._src == "t" and self._arr is None and self._t is not None and self._t.is_cuda:
             # read straight from the device into a fresh array (no cached
@@ -280,6 +333,19 @@ class Grid:
         """The grid as a torch tensor (on `device` if given), cached; no copy
         when it already lives there."""
         torch = _torch()
+        pend = getattr(self, "_pending", None)
+        if pend is not None and device is not None and torch.device(device).type == "cuda":
+            d, ev, _src = pend
+            if d.device == _cuda_index(torch, device):
+                # a prefetched upload: the consuming stream waits for the copy
+                cur = torch.cuda.current_stream(d.device)
+                cur.wait_event(ev)
+                d.record_stream(cur)
+                self._pending = None
+                self._t = d
+                if self._src != "list":
+                    self._src = "t"
+                return d.to(dtype) if dtype is not None and d.dtype != dtype else d
         t = self._t
         if t is None:
             a = self._host()
@@ -353,6 +419,27 @@ def _copy_pool():
 
         _COPY_POOL = ThreadPoolExecutor(8, thread_name_prefix="sk-hostcopy")
     return _COPY_POOL
+
+
+_COPY_STREAMS = {}
+
+
+def _copy_stream(device, kind):
+    """Side streams per device: "up" for prefetch_device, "down" for
+    prefetch_host (separate, so uploads and read-backs use both PCIe
+    directions at once)."""
+    torch = _torch()
+    dev = torch.device(device)
+    idx = dev.index if dev.index is not None else torch.cuda.current_device()
+    s = _COPY_STREAMS.get((idx, kind))
+    if s is None:
+        s = _COPY_STREAMS.setdefault((idx, kind), torch.cuda.Stream(device=idx))
+    return s
+
+
+def _cuda_index(torch, device):
+    dev = torch.device(device)
+    return dev if dev.index is not None else torch.device("cuda", torch.cuda.current_device())
 
 
 def _host_copy(dst: np.ndarray, src: np.ndarray) -> None:

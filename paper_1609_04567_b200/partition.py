@@ -437,6 +437,10 @@ def _u8_from(grid: Grid, what: str, lo: int, hi: int, dev):
         raise GridError(f"{what} expects integer pixels, got dtype {sd}")
     rng = grid.value_range
     known = rng is not None and rng[0] >= lo and rng[1] <= hi
+    if getattr(grid, "_pending", None) is not None:  # a prefetched upload
+        t = grid.tensor(device=dev)
+        if t.dtype == torch.uint8 and hi >= 255:
+            return t
     t0 = grid._t if grid._src == "t" else None
     if t0 is not None and not t0.is_cuda and t0.dtype == torch.uint8 and hi >= 255:
         # a uint8 host tensor needs no range check; from pinned memory the

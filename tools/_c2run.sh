@@ -1,2 +1,2 @@
-timeout 900 python bench.py --workload c5 --steps 2 --warmup 1 > gpurun_out/r02_bench_c5.json 2> gpurun_out/r02_bench_c5.err; tail -c 1400 gpurun_out/r02_bench_c5.json; tail -3 gpurun_out/r02_bench_c5.err
-timeout 900 python bench.py --workload c3 --steps 3 --warmup 2 > gpurun_out/r02_bench_c3.json 2> gpurun_out/r02_bench_c3.err; tail -c 300 gpurun_out/r02_bench_c3.json; tail -3 gpurun_out/r02_bench_c3.err
+python tools/_dbg_prefetch.py
+timeout 900 python -m pytest tests/test_gpu_resident_widths.py tests/test_gpu_prefetch.py -q -p no:cacheprovider 2>&1 | tail -8
