@@ -54,7 +54,9 @@ extern "C" {
 #define SK_KERNEL_HELMHOLTZ 1 /* params: ax, ay, b, keep, relax           */
 #define SK_KERNEL_SOBEL 2     /* u8 in/out, off-image reads = centre      */
 #define SK_KERNEL_AMF 3       /* params: wmax; u8 in, u8 0/1 out          */
-#define SK_KERNEL_RESTORE 4   /* params: beta, phi_eps; f64 work, u8 mask */
+#define SK_KERNEL_RESTORE 4   /* params: beta, phi_eps[, pa, pb]; f64 work, u8 mask.
+                                 pb > 0: the run computes partitions [pa, pb) only
+                                 (a frame split across runs / GPUs) */
 #define SK_KERNEL_LIFE 5      /* u8 0/1 board                             */
 #define SK_KERNEL_JIT 6       /* user elemental function (sk_jit_compile)  */
 
@@ -192,6 +194,15 @@ int sk_run_set_peers(sk_run* run, const sk_peers* peers);
  * launch `seq` (its flag word here >= seq).  The mailbox row to combine is
  * mail[rank] + (seq & 1) * world. */
 int sk_run_peer_wait(sk_run* run, int64_t seq);
+
+/* Halo exchange between two runs of the same geometry that split one grid
+ * (partition.py:247-262; e.g. a frame restored 1:n across GPUs, each run
+ * computing its own partitions over a full-size replica): copy rows
+ * [row_lo, row_hi) of iteration `it`'s result buffer -- and, for restore
+ * runs, of its change-flag plane -- from `src` to `dst` (any devices:
+ * peer copies over NVLink).  Enqueued on src's stream after iteration `it`;
+ * dst's stream waits for the copy before its next launch.  No host sync. */
+int sk_run_exchange_rows(sk_run* dst, sk_run* src, int64_t row_lo, int64_t row_hi, int64_t it);
 
 /* Device memory that other processes can map (cudaMalloc + CUDA IPC):
  * allocate (zeroed), export a 64-byte handle, map a peer's handle, unmap,

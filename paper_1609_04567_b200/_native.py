@@ -32,7 +32,7 @@ EXPORTS = (
     "sk_run_launches", "sk_run_destroy", "sk_verify_div_f32", "sk_sobel_frames",
     "sk_amf_frames", "sk_jit_compile", "sk_jit_log", "sk_jit_cubin_size", "sk_jit_cubin", "sk_jit_destroy",
     "sk_run_begin_jit", "sk_run_error",
-    "sk_run_set_peers", "sk_run_peer_wait", "sk_ipc_alloc", "sk_ipc_handle", "sk_ipc_open",
+    "sk_run_set_peers", "sk_run_peer_wait", "sk_run_exchange_rows", "sk_ipc_alloc", "sk_ipc_handle", "sk_ipc_open",
     "sk_ipc_close", "sk_ipc_free",
 )
 
@@ -127,6 +127,7 @@ def _declare(lib):
         "sk_run_error": [P, C.POINTER(I32), C.POINTER(I64), C.POINTER(I64)],
         "sk_run_set_peers": [P, C.POINTER(sk_peers)],
         "sk_run_peer_wait": [P, I64],
+        "sk_run_exchange_rows": [P, P, I64, I64, I64],
         "sk_ipc_alloc": [I64, C.POINTER(P)],
         "sk_ipc_handle": [P, C.c_char_p],
         "sk_ipc_open": [C.c_char_p, C.POINTER(P)],

@@ -181,15 +181,24 @@ def _flagged_count(noise: Grid) -> int:
 
 def restore_regularize(img: Grid, noise: Grid, cfg: Optional[RestoreConfig] = None,
                        *, partitions: int = 1, mode=DeploymentMode.ONE_TO_N,
-                       group: Optional[WorkerGroup] = None):
+                       group: Optional[WorkerGroup] = None, devices: Optional[list] = None):
     """Restore the flagged pixels; returns (fp64 grid, LoopReport)
-    (apps/denoise.py:262-288)."""
+    (apps/denoise.py:262-288).
+
+    `devices` (several GPUs, 1:n): the `partitions` row blocks are spread
+    over these GPUs (contiguous blocks per GPU) and restored together, the
+    boundary rows exchanged every iteration (_restore_split)."""
     cfg = cfg or RestoreConfig()
     if img.ndim != 2:
         raise GridError("restoration expects a 2D image")
     if noise.dims != img.dims:
         raise GridError(f"noise map dims {noise.dims} do not match image {img.dims}")
     _check_mask(noise)
+    if devices is not None and len(devices) > 1:
+        if partitions < len(devices):
+            raise GridError(f"{len(devices)} GPUs need at least as many partitions, got {partitions}")
+        return _restore_split(img, noise, cfg, partitions, [int(getattr(d, "index", d))
+                                                             for d in devices])
     # value / max(flagged, 1) < tol: on the device the run counts the flagged
     # pixels itself; a host-evaluated loop counts them once, on first use
     denom = []
@@ -204,6 +213,95 @@ def restore_regularize(img: Grid, noise: Grid, cfg: Optional[RestoreConfig] = No
         mode = DeploymentMode.ONE_TO_ONE
     return parallel_loop(mode, partitions, 1, restore_kernel(cfg), _float_sum(), cond, img,
                          env=noise, delta=abs_change(), indexed=True, group=group)
+
+
+def _restore_split(img: Grid, noise: Grid, cfg: RestoreConfig, P: int, devices: list):
+    """restore_regularize with its P row partitions spread over several GPUs
+    (the paper's 1:n deployment of one frame across a GPU pair, Table 3).
+
+    One run per partition, on devices[p * len(devices) // P], each over a
+    full-size replica of the frame but computing only its own partition
+    (SK_KERNEL_RESTORE params pa, pb).  After every iteration the rows at
+    each partition boundary (values and change flags) are copied to the
+    neighbouring partition's run (sk_run_exchange_rows: a peer copy,
+    stream-ordered before the neighbour's next sweep) -- the reference's
+    halo_exchange (partition.py:247-262).  Each run's value is its own
+    partition's sum; the host folds them in partition order from 0.0 and
+    applies value / max(flagged, 1) < tol (apps/denoise.py:262-288), exactly
+    the single-GPU engine's fold, so grids, iteration counts and values are
+    bit-identical to a one-GPU restore with the same partitions."""
+    import torch
+
+    from ..loop import LoopReport
+    from ..partition import _split_ranges, _u8_from, model_ledger
+
+    lib = N.require_cuda()
+    H, W = img.dims
+    if P > H or P > 64:
+        raise GridError(f"cannot split {H} rows across {P} partitions")
+    ranges = _split_ranges(H, P)
+    denom = max(_flagged_count(noise), 1)
+    Wp = -(-W // 2) * 2  # fp64 rows in whole 16-byte vectors
+    runs = []
+    try:
+        for p in range(P):
+            dev = devices[p * len(devices) // P]
+            with torch.cuda.device(dev):
+                st = torch.cuda.Stream(device=dev)
+                with torch.cuda.stream(st):
+                    d = torch.device("cuda", dev)
+                    src = torch.zeros((H, Wp), dtype=torch.float64, device=d)
+                    src[:, :W] = img.tensor(device=d).to(torch.float64)
+                    env = torch.zeros((H, -(-W // 16) * 16), dtype=torch.uint8, device=d)
+                    env[:, :W] = _u8_from(noise, "noise map", 0, 1, d)
+                    bufs = [torch.empty((H, Wp), dtype=torch.float64, device=d) for _ in range(2)]
+                    pl = N.sk_plan()
+                    pl.kernel, pl.dtype = N.SK_KERNEL_RESTORE, N.SK_F64
+                    pl.rows, pl.cols, pl.partitions = H, W, P
+                    pl.reduce_op, pl.delta_op = N.SK_REDUCE_SUM, N.SK_DELTA_ABS
+                    pl.identity = 0.0
+                    pl.params[0], pl.params[1] = cfg.beta, cfg.phi_eps
+                    pl.params[2], pl.params[3] = float(p), float(p + 1)
+                    h = C.c_void_p()
+                    N.check(lib.sk_run_begin(C.byref(pl), C.c_void_p(src.data_ptr()), Wp,
+                                             C.c_void_p(env.data_ptr()), env.stride(0),
+                                             C.c_void_p(bufs[0].data_ptr()),
+                                             C.c_void_p(bufs[1].data_ptr()), Wp,
+                                             N.stream_handle(st), C.byref(h)))
+                    runs.append({"h": h, "dev": dev, "stream": st, "keep": (src, env),
+                                 "bufs": bufs})
+        t, value, stopped = 0, 0.0, False
+        v = C.c_double()
+        while True:
+            t += 1
+            for r in runs:
+                N.check(lib.sk_run_launch(r["h"], 1))
+            for p in range(P - 1):  # boundary rows of iteration t, both ways
+                lo_next = ranges[p + 1][0]
+                N.check(lib.sk_run_exchange_rows(runs[p + 1]["h"], runs[p]["h"], lo_next - 1,
+                                                 lo_next, t))
+                N.check(lib.sk_run_exchange_rows(runs[p]["h"], runs[p + 1]["h"], lo_next,
+                                                 lo_next + 1, t))
+            value = 0.0
+            for r in runs:  # partition order, from the identity
+                N.check(lib.sk_run_value(r["h"], t, C.byref(v)))
+                value = value + v.value
+            if value / denom < cfg.tol:
+                stopped = True
+                break
+            if t >= cfg.max_iterations:
+                break
+        home = torch.device("cuda", devices[0])
+        out = torch.empty((H, W), dtype=torch.float64, device=home)
+        for (lo, hi), r in zip(ranges, runs):
+            r["stream"].synchronize()
+            out[lo:hi].copy_(r["bufs"][t & 1][lo:hi, :W])
+    finally:
+        for r in runs:
+            N.check(lib.sk_run_destroy(r["h"]))
+    g = Grid.from_tensor(out, logical_dtype=np.float64)
+    return g, LoopReport(iterations=t, final_reduce=value, copies=model_ledger((H, W), P, 1, t),
+                         exhausted=not stopped)
 
 
 def restore_frames(frames, masks, cfg: Optional[RestoreConfig] = None, stream=None):
@@ -593,7 +691,8 @@ def video_restore_pipeline(frames: Iterable, *, width: int = 1, partitions: int 
                            writer: Optional[Callable] = None, loader: Optional[Callable] = None,
                            mask_writer: Optional[Callable] = None,
                            devices: Optional[list] = None,
-                           host_buffers: bool = False) -> StreamReport:
+                           host_buffers: bool = False,
+                           gpus_per_frame: int = 1) -> StreamReport:
     """read -> detect -> ordered_farm(restore, width) -> write
     (apps/denoise.py:307-368), over one GPU or several.
 
@@ -607,7 +706,11 @@ def video_restore_pipeline(frames: Iterable, *, width: int = 1, partitions: int 
     device-side farm of loops, restore_frames).  With a `mask_writer` the
     detector runs per frame in the detect stage instead, so masks are written
     in stream order.  1:n deployment: each lane runs restore_regularize over
-    `partitions` row blocks of its frame on its GPU.
+    `partitions` row blocks of its frame on its GPU -- or, with
+    `gpus_per_frame=g` > 1, across a group of g GPUs (`devices` cut into
+    consecutive groups, lanes round-robin over the groups; boundary rows
+    exchanged over NVLink every iteration): the paper's "2xGPUs 1:2"
+    deployment (Table 3).
 
     `host_buffers=True` (with a `writer`): each restored frame is read back by
     one DMA into a recycled pinned host frame and handed to the writer as a
@@ -629,6 +732,15 @@ def video_restore_pipeline(frames: Iterable, *, width: int = 1, partitions: int 
     if devices is None:
         devices = [torch.cuda.current_device()]
     devices = [int(getattr(d, "index", d)) for d in devices]
+    groups = None
+    if gpus_per_frame > 1:
+        if mode is not DeploymentMode.ONE_TO_N or eff < gpus_per_frame:
+            raise GridError("gpus_per_frame > 1 needs 1:n mode with at least that many partitions")
+        if len(devices) % gpus_per_frame:
+            raise GridError(f"{len(devices)} devices do not split into groups of {gpus_per_frame}")
+        groups = [devices[i:i + gpus_per_frame] for i in range(0, len(devices), gpus_per_frame)]
+        devices = [g[0] for g in groups]  # a lane runs on its group's first GPU
+        group_of = {k: groups[k % len(groups)] for k in range(width)}
     batched = eff == 1
     fused_detect = batched and mask_writer is None
     if fused_detect and not os.environ.get("SK_LANE_FARM"):
@@ -688,6 +800,9 @@ def video_restore_pipeline(frames: Iterable, *, width: int = 1, partitions: int 
                     up.record(lane.stream)
                     out, _rep, done = batchers[lane.device].submit(img, mask, after=up)
                     lane.stream.wait_event(done)
+                elif groups is not None:  # the frame split across the lane's GPU group
+                    out, _rep = restore_regularize(img, mask, cfg, partitions=eff, mode=mode,
+                                                   devices=group_of[lane.index])
                 else:
                     out, _rep = restore_regularize(
                         img, mask, cfg, partitions=eff,

@@ -37,6 +37,7 @@ const KernelOps* helmholtz_ops();
 const KernelOps* life_ops();
 const KernelOps* restore_ops();
 int restore_frame_status(sk_run* r, long long* iters, double* values, int* exhausted);
+unsigned char* restore_chg(sk_run* r, long long it);  // null unless a restore run
 const KernelOps* u8_ops();   // Sobel / Life (sk_u8stencil.cu)
 const KernelOps* amf_ops();  // adaptive-median detection (sk_amf.cu)
 const KernelOps* jit_ops();  // user elemental functions (sk_jit.cu)

@@ -336,7 +336,7 @@ __global__ void flag_scatter(const unsigned char* mask, long long mpitch, int ro
 // partition p's flagged pixels start at lower_bound(list, part_row[p] * cols);
 // then one thread turns the offsets into per-partition chunk ranges
 __global__ void list_bounds(const int* list, const int* n_ptr, const int* part_row, int nparts,
-                            int cols, int* off, int* pchunk) {
+                            int cols, int* off, int* pchunk, int pa, int pb) {
   const int p = threadIdx.x;
   const int n = *n_ptr;
   if (p < nparts) {
@@ -356,7 +356,9 @@ __global__ void list_bounds(const int* list, const int* n_ptr, const int* part_r
     int acc = 0;
     pchunk[0] = 0;
     for (int i = 0; i < nparts; ++i) {
-      acc += (off[i + 1] - off[i] + kCh - 1) / kCh;
+      // partitions outside [pa, pb) get no chunks: another run computes them
+      // (a frame split across GPUs, sk_run_exchange_rows)
+      if (i >= pa && i < pb) acc += (off[i + 1] - off[i] + kCh - 1) / kCh;
       pchunk[i + 1] = acc;
     }
   }
@@ -404,8 +406,18 @@ int setup(sk_run* r) {
   flag_scatter<<<nseg, 256, 0, s>>>(mask, r->env_pitch, (int)p.rows, (int)p.cols, seg, list);
   SK_CUDA(cudaMemcpyAsync(d_prow, r->part_row, sizeof(int) * (r->nparts + 1),
                           cudaMemcpyHostToDevice, s));
+  // params[2], params[3]: this run computes partitions [pa, pb) only (pb = 0: all)
+  int pa = 0, pb = r->nparts;
+  if (p.params[3] > 0) {
+    pa = (int)p.params[2];
+    pb = (int)p.params[3];
+    if (pa < 0 || pb > r->nparts || pa >= pb || (p.flags & SK_FLAG_FRAMES)) {
+      set_error("restore: active partition range must satisfy 0 <= pa < pb <= partitions");
+      return SK_ERR_ARG;
+    }
+  }
   list_bounds<<<1, kMaxParts + 1, 0, s>>>(list, seg + nseg, d_prow, r->nparts, (int)p.cols, d_off,
-                                         d_pch);
+                                         d_pch, pa, pb);
   SK_CUDA(cudaGetLastError());
   unsigned char* chg = nullptr;
   SK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&chg), (size_t)npix * 2, s));
@@ -484,6 +496,12 @@ const KernelOps kOps = {setup, launch, teardown};
 }  // namespace
 
 const KernelOps* restore_ops() { return &kOps; }
+
+// Change-flag plane of iteration `it` (restore runs), for the row exchange.
+unsigned char* restore_chg(sk_run* r, long long it) {
+  if (r->ops != &kOps || !r->aux[AUX_CHG]) return nullptr;
+  return static_cast<unsigned char*>(r->aux[AUX_CHG]) + (it & 1) * r->plan.rows * r->plan.cols;
+}
 
 int restore_frame_status(sk_run* r, long long* iters, double* values, int* exhausted) {
   if (!(r->plan.flags & SK_FLAG_FRAMES) || !r->aux[AUX_FSTAT]) {

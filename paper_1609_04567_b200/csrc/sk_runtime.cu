@@ -512,6 +512,48 @@ int sk_run_result(sk_run* r, int64_t it, int32_t* which) {
   return SK_OK;
 }
 
+static size_t dtype_size(int dt) {
+  switch (dt) {
+    case SK_U8: return 1;
+    case SK_F32: return 4;
+    case SK_F64: return 8;
+    default: return 8;
+  }
+}
+
+int sk_run_exchange_rows(sk_run* dst, sk_run* src, int64_t row_lo, int64_t row_hi, int64_t it) {
+  if (!dst || !src || dst == src || row_lo < 0 || row_hi > src->plan.rows || row_lo >= row_hi ||
+      it < 1 || it > src->launched || dst->plan.rows != src->plan.rows ||
+      dst->plan.cols != src->plan.cols || dst->plan.dtype != src->plan.dtype ||
+      dst->plan.kernel != src->plan.kernel || dst->plan.halo_top != src->plan.halo_top ||
+      src->steps_per_launch != 1 || dst->steps_per_launch != 1) {
+    set_error("sk_run_exchange_rows: runs of one geometry, rows inside the grid, a launched iteration");
+    return SK_ERR_ARG;
+  }
+  const size_t esz = dtype_size(src->plan.dtype);
+  const int b = (int)(it & 1);
+  const long long off_rows = src->plan.halo_top + row_lo;
+  const size_t width = (size_t)src->plan.cols * esz;
+  const char* sp = static_cast<const char*>(src->buf[b]) + off_rows * src->pitch * esz;
+  char* dp = static_cast<char*>(dst->buf[b]) + off_rows * dst->pitch * esz;
+  SK_CUDA(cudaMemcpy2DAsync(dp, dst->pitch * esz, sp, src->pitch * esz, width,
+                            (size_t)(row_hi - row_lo), cudaMemcpyDefault, src->stream));
+  unsigned char* sc = restore_chg(src, it);
+  unsigned char* dc = restore_chg(dst, it);
+  if (sc && dc) {
+    const size_t n = (size_t)(row_hi - row_lo) * src->plan.cols;
+    SK_CUDA(cudaMemcpyAsync(dc + row_lo * src->plan.cols, sc + row_lo * src->plan.cols, n,
+                            cudaMemcpyDefault, src->stream));
+  }
+  cudaEvent_t ev = nullptr;
+  SK_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  cudaError_t e1 = cudaEventRecord(ev, src->stream);
+  cudaError_t e2 = e1 == cudaSuccess ? cudaStreamWaitEvent(dst->stream, ev, 0) : e1;
+  cudaEventDestroy(ev);  // released once the wait has been satisfied
+  if (e2 != cudaSuccess) return cuda_fail(e2, "sk_run_exchange_rows");
+  return SK_OK;
+}
+
 int sk_run_value_ptr(sk_run* r, void** d_value) {
   if (!r || !d_value) {
     set_error("sk_run_value_ptr: null argument");
