@@ -4,10 +4,11 @@
 // Reference: Sobel block kernel apps/sobel.py:47-66 (point :33-44, border rule
 // :53-56, magnitude rounding :60-64); per-frame pixel sum apps/sobel.py:73-74.
 //
-// HBM-bound: 2 B/pixel (read 1 + write 1).  The arithmetic is the paired-fp32
-// form of sk_u8stencil.cu's sobel_sweep (exact integer features under a 2^15
-// bias, sqrt.approx + a magic add for rint, one u16x2 clip per two pixels);
-// what changes is how bytes reach the warps:
+// HBM-bound: 2 B/pixel (read 1 + write 1).  Default arithmetic: exact
+// integer features as f16 subnormals (HALF below; the paired-fp32 form of
+// sk_u8stencil.cu's sobel_sweep remains as a configuration), sqrt.approx +
+// a magic add for rint, one u16x2 clip per two pixels.  How bytes reach
+// the warps:
 //
 //  * A CTA owns a contiguous run of OUTPUT rows of the batch (frame-major, so
 //    a run covers parts of 1-3 frames); every CTA gets the same number of
@@ -37,6 +38,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdint>
+#include <type_traits>
 #include <cstdlib>
 #include <mutex>
 
@@ -128,6 +130,47 @@ __device__ __forceinline__ F2 sub2(F2 a, F2 b) { return __fadd2_rn(a, make_float
 __device__ __forceinline__ F2 mul2(F2 a, F2 b) { return __fmul2_rn(a, b); }
 __device__ __forceinline__ F2 fma2(F2 a, F2 b, F2 c) { return __ffma2_rn(a, b, c); }
 
+// ---- half-precision features (HALF): a byte x is the f16 subnormal x * 2^-24
+// (bits 0x00xx, one PRMT with a zero byte), and every Sobel feature -- S, D,
+// gx, gy, all integers of magnitude <= 1020 -- is exact as an f16 integer
+// multiple of 2^-24 (exact below 2048).  f16x2 arithmetic (HADD2 / HFMA2)
+// costs the FMA pipe one cycle per instruction where the paired fp32 form
+// costs two; gx^2 + gy^2 is formed in fp32 straight from the f16 halves by
+// the mixed-precision FHFMA (exact: < 2^22 * 2^-48), sqrt.approx of the
+// scaled value is the scaled sqrt.approx (even exponent shift), and the
+// rint adds 1.5 * 2^23 after scaling back by 2^24 (one FFMA2 per pair).
+__device__ __forceinline__ unsigned h2add(unsigned a, unsigned b) {
+  unsigned d;
+  asm("add.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ unsigned h2sub(unsigned a, unsigned b) {
+  unsigned d;
+  asm("sub.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ unsigned h2fma(unsigned a, unsigned b, unsigned c) {
+  unsigned d;
+  asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+constexpr unsigned kH2Two = 0x40004000u, kH2Four = 0x44004400u;
+// gx^2 + gy^2 of the low / high halves, in fp32
+__device__ __forceinline__ float hsq_lo(unsigned gx, unsigned gy) {
+  float r;
+  asm("{ .reg .f16 a0, a1, b0, b1; .reg .f32 t; mov.b32 {a0, a1}, %1; mov.b32 {b0, b1}, %2;"
+      " fma.rn.f32.f16 t, b0, b0, 0f00000000; fma.rn.f32.f16 %0, a0, a0, t; }"
+      : "=f"(r) : "r"(gx), "r"(gy));
+  return r;
+}
+__device__ __forceinline__ float hsq_hi(unsigned gx, unsigned gy) {
+  float r;
+  asm("{ .reg .f16 a0, a1, b0, b1; .reg .f32 t; mov.b32 {a0, a1}, %1; mov.b32 {b0, b1}, %2;"
+      " fma.rn.f32.f16 t, b1, b1, 0f00000000; fma.rn.f32.f16 %0, a1, a1, t; }"
+      : "=f"(r) : "r"(gx), "r"(gy));
+  return r;
+}
+
 template <int k>
 __device__ __forceinline__ float bf_opaque(unsigned w, unsigned K2) {
   unsigned r;
@@ -166,9 +209,10 @@ constexpr int block_of() {
 }
 // WIDE: ring rows and output rows are exactly kRowMax bytes (compile-time
 // shared and global row offsets, no per-row address arithmetic)
-template <int SR, int STAGES, int MINB, bool COPY, int VEC, bool WIDE>
+template <int SR, int STAGES, int MINB, bool COPY, int VEC, bool WIDE, bool HALF>
 __global__ void __launch_bounds__(block_of<VEC>(), MINB)
     sobel_tma_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ Args A) {
+  static_assert(!HALF || VEC == 8, "half-precision features: 8 pixels per lane");
   constexpr int NW = kRowMax / (32 * VEC);
   constexpr int NP = VEC / 2;       // pixel pairs per lane: (p_t, p_t+NP)
   constexpr int WCOLS = 32 * VEC;   // columns per consumer warp
@@ -178,9 +222,10 @@ __global__ void __launch_bounds__(block_of<VEC>(), MINB)
   const unsigned base = (raw + 127u) & ~127u;
   const int ws = WIDE ? kRowMax : A.ws;
   const long long opitch = WIDE ? (long long)kRowMax : A.out_pitch;
-  const unsigned stage_bytes = (unsigned)(SR * ws);
+  const unsigned stage_bytes = (unsigned)(SR * ws);              // one box (the tx count)
+  const unsigned stage_stride = (stage_bytes + 127u) & ~127u;      // TMA destinations: 128-byte aligned
   const unsigned ring = base + FRONT;
-  const unsigned bars = ring + STAGES * stage_bytes + BACK;  // full[STAGES], empty[STAGES]
+  const unsigned bars = ring + STAGES * stage_stride + BACK;  // full[STAGES], empty[STAGES]
   auto full = [&](int s) { return bars + 8u * s; };
   auto empty = [&](int s) { return bars + 8u * (STAGES + s); };
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -222,7 +267,7 @@ __global__ void __launch_bounds__(block_of<VEC>(), MINB)
       if (lane == 0) {
         const int s = (int)(qi % STAGES);
         mbar_expect_tx(full(s), stage_bytes);
-        tma_load_4d(ring + s * stage_bytes, &tm, 0, 0, is.a - 1 + SR * is_k, is.f, full(s));
+        tma_load_4d(ring + s * stage_stride, &tm, 0, 0, is.a - 1 + SR * is_k, is.f, full(s));
       }
       ++is_k;
       ++qi;
@@ -251,8 +296,8 @@ __global__ void __launch_bounds__(block_of<VEC>(), MINB)
       unsigned acc = 0;
       for (int k = 0; k < nst; ++k, ++q) {
         mbar_wait(empty(q % STAGES), (q / STAGES) & 1, A.hint);
-        const unsigned sb = ring + (q % STAGES) * stage_bytes;
-        const unsigned pb = ring + ((q + STAGES - 1) % STAGES) * stage_bytes;
+        const unsigned sb = ring + (q % STAGES) * stage_stride;
+        const unsigned pb = ring + ((q + STAGES - 1) % STAGES) * stage_stride;
         const int i = SR * k + t;  // input row of this lane's output row r = a + i - 2
         if (mine && i >= 2 && i < n_in) {
           const int r = a + i - 2;
@@ -312,7 +357,9 @@ __global__ void __launch_bounds__(block_of<VEC>(), MINB)
   const unsigned lofs = (unsigned)col;  // this lane's byte offset in a ring row
   const F2 two = f2(2.0f, 2.0f), four = f2(4.0f, 4.0f), magic = f2(12582912.0f, 12582912.0f);
 
-  F2 G[NP], SA[NP], SB[NP], DA[NP], DB[NP];
+  // feature pairs: fp32 (x, y) pairs, or f16x2 words of adjacent pixels (HALF)
+  using FT = std::conditional_t<HALF, unsigned, F2>;
+  FT G[NP], SA[NP], SB[NP], DA[NP], DB[NP];
   unsigned acc = 0;
   unsigned char* po = nullptr;
 
@@ -336,14 +383,14 @@ __global__ void __launch_bounds__(block_of<VEC>(), MINB)
     }
   };
   // 4 Q of the ring row at p (the S of a missing row above / below the frame)
-  auto quad4 = [&](unsigned p, F2* S) {
+  auto quad4_f = [&](unsigned p, F2* S) {
     unsigned wlo, whi;
     pairs(p, S, wlo, whi);
 #pragma unroll
     for (int t = 0; t < NP; ++t) S[t] = mul2(S[t], four);
   };
   // features of the ring row at shared address p: S = L + 2Q + R, D = R - L
-  auto take = [&](unsigned p, F2* S, F2* D) {
+  auto take_f = [&](unsigned p, F2* S, F2* D) {
     unsigned xl, xr, wlo, whi;
     F2 Q[NP];
     pairs(p, Q, wlo, whi);
@@ -362,31 +409,85 @@ __global__ void __launch_bounds__(block_of<VEC>(), MINB)
       D[t] = sub2(R, L);
     }
   };
+  // HALF: the lane's adjacent-pixel pairs P_i = (p_2i, p_2i+1) and the
+  // shifted pairs F_i = (p_2i-1, p_2i), all f16 subnormal integers
+  auto quad4_h = [&](unsigned p, unsigned* S) {
+    unsigned wx, wy;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(wx), "=r"(wy) : "r"(p) : "memory");
+    S[0] = h2fma(__byte_perm(wx, 0u, 0x4140u), kH2Four, 0u);
+    S[1] = h2fma(__byte_perm(wx, 0u, 0x4342u), kH2Four, 0u);
+    S[2] = h2fma(__byte_perm(wy, 0u, 0x4140u), kH2Four, 0u);
+    S[3] = h2fma(__byte_perm(wy, 0u, 0x4342u), kH2Four, 0u);
+  };
+  auto take_h = [&](unsigned p, unsigned* S, unsigned* D) {
+    unsigned wx, wy, xl, xr;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(wx), "=r"(wy) : "r"(p) : "memory");
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(xl) : "r"(p - 1) : "memory");
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(xr) : "r"(p + 8) : "memory");
+    unsigned P[4], F[5];
+    P[0] = __byte_perm(wx, 0u, 0x4140u);
+    P[1] = __byte_perm(wx, 0u, 0x4342u);
+    P[2] = __byte_perm(wy, 0u, 0x4140u);
+    P[3] = __byte_perm(wy, 0u, 0x4342u);
+    F[0] = __byte_perm(xl, P[0], 0x5410u);  // (p_-1, p_0): xl's byte 1 is 0
+    F[1] = __byte_perm(P[0], P[1], 0x5432u);
+    F[2] = __byte_perm(P[1], P[2], 0x5432u);
+    F[3] = __byte_perm(P[2], P[3], 0x5432u);
+    F[4] = __byte_perm(P[3], xr, 0x5432u);  // (p_7, p_8)
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      S[t] = h2fma(P[t], kH2Two, h2add(F[t], F[t + 1]));
+      D[t] = h2sub(F[t + 1], F[t]);
+    }
+  };
+  auto take = [&](unsigned p, FT* S, FT* D) {
+    if constexpr (HALF) take_h(p, S, D);
+    else take_f(p, S, D);
+  };
+  auto quad4 = [&](unsigned p, FT* S) {
+    if constexpr (HALF) quad4_h(p, S);
+    else quad4_f(p, S);
+  };
+  auto gfma = [&](FT d, FT e) -> FT {  // 2 d + e
+    if constexpr (HALF) return h2fma(d, kH2Two, e);
+    else return fma2(d, two, e);
+  };
   // input row at p -> the output row above it: gx = G + D(new), gy = S(new) - S(old).
   // Image rows 0 / rows-1 need no fix-up: rows outside the frame arrive as
   // zeros (D = 0, which is the reference's gx there), and S of the missing
   // row is replaced by 4 Q of the centre row (the reference's gy there):
   // SA at the top (below), S(new) = 4 Q(row above) at the bottom (`pbot`).
-  auto step = [&](auto masked_t, auto hot_t, unsigned p, F2* Sold, F2* Dprev, F2* Dnew,
+  auto step = [&](auto masked_t, auto hot_t, unsigned p, FT* Sold, FT* Dprev, FT* Dnew,
                   unsigned pbot, unsigned char* q) {
     constexpr bool MASKED = decltype(masked_t)::value;
     constexpr bool HOT = decltype(hot_t)::value;
-    F2 S[NP];
+    FT S[NP];
     take(p, S, Dnew);
     if (!HOT && pbot) quad4(pbot, S);
     unsigned o[VEC];  // o[k]: pixel k, rint(sqrt(n)) in the low 16 bits
 #pragma unroll
     for (int k = 0; k < NP; ++k) {
-      const F2 gx = add2(G[k], Dnew[k]);
-      const F2 gy = sub2(S[k], Sold[k]);
-      const F2 n = fma2(gx, gx, mul2(gy, gy));
-      float x = n.x, y = n.y;
-      asm("sqrt.approx.ftz.f32 %0, %0;" : "+f"(x));
-      asm("sqrt.approx.ftz.f32 %0, %0;" : "+f"(y));
-      const F2 r = add2(f2(x, y), magic);
-      o[k] = __float_as_uint(r.x);
-      o[k + NP] = __float_as_uint(r.y);
-      G[k] = fma2(Dnew[k], two, Dprev[k]);
+      if constexpr (HALF) {
+        const unsigned gx = h2add(G[k], Dnew[k]);
+        const unsigned gy = h2sub(S[k], Sold[k]);
+        float x = hsq_lo(gx, gy), y = hsq_hi(gx, gy);  // (gx^2 + gy^2) 2^-48
+        asm("sqrt.approx.ftz.f32 %0, %0;" : "+f"(x));
+        asm("sqrt.approx.ftz.f32 %0, %0;" : "+f"(y));
+        const F2 r = fma2(f2(x, y), f2(16777216.0f, 16777216.0f), magic);
+        o[2 * k] = __float_as_uint(r.x);  // pair k = pixels 2k, 2k+1
+        o[2 * k + 1] = __float_as_uint(r.y);
+      } else {
+        const F2 gx = add2(G[k], Dnew[k]);
+        const F2 gy = sub2(S[k], Sold[k]);
+        const F2 n = fma2(gx, gx, mul2(gy, gy));
+        float x = n.x, y = n.y;
+        asm("sqrt.approx.ftz.f32 %0, %0;" : "+f"(x));
+        asm("sqrt.approx.ftz.f32 %0, %0;" : "+f"(y));
+        const F2 r = add2(f2(x, y), magic);
+        o[k] = __float_as_uint(r.x);  // pair k = pixels k, k+NP
+        o[k + NP] = __float_as_uint(r.y);
+      }
+      G[k] = gfma(Dnew[k], Dprev[k]);
       Sold[k] = S[k];
     }
     unsigned wd[VEC / 4];
@@ -446,7 +547,7 @@ __global__ void __launch_bounds__(block_of<VEC>(), MINB)
         } else if (!HOT && k == 0 && j == 1) {
           take(p, SB, DB);
 #pragma unroll
-          for (int t = 0; t < NP; ++t) G[t] = fma2(DB[t], two, DA[t]);
+          for (int t = 0; t < NP; ++t) G[t] = gfma(DB[t], DA[t]);
         } else {
           const unsigned pb = (!HOT && bottom && j == jn - 1)
                                   ? (j > 0 ? p - ws : prev_sb + (SR - 1) * ws + lofs)
@@ -461,7 +562,7 @@ __global__ void __launch_bounds__(block_of<VEC>(), MINB)
     };
     for (int k = 0; k < nst; ++k) {
       mbar_wait(full(cs), cph, A.hint);
-      const unsigned sb = ring + cs * stage_bytes;
+      const unsigned sb = ring + cs * stage_stride;
       const int ns = cs + 1 == STAGES ? 0 : cs + 1;
       const unsigned nph = ns == 0 ? cph ^ 1u : cph;
       if (k > 0 && SR * (k + 1) < n_in) {
@@ -509,7 +610,7 @@ bool disabled() {
 }
 
 size_t smem_bytes(int ws, int sr, int stages) {
-  return 128 + FRONT + (size_t)stages * sr * ws + BACK + 16 * stages;
+  return 128 + FRONT + (size_t)stages * (((size_t)sr * ws + 127) & ~(size_t)127) + BACK + 16 * stages;
 }
 
 using KFn = void (*)(const CUtensorMap, const Args);
@@ -520,14 +621,19 @@ struct Cfg {
   KFn fn, fn_wide;
 };
 // measured configurations (SK_TMA_CFG=<index> selects one; 0 is the default)
-#define SK_TMA_CFG_ROW(sr, st, mb, cp, v) \
-  {sr, st, mb, cp, v, sobel_tma_kernel<sr, st, mb, cp, v, false>, sobel_tma_kernel<sr, st, mb, cp, v, true>}
+#define SK_TMA_CFG_ROW(sr, st, mb, cp, v, h)                               \
+  {sr, st, mb, cp, v, sobel_tma_kernel<sr, st, mb, cp, v, false, h>, \
+   sobel_tma_kernel<sr, st, mb, cp, v, true, h>}
 const Cfg kCfgs[] = {
-    SK_TMA_CFG_ROW(8, 6, 2, false, 8),   // default: 1.03 ms per 512 C2 frames
-    SK_TMA_CFG_ROW(4, 12, 2, false, 8),  // finer stages: 1.15 ms
-    SK_TMA_CFG_ROW(8, 6, 2, false, 4),   // 4 pixels per lane, 2x warps: 1.20 ms
-    SK_TMA_CFG_ROW(8, 12, 1, false, 8),  // one CTA per SM, 12 stages: 1.10 ms
-    SK_TMA_CFG_ROW(8, 6, 2, true, 8),    // copy probe (not Sobel): 0.73 ms = 5.9 TB/s
+    SK_TMA_CFG_ROW(8, 4, 3, false, 8, true),    // default: f16 features, 3 CTAs x 4 stages: 0.84 ms
+    SK_TMA_CFG_ROW(8, 6, 2, false, 8, false),   // fp32 paired features: 1.04 ms per 512 C2 frames
+    SK_TMA_CFG_ROW(8, 6, 2, false, 8, true),    // f16, 2 CTAs x 6 stages: 0.89 ms
+    SK_TMA_CFG_ROW(8, 6, 3, false, 8, true),    // f16, 3 CTAs x 6 stages: 0.87 ms
+    SK_TMA_CFG_ROW(8, 3, 4, false, 8, true),    // f16, 4 CTAs x 3 stages
+    SK_TMA_CFG_ROW(4, 8, 3, false, 8, true),    // f16, 3 CTAs x 8 stages of 4 rows
+    SK_TMA_CFG_ROW(4, 6, 4, false, 8, true),    // f16, 4 CTAs x 6 stages of 4 rows
+    SK_TMA_CFG_ROW(8, 6, 2, false, 4, false),   // 4 pixels per lane, 2x warps: 1.20 ms
+    SK_TMA_CFG_ROW(8, 6, 2, true, 8, false),    // copy probe (not Sobel): 0.73 ms = 5.9 TB/s
 };
 #undef SK_TMA_CFG_ROW
 

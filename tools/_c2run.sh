@@ -1,1 +1,2 @@
-timeout 900 python -m pytest tests/test_gpu_split_restore.py tests/test_gpu_stream_farm.py tests/test_gpu_apps.py tests/test_native_abi.py -q -x -p no:cacheprovider 2>&1 | tail -25
+timeout 300 python bench.py --workload c2 --steps 5 --warmup 3 > gpurun_out/r02_bench_c2.json 2> gpurun_out/r02_bench_c2.err; tail -c 700 gpurun_out/r02_bench_c2.json
+FRAMES=512 timeout 600 ncu --set full --clock-control none --import-source on -k regex:sobel_tma -s 1 -c 1 -o gpurun_out/r02_sobel_tma_h python tools/sobel_sweep.py > gpurun_out/ncu_c2.log 2>&1; tail -1 gpurun_out/ncu_c2.log
