@@ -45,8 +45,10 @@ extern "C" {
 
 /* element types */
 #define SK_U8 1
+#define SK_I32 2 /* reduce_all only */
 #define SK_F32 3
 #define SK_F64 4
+#define SK_I64 5 /* reduce_all only */
 
 /* device kernels: the reference's block kernels, one per app
  * (apps/helmholtz.py:85-92, apps/sobel.py:47-66, apps/denoise.py:105-135,
@@ -238,6 +240,16 @@ int sk_run_destroy(sk_run* run);
  * sk_common.cuh div_const): number of fp32 numerators in the fast range whose
  * result differs from IEEE division x / b (0 expected; -1 = check failed). */
 long long sk_verify_div_f32(float b, void* stream);
+
+/* reduce_all for SUM / MAX (patterns.py:143-147): the left fold
+ * acc = identity; for v in data: acc = fn(acc, v), row-major, on the device.
+ * dtype SK_U8 / SK_I32 / SK_I64 (identity and result: int64; SUM wraps like
+ * int64), SK_F32 / SK_F64 (identity and result in the element type; SUM is
+ * folded sequentially in that type, MAX keeps `a if b < a else b`'s NaN and
+ * tie behaviour): bit-identical to the sequential fold.  `identity` is a host
+ * pointer (8 bytes; 4 for SK_F32), `d_out` device memory (8 bytes). */
+int sk_reduce_fold(const void* d_data, int64_t n, int32_t dtype, int32_t op, const void* identity,
+                   void* d_out, void* stream);
 
 /* ---- batched map-only stencils for frame streams (config C2) -----------
  * Sobel edge magnitude (apps/sobel.py:47-66) over `frames` frames of

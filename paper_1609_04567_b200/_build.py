@@ -26,6 +26,7 @@ SOURCES = [
     "sk_verify.cu",
     "sk_u8stencil.cu",
     "sk_sobel_tma.cu",
+    "sk_reduce.cu",
     "sk_amf.cu",
     "sk_restore.cu",
     "sk_dispatch.cu",

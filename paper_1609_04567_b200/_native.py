@@ -14,6 +14,7 @@ from . import _build
 
 SK_OK, SK_ERR_ARG, SK_ERR_CUDA, SK_ERR_STATE, SK_ERR_UNSUPPORTED = 0, 1, 2, 3, 4
 SK_U8, SK_F32, SK_F64 = 1, 3, 4
+SK_I32, SK_I64 = 2, 5  # sk_reduce_fold only
 SK_KERNEL_HELMHOLTZ, SK_KERNEL_SOBEL, SK_KERNEL_AMF, SK_KERNEL_RESTORE, SK_KERNEL_LIFE = 1, 2, 3, 4, 5
 SK_KERNEL_JIT = 6
 SK_REDUCE_SUM, SK_REDUCE_MAX, SK_REDUCE_CUSTOM = 1, 2, 3
@@ -33,7 +34,7 @@ EXPORTS = (
     "sk_amf_frames", "sk_jit_compile", "sk_jit_log", "sk_jit_cubin_size", "sk_jit_cubin", "sk_jit_destroy",
     "sk_run_begin_jit", "sk_run_error",
     "sk_run_set_peers", "sk_run_peer_wait", "sk_run_exchange_rows", "sk_ipc_alloc", "sk_ipc_handle", "sk_ipc_open",
-    "sk_ipc_close", "sk_ipc_free",
+    "sk_ipc_close", "sk_ipc_free", "sk_reduce_fold",
 )
 
 SK_MAX_PEERS = 8
@@ -128,6 +129,7 @@ def _declare(lib):
         "sk_run_set_peers": [P, C.POINTER(sk_peers)],
         "sk_run_peer_wait": [P, I64],
         "sk_run_exchange_rows": [P, P, I64, I64, I64],
+        "sk_reduce_fold": [P, I64, I32, I32, P, P, P],
         "sk_ipc_alloc": [I64, C.POINTER(P)],
         "sk_ipc_handle": [P, C.c_char_p],
         "sk_ipc_open": [C.c_char_p, C.POINTER(P)],

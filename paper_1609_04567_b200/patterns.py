@@ -312,30 +312,105 @@ def apply_to_all(f: Callable[[Any], Any], a: Grid) -> Grid:
 
 
 def reduce_all(op: Combinator, a: Grid) -> Any:
-    """Left fold of all elements from the identity (patterns.py:143-147) on
-    the device: SUM / MAX directly; any other combinator as a one-iteration
-    loop of the identity stencil whose reduce is the compiled combinator."""
+    """Left fold of all elements from the identity, row-major
+    (patterns.py:143-147), on the device.  SUM / MAX combinators
+    (declared or recognised exactly, combinator_kind) run sk_reduce_fold:
+    bit-identical to the sequential fold -- integer sums are order-free,
+    float MAX keeps `a if b < a else b`'s NaN / tie behaviour, float SUM is
+    folded sequentially in the element type (numpy NEP 50).  Any other
+    combinator, or an identity whose type would change the arithmetic
+    (a float identity on integers, a numpy scalar of another width), runs
+    as a one-iteration loop of the identity stencil whose reduce is the
+    compiled combinator."""
+    import ctypes as C
+
     from . import _native
 
-    _native.require_cuda()
+    lib = _native.require_cuda()
+    import numpy as np
     import torch
 
     try:
         kind = combinator_kind(op)
     except DeviceUnsupported:
         kind = None
-    if kind is None:
+    t = a.tensor(device="cuda") if kind is not None else None
+    plan = None if t is None else _fold_plan(kind, t.dtype, op.identity)
+    if plan is not None and kind == "max" and t.is_floating_point() and not _is_ifexp_max(op):
+        plan = None  # builtin max() keeps the first of equal values and skips NaN: fold it as written
+    if plan is None:
         from .loop import loop_stencil_reduce, stop_after
 
         _, rep = loop_stencil_reduce(0, ElementalFn(point=lambda nb, env: nb.center, k=0), op,
                                      stop_after(1), a)
         return rep.final_reduce
-    t = a.tensor(device="cuda")
-    if t.numel() == 0:
-        return op.identity
-    v = (t.sum(dtype=torch.float64) if t.is_floating_point() else t.sum()).item() \
-        if kind == "sum" else t.max().item()
-    return op.fn(op.identity, v)
+    dt, ident_bytes, host_post = plan
+    t = t.contiguous().reshape(-1)
+    out = torch.zeros(1, dtype=torch.float64, device=t.device)
+    buf = C.create_string_buffer(ident_bytes, 8)
+    _native.check(lib.sk_reduce_fold(C.c_void_p(t.data_ptr()), t.numel(), dt,
+                                     _native.SK_REDUCE_SUM if kind == "sum" else _native.SK_REDUCE_MAX,
+                                     buf, C.c_void_p(out.data_ptr()),
+                                     _native.stream_handle(torch.cuda.current_stream(t.device))))
+    raw = out.cpu().numpy().view(np.uint8)
+    return host_post(raw)
+
+
+def _fold_plan(kind, tdtype, ident):
+    """(sk dtype, identity bytes, result decoder) for sk_reduce_fold, or None
+    when the reference's arithmetic would differ from the kernel's."""
+    import numpy as np
+    import torch
+
+    from . import _native
+
+    ints = {torch.uint8: _native.SK_U8, torch.int32: _native.SK_I32, torch.int64: _native.SK_I64}
+    if tdtype in ints:
+        if isinstance(ident, (bool, np.bool_)):
+            return None
+        if isinstance(ident, (int, np.integer)):
+            iv = int(ident)
+            if not -(1 << 63) <= iv < (1 << 63):
+                return None
+            if kind == "sum":
+                return ints[tdtype], np.int64(iv).tobytes(), lambda r: int(r[:8].view(np.int64)[0])
+            # MAX: the kernel folds from int64's minimum; the identity joins last
+            # (integers: no NaN, equal values are equal)
+            return (ints[tdtype], np.int64(np.iinfo(np.int64).min).tobytes(),
+                    lambda r: _max_join(iv, int(r[:8].view(np.int64)[0])))
+        if kind == "max" and isinstance(ident, float):
+            return (ints[tdtype], np.int64(np.iinfo(np.int64).min).tobytes(),
+                    lambda r: _max_join(ident, int(r[:8].view(np.int64)[0])))
+        return None  # a float identity makes the reference's sum float arithmetic
+    if tdtype not in (torch.float32, torch.float64):
+        return None
+    npdt = np.float32 if tdtype == torch.float32 else np.float64
+    weak = isinstance(ident, (int, float)) and not isinstance(ident, bool)
+    if not weak and not (isinstance(ident, np.floating) and ident.dtype == npdt):
+        return None
+    iv = npdt(ident)  # NEP 50: a Python scalar takes the array's type
+    if npdt == np.float32:
+        dec = lambda r: np.float32(r[:4].view(np.float32)[0])  # noqa: E731
+    else:
+        dec = lambda r: float(r[:8].view(np.float64)[0])  # noqa: E731
+    return (_native.SK_F32 if npdt == np.float32 else _native.SK_F64, iv.tobytes(), dec)
+
+
+def _is_ifexp_max(op) -> bool:
+    """The reference's `a if b < a else b` (declared by max_combinator, or
+    that exact expression), as opposed to the builtin max()."""
+    import ast
+
+    if getattr(op, "kind", None) == "max" and op.fn is not max:
+        le = _lambda_expr(op.fn)
+        return le is None or not isinstance(le[1], ast.Call)
+    le = _lambda_expr(op.fn)
+    return le is not None and isinstance(le[1], ast.IfExp) and _ast_combinator(op.fn) == "max"
+
+
+def _max_join(ident, m):
+    """`a if b < a else b` of the identity and the data's maximum (ints)."""
+    return ident if m < ident else m
 
 
 def map_pattern(f, a: Grid) -> Grid:
