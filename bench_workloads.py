@@ -296,7 +296,7 @@ def c2(args, ClockSampler, measured_peaks, local=0, world=1, rank=0):
                      "frac": ach / peak, "traffic": _traffic("sobel_2048_per_frame", B),
                      "avg_kernel_ms": kms,
                      "kernel": f"sobel_tma_kernel ({B} frames/launch; TMA row ring), 2 B/pixel",
-                     "note": "issue-bound (77% issue-active, FMA pipe 66%, XU 57%): exact "
+                     "note": "issue-bound (79% issue-active; FMA 57%, XU 60%, ALU 54%): exact "
                              "f16-subnormal features, fp32 magnitude, per-pixel sqrt/round "
                              "(profiles/r02_ncu_sobel_tma.json; the same ring as a pure copy "
                              "streams 5.9 TB/s)",
