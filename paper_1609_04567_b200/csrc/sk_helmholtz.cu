@@ -21,8 +21,13 @@
 // division): keep*c + ((relax*((f + ax*(l+r)) + ay*(u+d))) / b), constants
 // rounded to the grid dtype first (numpy NEP 50).  Results are bit-identical
 // to the reference block route in fp32 and fp64.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 
 #include "sk_internal.h"
 #include "sk_sweep.cuh"
@@ -749,6 +754,8 @@ __global__ void __launch_bounds__(BLOCK, 1) helm_resident(const __grid_constant_
   }
 }
 
+#include "sk_helm_tma.cuh"
+
 // ---------------------------------------------------------------- host side
 
 namespace {
@@ -1011,6 +1018,129 @@ int fixup_t(sk_run* r, long long it, cudaStream_t s) {
   return SK_OK;
 }
 
+// ---- TMA row-ring sweep (sk_helm_tma.cuh), opt-in: SK_HELM_TMA=1 for fp64
+// grids, =2 for fp32 too.  Measured on B200 (23170^2 fp64, 36 sweeps):
+// 2.16-2.17 ms per sweep, level with the register march below (2.16-2.17,
+// run to run) -- the ring keeps the bytes in flight, but with 8 consumer
+// warps per CTA the dependent fp64 update chain per row bounds the
+// consumers (the register march hides it with 32 warps per SM).  Ring
+// shapes tried (rows per stage x stages x CTAs per SM, elements per
+// thread): 6x2x2 v2 2.16-2.17, 4x3x2 v2 2.26, 4x2x3 v2 2.32, 6x2x2 v4 2.31,
+// 2x4x3 v2 2.31, 4x3x2 v4 2.29 ms.  Parity-tested (SK_HELM_TMA=2 runs the
+// Helmholtz / production / fuzz / odd-width suites through it).
+constexpr int kTmaSR = 6, kTmaStages = 2, kTmaMinB = 2, kTmaVec = 2;
+
+template <typename T>
+using TmaFn = void (*)(const helm_tma::Args<T>);
+
+template <typename T>
+TmaFn<T> pick_tma(int delta, int reduce) {
+#define SK_HT(D, R)                                                                         \
+  if (delta == D && reduce == R)                                                            \
+    return helm_tma::helm_tma_sweep<T, kTmaSR, kTmaStages, kTmaMinB, kTmaVec, D, R>;
+  SK_HT(SK_DELTA_NONE, SK_REDUCE_SUM)
+  SK_HT(SK_DELTA_NONE, SK_REDUCE_MAX)
+  SK_HT(SK_DELTA_ABS, SK_REDUCE_SUM)
+  SK_HT(SK_DELTA_ABS, SK_REDUCE_MAX)
+  SK_HT(SK_DELTA_SQUARE, SK_REDUCE_SUM)
+  SK_HT(SK_DELTA_SQUARE, SK_REDUCE_MAX)
+#undef SK_HT
+  return nullptr;
+}
+
+template <typename T>
+size_t tma_stage_bytes(int sr) {
+  const size_t hb = 16 / sizeof(T);
+  return 4 * (size_t)sr * helm_tma::HALF * sizeof(T) + 2 * ((sr * hb * sizeof(T) + 127) & ~(size_t)127);
+}
+
+int tma_mode() {
+  static const int v = [] {
+    const char* e = getenv("SK_HELM_TMA");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
+// the run's tensor maps (host memory in aux[5]; built on first use)
+struct HelmMaps {
+  CUtensorMap um[3], uh[3], fm;
+};
+
+template <typename T>
+int launch_tma(sk_run* r, const LoopCtl& L, cudaStream_t s, const HelmArgs<T>& a) {
+  const sk_plan& p = r->plan;
+  const int mode = tma_mode();
+  if (mode == 0 || (sizeof(T) == 4 && mode < 2)) return SK_ERR_UNSUPPORTED;
+  const int SR = kTmaSR;
+  const size_t esz = sizeof(T);
+  auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+  if (L.persistent || r->has_peers || p.halo_top || p.halo_bottom || !r->env || p.cols < 512 ||
+      p.rows < SR || (r->pitch * esz) % 16 || (r->src_pitch * esz) % 16 ||
+      (r->env_pitch * esz) % 16 || !al16(r->src) || !al16(r->env) || !al16(r->buf[0]) ||
+      !al16(r->buf[1]))
+    return SK_ERR_UNSUPPORTED;
+  TmaFn<T> fn = pick_tma<T>(p.delta_op, p.reduce_op);
+  auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(tma_encoder());
+  if (!fn || !enc) return SK_ERR_UNSUPPORTED;
+  HelmMaps* mp = static_cast<HelmMaps*>(r->aux[5]);
+  if (!mp) {
+    mp = static_cast<HelmMaps*>(malloc(sizeof(HelmMaps)));
+    if (!mp) return SK_ERR_UNSUPPORTED;
+    const CUtensorMapDataType dt =
+        sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    auto make = [&](CUtensorMap* m, const void* ptr, long long pitch, int boxw) {
+      cuuint64_t dims[2] = {(cuuint64_t)p.cols, (cuuint64_t)p.rows};
+      cuuint64_t strides[1] = {(cuuint64_t)(pitch * esz)};
+      cuuint32_t box[2] = {(cuuint32_t)boxw, (cuuint32_t)SR};
+      cuuint32_t estr[2] = {1, 1};
+      return enc(m, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+             CUDA_SUCCESS;
+    };
+    const void* us[3] = {r->src, r->buf[0], r->buf[1]};
+    const long long ps[3] = {r->src_pitch, r->pitch, r->pitch};
+    bool ok = make(&mp->fm, r->env, r->env_pitch, helm_tma::HALF);
+    for (int i = 0; i < 3 && ok; ++i)
+      ok = make(&mp->um[i], us[i], ps[i], helm_tma::HALF) &&
+           make(&mp->uh[i], us[i], ps[i], (int)(16 / sizeof(T)));
+    if (!ok) {
+      free(mp);
+      return SK_ERR_UNSUPPORTED;
+    }
+    r->aux[5] = mp;
+  }
+  helm_tma::Args<T> A;
+  for (int i = 0; i < 3; ++i) {
+    A.um[i] = mp->um[i];
+    A.uh[i] = mp->uh[i];
+  }
+  A.fm = mp->fm;
+  A.h = a;
+  const size_t smem = 128 + (size_t)kTmaStages * tma_stage_bytes<T>(SR) + 16 * kTmaStages;
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, bool> attr;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_pair(r->device, reinterpret_cast<const void*>(fn));
+    if (!attr[key]) {
+      SK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr[key] = true;
+    }
+  }
+  int per_sm = 0;
+  const int nt = helm_tma::nthreads<kTmaVec>();
+  SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, nt, smem));
+  if (per_sm < 1) return SK_ERR_UNSUPPORTED;
+  const int nch = r->part_chunk[r->nparts];
+  int grid = device_sms(r->device) * per_sm;
+  if (grid > nch) grid = nch;
+  fn<<<grid, nt, smem, s>>>(A);
+  SK_CUDA(cudaGetLastError());
+  return SK_OK;
+}
+
 template <typename T>
 int launch_t(sk_run* r, const LoopCtl& L, cudaStream_t s) {
   const sk_plan& p = r->plan;
@@ -1036,6 +1166,11 @@ int launch_t(sk_run* r, const LoopCtl& L, cudaStream_t s) {
   }
   if (persist) {
     const int rc = launch_resident<T>(r, L, s, a);
+    if (rc == SK_OK) return SK_OK;
+    if (rc != SK_ERR_UNSUPPORTED) return rc;
+  }
+  if (!persist) {
+    const int rc = launch_tma<T>(r, L, s, a);
     if (rc == SK_OK) return SK_OK;
     if (rc != SK_ERR_UNSUPPORTED) return rc;
   }
@@ -1069,6 +1204,10 @@ int fixup(sk_run* r, long long it, cudaStream_t s) {
 }
 
 void teardown(sk_run* r) {
+  if (r->aux[5]) {  // tensor maps (host memory)
+    free(r->aux[5]);
+    r->aux[5] = nullptr;
+  }
   for (int i : {6, 7})
     if (r->aux[i]) {
       cudaFreeAsync(r->aux[i], r->stream);

@@ -79,6 +79,9 @@ int sobel_frames_tma(const uint8_t* in, long long in_pitch, long long in_fs, uin
                      long long out_pitch, long long out_fs, int frames, long long rows,
                      long long cols, long long* sums, cudaStream_t s);
 
+// cuTensorMapEncodeTiled (PFN_cuTensorMapEncodeTiled_v12000), or null
+void* tma_encoder();
+
 // mismatches of div_const vs IEEE division over all safe fp32 numerators
 // (cached per divisor; -1 if the check could not run)
 long long verify_div_f32(float b, cudaStream_t s);

@@ -662,6 +662,9 @@ unsigned hint_ns() {
 
 }  // namespace sobel_tma
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
+void* tma_encoder() { return reinterpret_cast<void*>(sobel_tma::encoder()); }
+
 // Returns SK_OK after enqueueing the TMA kernel, or SK_ERR_UNSUPPORTED when the
 // geometry does not fit it (the caller then runs the generic batched sweep).
 int sobel_frames_tma(const uint8_t* in, long long in_pitch, long long in_fs, uint8_t* out,
