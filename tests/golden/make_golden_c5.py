@@ -55,18 +55,31 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--frames", type=int, default=64)
     ap.add_argument("--procs", type=int, default=os.cpu_count() or 8)
+    ap.add_argument("--extend", action="store_true",
+                    help="keep the frames already in golden_c5.json, compute the rest")
     args = ap.parse_args()
     out = {}
+    path = os.path.join(HERE, "golden_c5.json")
+    if args.extend and os.path.exists(path):
+        out = dict(json.load(open(path))["frames"])
+    todo = [i for i in range(args.frames) if str(i) not in out]
     with Pool(args.procs) as pool:
-        for i, rec in pool.imap_unordered(one, range(args.frames)):
+        for n, (i, rec) in enumerate(pool.imap_unordered(one, todo)):
             out[str(i)] = rec
             print(i, rec["iterations"], rec["flagged"], f"{rec['wall_s']:.1f}s", flush=True)
+            if n % 64 == 63:  # checkpoint
+                _write(path, out)
+    _write(path, out)
+    print("wrote", len(out), "frames")
+
+
+def _write(path, out):
     meta = {"source": "reference stencilkit (P=1), tests/golden/make_golden_c5.py",
             "level": 0.1, "rows": 1080, "cols": 1920,
             "frames": {k: out[k] for k in sorted(out, key=int)}}
-    with open(os.path.join(HERE, "golden_c5.json"), "w") as fh:
+    with open(path + ".tmp", "w") as fh:
         json.dump(meta, fh, indent=1)
-    print("wrote", len(out), "frames")
+    os.replace(path + ".tmp", path)
 
 
 if __name__ == "__main__":
