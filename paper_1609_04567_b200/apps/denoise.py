@@ -31,7 +31,7 @@ from ..grid import Grid, GridError
 from ..loop import Condition, DeviceCond, stop_after
 from ..partition import DeploymentMode, WorkerGroup, parallel_loop
 from ..patterns import Combinator, DeviceKernel, DeviceUnsupported, ElementalFn, abs_change
-from ..streams import (Stage, StageStats, StreamError, StreamReport, ordered_farm, pipeline,
+from ..streams import (Stage, StreamReport, _host_ring, batch_farm, ordered_farm, pipeline,
                        run_stream)
 
 _SEARCH_STEPS = math.ceil(math.log((255.0 - 0.0) / 0.25) / math.log(1.5))  # 18, as the reference
@@ -385,32 +385,6 @@ def salt_pepper(img: Grid, level: float, seed: int = 42):
     return Grid.from_array(noisy), Grid.from_array(hit.astype(np.int64))
 
 
-class _HostRing:
-    """Pinned host frames the restore lanes read results back into (the
-    `host_buffers` mode of video_restore_pipeline): a frame's buffer returns
-    to the pool when the writer is done with it, so steady state allocates
-    nothing and every device->host copy is one DMA into pinned memory.  The
-    pool grows on demand (never blocks: out-of-order completions waiting for
-    the ordered writer hold buffers too)."""
-
-    def __init__(self):
-        self.lock = threading.Lock()
-        self.free = []
-
-    def get(self, shape, dtype):
-        import torch
-
-        with self.lock:
-            for i, t in enumerate(self.free):
-                if tuple(t.shape) == tuple(shape) and t.dtype == dtype:
-                    return self.free.pop(i)
-        return torch.empty(tuple(shape), dtype=dtype, pin_memory=True)
-
-    def put(self, t):
-        with self.lock:
-            self.free.append(t)
-
-
 class _RestoreBatcher:
     """Coalesces the restore farm's frames on ONE GPU into device batches.
 
@@ -531,159 +505,19 @@ def _host_u8(img):
 def _batched_restore_stream(frames, cfg, writer, loader, devices, host_buffers,
                             batch) -> StreamReport:
     """read -> detect -> ordered_farm(restore) -> write for the 1:1 case with
-    fused detection, farmed at batch granularity: a feeder thread reads and
-    validates frames and groups up to `batch` consecutive same-shape frames;
-    two workers per GPU each upload a batch on their own stream, detect it
-    (amf_frames) and restore it (restore_frames: every frame its own loop in
-    one persistent launch) while the other worker's batch is read back and
-    the next one uploaded; the calling thread hands the frames to `writer`
-    in stream order.  Same report contract as run_stream: a frame whose
-    read / detection input / restore / write fails is a failure of that item
-    only; a failing source raises StreamError after the run drains."""
-    import queue
+    fused detection, farmed at batch granularity (streams.batch_farm): each
+    batch is detected (amf_frames) and restored (restore_frames: every frame
+    its own loop in one persistent launch) on one GPU."""
+    import numpy as np
 
-    import torch
+    def run_batch(d, stream):
+        masks, _ = amf_frames(d, cfg.amf_wmax, stream=stream)
+        outs, _reps = restore_frames(d, masks, cfg, stream=stream)
+        return outs
 
-    started = time.perf_counter()
-    rep = StreamReport()
-    names = ("read", "detect", "restore", "write")
-    stats = {n: StageStats(n) for n in names}
-    lock = threading.Lock()
-    ring = _HostRing() if (host_buffers and writer is not None) else None
-    jobs = queue.Queue(maxsize=2 * len(devices))
-    done = {}  # batch index -> list of (seq, grid or None, error or None)
-    cv = threading.Condition()
-    fed = [0]
-    source_error = [None]
-    nbatches = [None]
-
-    def busy(name, dt, n=1):
-        with lock:
-            stats[name].items += n
-            stats[name].busy_s += dt
-
-    def feeder():
-        bi, cur, shape = 0, [], None
-
-        def flush():
-            nonlocal bi, cur, shape
-            if cur:
-                jobs.put((bi, cur))
-                bi += 1
-            cur, shape = [], None
-
-        try:
-            for seq, item in enumerate(frames):
-                fed[0] = seq + 1
-                t0 = time.perf_counter()
-                try:
-                    img = loader(item) if loader is not None else item
-                    busy("read", time.perf_counter() - t0)
-                    t = _host_u8(img)
-                    entry = (seq, t, None)
-                except Exception as e:  # poisons this frame only
-                    entry = (seq, None, e)
-                if entry[1] is not None and shape is not None and tuple(entry[1].shape) != shape:
-                    flush()
-                if entry[1] is not None:
-                    shape = tuple(entry[1].shape)
-                cur.append(entry)
-                if len(cur) >= batch:
-                    flush()
-        except Exception as e:
-            source_error[0] = e
-        finally:
-            flush()
-            with cv:
-                nbatches[0] = bi
-                cv.notify_all()
-            for _ in range(2 * len(devices)):
-                jobs.put(None)
-
-    def worker(dev):
-        torch.cuda.set_device(dev)
-        stream = torch.cuda.Stream(device=dev)
-        while True:
-            job = jobs.get()
-            if job is None:
-                return
-            bi, entries = job
-            res = [(seq, None, err) for seq, _t, err in entries if err is not None]
-            good = [(seq, t) for seq, t, err in entries if err is None]
-            if good:
-                t0 = time.perf_counter()
-                try:
-                    with torch.cuda.stream(stream):
-                        H, W = good[0][1].shape
-                        d = torch.empty((len(good), H, W), dtype=torch.uint8, device=dev)
-                        for i, (_seq, t) in enumerate(good):
-                            d[i].copy_(t, non_blocking=True)
-                        masks, _ = amf_frames(d, cfg.amf_wmax, stream=stream)
-                        t1 = time.perf_counter()
-                        outs, _reps = restore_frames(d, masks, cfg, stream=stream)
-                        t2 = time.perf_counter()
-                        grids = []
-                        for o in outs:
-                            if ring is not None:
-                                h = ring.get(o.shape, o.dtype)
-                                h.copy_(o, non_blocking=True)
-                                g = Grid.from_tensor(h, logical_dtype=np.float64)
-                                grids.append((g, h))
-                            else:
-                                grids.append((Grid.from_tensor(o, logical_dtype=np.float64), None))
-                        stream.synchronize()
-                    if ring is None and writer is not None:
-                        for g, _h in grids:
-                            g.prefetch_host()
-                    busy("detect", t1 - t0, len(good))
-                    busy("restore", t2 - t1, len(good))
-                    res += [(seq, g, None, h) for (seq, _t), (g, h) in zip(good, grids)]
-                except Exception as e:  # the batch's frames all fail with it
-                    res += [(seq, None, e) for seq, _t in good]
-            res.sort(key=lambda r: r[0])
-            with cv:
-                done[bi] = res
-                cv.notify_all()
-
-    threads = [threading.Thread(target=feeder, daemon=True)]
-    for d in devices:
-        threads += [threading.Thread(target=worker, args=(d,), daemon=True) for _ in range(2)]
-    for t in threads:
-        t.start()
-    nxt = 0
-    while True:
-        with cv:
-            while nxt not in done and not (nbatches[0] is not None and nxt >= nbatches[0]):
-                cv.wait()
-            if nxt not in done:
-                break
-            res = done.pop(nxt)
-        nxt += 1
-        for r in res:
-            seq, g, err = r[0], r[1], r[2]
-            if err is not None:
-                rep.failures.append((seq, err))
-                continue
-            t0 = time.perf_counter()
-            try:
-                if writer is not None:
-                    writer(g)
-                rep.items_out += 1
-            except Exception as e:  # a failing write poisons its frame only
-                rep.failures.append((seq, e))
-            finally:
-                busy("write", time.perf_counter() - t0)
-                if len(r) > 3 and r[3] is not None:
-                    ring.put(r[3])
-    for t in threads:
-        t.join()
-    rep.items_in = fed[0]
-    rep.wall_s = time.perf_counter() - started
-    rep.stages = [stats[n] for n in names]
-    if source_error[0] is not None:
-        e = source_error[0]
-        raise StreamError(f"stream source failed: {e!r}") from e
-    return rep
+    return batch_farm(frames, _host_u8, run_batch, writer=writer, loader=loader,
+                      devices=devices, batch=batch, host_buffers=host_buffers,
+                      logical_dtype=np.float64, compute_name="restore")
 
 
 def video_restore_pipeline(frames: Iterable, *, width: int = 1, partitions: int = 1,
@@ -755,7 +589,7 @@ def video_restore_pipeline(frames: Iterable, *, width: int = 1, partitions: int 
     cap = int(os.environ.get("SK_BATCH_CAP", "0")) or max(1, -(-per_dev // 2))
     batchers = ({d: _RestoreBatcher(cfg, cap, detect=fused_detect, device=d)
                  for d in dict.fromkeys(devices)} if batched else {})
-    ring = _HostRing() if (host_buffers and writer is not None) else None
+    ring = _host_ring() if (host_buffers and writer is not None) else None
     held, held_lock = {}, threading.Lock()  # id(grid handed on) -> its pinned frame
 
     def detect_fn(img: Grid):

@@ -14,6 +14,7 @@ from typing import Optional
 
 from .. import _native as N
 from ..grid import Grid, GridError
+from ..streams import StreamReport, batch_farm
 from ..loop import stop_after
 from ..partition import DeploymentMode, WorkerGroup, parallel_loop
 from ..patterns import Combinator, DeviceKernel, DeviceUnsupported, ElementalFn
@@ -70,3 +71,51 @@ def sobel_frames(frames, out=None, stream=None):
                                 out.stride(0), F, H, W, C.c_void_p(sums.data_ptr()),
                                 N.stream_handle(st)))
     return out, sums
+
+
+def _frame_u8(img):
+    """One stream frame as a uint8 tensor (host or device), values checked
+    in [0, 255] like sobel_filter's input."""
+    import torch
+
+    from ..partition import _u8_from
+
+    if not isinstance(img, Grid):
+        raise GridError(f"frames must be grids, got {type(img).__name__}")
+    if img.ndim != 2:
+        raise GridError("sobel expects a 2D image")
+    t0 = img._t if img._src == "t" else None
+    if t0 is not None and t0.dtype == torch.uint8:
+        return t0
+    dev = img._t.device if img.is_device else torch.device("cpu")
+    return _u8_from(img, "sobel", 0, 255, dev)
+
+
+def sobel_stream(frames, *, writer=None, loader=None, width: int = 32, devices=None,
+                 host_buffers: bool = False, workers_per_device: int = 2) -> StreamReport:
+    """Stream mode of the Sobel filter (BASELINE C2): read -> ordered farm of
+    the batched Sobel (sobel_frames, one launch per batch of width/2 frames;
+    `workers_per_device` batches in flight per GPU, so uploads, launches and
+    read-backs overlap on both PCIe directions) -> write, in stream order
+    (streams.batch_farm).  Each frame is an 8-bit image Grid; the writer
+    receives its edge image (the same values sobel_filter returns) as a Grid
+    -- with host_buffers=True over a recycled pinned host frame filled by
+    one DMA (`g.tensor()` is that uint8 tensor, valid during the call)."""
+    import numpy as np
+    import torch
+
+    N.require_cuda()
+
+    def run_batch(d, stream):
+        n, h, w = d.shape
+        if w % 16:  # sobel_frames' row pitch: whole 16-byte vectors
+            p = torch.zeros((n, h, -(-w // 16) * 16), dtype=torch.uint8, device=d.device)
+            p[:, :, :w] = d
+            d = p[:, :, :w]
+        out, _sums = sobel_frames(d, stream=stream)
+        return [out[i] for i in range(n)]
+
+    return batch_farm(frames, _frame_u8, run_batch, writer=writer, loader=loader,
+                      devices=devices, batch=max(1, min(512, width // 2)),
+                      host_buffers=host_buffers, logical_dtype=np.int64, compute_name="sobel",
+                      workers_per_device=workers_per_device)

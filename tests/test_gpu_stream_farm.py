@@ -193,3 +193,37 @@ def test_video_pipeline_batched_farm_failures_shapes_loader(monkeypatch):
     assert len(g0) == len(g1)
     for a, b in zip(g0, g1):
         assert (a is None and b is None) or np.array_equal(a, b)
+
+
+def test_sobel_stream_order_failures_and_host_buffers():
+    """sobel_stream (C2 stream mode): frames in stream order through the
+    batched TMA Sobel, every output the oracle's, a bad frame failing alone,
+    pinned host buffers recycled."""
+    import torch
+
+    from oracle import stencil_oracle as O
+    from paper_1609_04567_b200.apps import sobel_stream
+
+    rng = np.random.default_rng(21)
+    imgs = [rng.integers(0, 256, (97, 333)).astype(np.uint8) for _ in range(9)]
+    imgs.insert(4, rng.integers(0, 256, (40, 2049)).astype(np.uint8))  # shape change mid-stream
+    src = [sk.Grid(a.shape, a) for a in imgs]
+    src.insert(6, sk.Grid.from_array(np.full((97, 333), 300, dtype=np.int64)))  # out of range
+    for hb in (False, True):
+        got, ptrs = [], set()
+
+        def writer(g):
+            if hb:
+                t = g.tensor()
+                assert t.is_pinned() and t.dtype == torch.uint8
+                ptrs.add(t.untyped_storage().data_ptr())
+            got.append(np.asarray(g.to_array()).astype(np.uint8))
+
+        rep = sobel_stream(src, writer=writer, width=4, host_buffers=hb)
+        assert rep.items_in == 11 and rep.items_out == 10 and [s for s, _ in rep.failures] == [6]
+        want = [O.sobel(a) for a in imgs]
+        assert len(got) == 10
+        for a, b in zip(got, want):
+            assert np.array_equal(a, b)
+        if hb:
+            assert len(ptrs) < 10
