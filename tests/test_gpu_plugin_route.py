@@ -70,3 +70,44 @@ def test_user_elemental_through_reference_drive(name):
     assert rep.iterations == m["iterations"] and rep.exhausted == m["exhausted"]
     assert rep.final_reduce == m["final_reduce"]
     assert np.array_equal(out.to_array(), arrays[name])
+
+
+def test_app_kernels_through_reference_drive():
+    """The hand-written app kernels (Sobel, adaptive-median detection,
+    variational restore) behind the reference's own host loop with our
+    executor: each equals the oracle's restatement of the reference, with
+    the reference's iteration count for the restore loop."""
+    from oracle import stencil_oracle as O
+    from paper_1609_04567_b200.apps import RestoreConfig, detect_kernel, restore_kernel, sobel_kernel
+
+    rng = np.random.default_rng(5)
+    img = rng.integers(0, 256, (61, 93))
+    grid = S.Grid(img.shape, img.ravel().tolist())
+    out, rep = S.loop_stencil_reduce(1, sobel_kernel, S.sum_combinator(0),
+                                     S.Condition(lambda v, it, s: it >= 1), grid,
+                                     executor=sk.DeviceExecutor(2))
+    want = O.sobel(img)
+    assert np.array_equal(np.asarray(out.to_array()).astype(np.uint8), want)
+    assert rep.iterations == 1 and rep.final_reduce == int(want.astype(np.int64).sum())
+
+    base = ((np.arange(48)[:, None] * 3 + np.arange(70)[None, :] * 2) % 200 + 20)
+    noisy, _ = O.salt_pepper(base, 0.3, seed=9)
+    g = S.Grid(noisy.shape, noisy.ravel().tolist())
+    mask, mrep = S.loop_stencil_reduce(3, detect_kernel(7), S.sum_combinator(0),
+                                       S.Condition(lambda v, it, s: it >= 1), g,
+                                       executor=sk.DeviceExecutor(1))
+    wm = O.amf_detect(noisy)
+    assert np.array_equal(np.asarray(mask.to_array()).astype(np.uint8), wm)
+    cfg = RestoreConfig()
+    denom = max(int(wm.sum()), 1)
+    mg = S.Grid(wm.shape, wm.astype(np.int64).ravel().tolist())
+    out, rep = S.loop_stencil_reduce_d(
+        1, restore_kernel(cfg), S.Delta(lambda a, b: abs(a - b)), S.sum_combinator(0.0),
+        S.Condition(lambda v, it, s: v / denom < cfg.tol, cfg.max_iterations),
+        S.Grid(noisy.shape, [float(v) for v in noisy.ravel()]), env=mg, indexed=True,
+        executor=sk.DeviceExecutor(2))
+    wo, it, v, ex = O.restore_loop(noisy, wm, P=2)
+    assert rep.iterations == it and rep.exhausted == ex
+    assert rep.final_reduce == pytest.approx(v, rel=1e-12)
+    assert np.array_equal(np.asarray(out.to_array(), dtype=np.float64).view(np.uint64),
+                          wo.view(np.uint64))
