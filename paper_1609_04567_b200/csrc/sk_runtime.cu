@@ -38,6 +38,24 @@ int device_sms(int device) {
   return cache[device];
 }
 
+// The runs' small and per-run buffers come from the device's default
+// stream-ordered pool (cudaMallocAsync).  Its release threshold defaults to
+// 0: every synchronisation hands unused pool memory back to the driver, so
+// a stream of runs (a farm restoring batch after batch) re-maps hundreds of
+// MB per batch.  Keep it: the threshold goes to the maximum once per device.
+void keep_pool(int device) {
+  static std::mutex mu;
+  static bool done[64] = {};
+  std::lock_guard<std::mutex> lk(mu);
+  if (device < 0 || device >= 64 || done[device]) return;
+  done[device] = true;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    unsigned long long thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+}
+
 unsigned* stream_counter(int device, cudaStream_t s) {
   constexpr int kSlab = 4096;
   static std::mutex mu;
@@ -332,6 +350,7 @@ int begin_impl(const sk_plan* plan, const sk_jit* jit, const void* d_src, int64_
       r->part_row[i + 1] = (int)b;
     }
   }
+  keep_pool(r->device);
   rc = r->ops->setup(r);
   if (rc) {
     delete r;
