@@ -754,6 +754,239 @@ __global__ void __launch_bounds__(BLOCK, 1) helm_resident(const __grid_constant_
   }
 }
 
+// ---- split-phase resident loop (MAX reduces; SK_RES_SPLIT=0 turns it off)
+// helm_resident with the grid step split into arrive and wait: after a band
+// publishes its edge rows and its partial for iteration t and arrives, it
+// computes the INTERIOR rows of t+1 -- they need only its own rows of t --
+// while the other bands arrive, then waits, loads the halo rows, decides,
+// and finishes t+1 with its first and last rows.  The grid step's latency
+// hides behind most of the next iteration's update.  If the loop stops at
+// t, the speculative rows are dropped and u(t) is written.  MAX reduces
+// only (order-free: the interior rows' deltas fold before the edge rows'),
+// every value op for op as helm_resident: bit-identical.
+template <int BLOCK, bool AMAX>
+__device__ __forceinline__ void res_arrive(const LoopCtl& L, long long it, double mine,
+                                           unsigned* cnt, double* parts, int nb, double* sh) {
+  const double v = block_reduce<BLOCK>(L.reduce, mine, sh);
+  double* slot = parts + (it & 1) * nb;
+  unsigned long long* amax = reinterpret_cast<unsigned long long*>(parts + 2 * nb);
+  if (threadIdx.x == 0) {
+    if (AMAX) {
+      atomicMax(&amax[it % 3], (unsigned long long)__double_as_longlong(v));
+      if (blockIdx.x == 0) amax[(it + 1) % 3] = 0ull;
+    } else {
+      slot[blockIdx.x] = v;
+    }
+    __threadfence();
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
+  }
+}
+
+template <int BLOCK, bool AMAX, class Pre>
+__device__ __forceinline__ int res_wait(const LoopCtl& L, long long it, unsigned* cnt,
+                                        double* parts, int nb, double* sh, const Pre& prefetch) {
+  __shared__ int s_stop;
+  if (threadIdx.x == 0) {
+    const unsigned want = (unsigned)(nb * it);
+    unsigned seen;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(cnt) : "memory");
+    } while ((int)(seen - want) < 0);
+  }
+  __syncthreads();
+  prefetch();
+  const OpCombine comb{L.reduce};
+  double acc = L.identity;
+  double* slot = parts + (it & 1) * nb;
+  unsigned long long* amax = reinterpret_cast<unsigned long long*>(parts + 2 * nb);
+  if (AMAX) {
+    if (threadIdx.x == 0)
+      acc = comb.fold(acc, __longlong_as_double((long long)__ldcg(&amax[it % 3])));
+  } else {
+    const double neutral = comb.neutral(L.identity);
+    for (int p = 0; p < L.nparts; ++p) {
+      double t = neutral;
+      for (int c = L.part_chunk[p] + (int)threadIdx.x; c < L.part_chunk[p + 1]; c += BLOCK)
+        t = comb(t, __ldcg(&slot[c]));
+      const double pv = block_reduce_c<BLOCK>(comb, neutral, t, sh);
+      if (threadIdx.x == 0) acc = comb.fold(acc, pv);
+    }
+  }
+  if (threadIdx.x == 0) {
+    const int c = eval_cond(L.cond, acc, it, L.flagged_dev);
+    const int capped = it >= L.cond.max_it;
+    const int stop = c || capped;
+    if (stop && blockIdx.x == 0) {
+      Status* st = L.st;
+      st->value = acc;
+      st->cond_true = c;
+      st->exhausted = !c && capped;
+      st->iter = it;
+      st->stop = 1;
+      __threadfence();
+    }
+    s_stop = stop;
+  }
+  __syncthreads();
+  return s_stop;
+}
+
+template <typename T, int BLOCK, int VEC, int RMAX, int DELTA>
+__global__ void __launch_bounds__(BLOCK, 1) helm_resident_split(const __grid_constant__ HelmArgs<T> a,
+                                                                T* xbuf, unsigned* cnt, double* parts) {
+  constexpr unsigned FULL = 0xffffffffu;
+  constexpr int NW = BLOCK / 32;
+  __shared__ double sh[NW];
+  // warp-edge columns, double-buffered by iteration parity: a band's warps
+  // read parity t while the fastest may already write parity t+1
+  __shared__ T s_edge[2][RMAX][2][NW];
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  T* s_f = reinterpret_cast<T*>(s_dyn);
+  const Sweep2D& g = a.g;
+  long long it = loop_enter(a.L);
+  if (it == 0) return;
+  const int cols = g.cols, rows = g.rows;
+  int cb, r0, r1;
+  chunk_geom(a.L, g, blockIdx.x, &cb, &r0, &r1);
+  const int R = r1 - r0;
+  const int nb = gridDim.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int col = threadIdx.x * VEC;
+  const int nvalid = cols - col;
+  const bool active = nvalid > 0;
+  const T rb = rcp_rn(a.b);
+  const bool fast = a.fast_div != 0;
+  const bool top_zero = !g.halo_top, bot_zero = !g.halo_bottom;
+  constexpr bool kAmax = DELTA != SK_DELTA_NONE;  // MAX of a non-negative delta
+
+  VecN<T, VEC> u[RMAX], w[RMAX];
+  const T* src = static_cast<const T*>(g.src) + (long long)g.halo_top * g.src_pitch;
+  const T* env = static_cast<const T*>(g.env) + (long long)g.halo_top * g.env_pitch;
+#pragma unroll
+  for (int r = 0; r < RMAX; ++r) {
+    u[r] = (active && r < R) ? ldgN<T, VEC>(src + (long long)(r0 + r) * g.src_pitch + col) : zeroN<T, VEC>();
+    w[r] = u[r];
+    if (active && r < R) {
+      const VecN<T, VEC> fv = ldgN<T, VEC>(env + (long long)(r0 + r) * g.env_pitch + col);
+#pragma unroll
+      for (int e = 0; e < VEC; ++e)
+        if (e < nvalid) s_f[r * cols + col + e] = fv.v[e];
+    }
+  }
+  VecN<T, VEC> up = (active && !(r0 == 0 && top_zero)) ? ldgN<T, VEC>(src + (long long)(r0 - 1) * g.src_pitch + col)
+                                                   : zeroN<T, VEC>();
+  VecN<T, VEC> dn = (active && !(r1 == rows && bot_zero)) ? ldgN<T, VEC>(src + (long long)r1 * g.src_pitch + col)
+                                                      : zeroN<T, VEC>();
+  T accm = -INFINITY;
+  int sp = (int)((it - 1) & 1);  // s_edge slot of the state being updated: u(t) -> t & 1
+  auto update = [&](int r, const VecN<T, VEC>& cen, const VecN<T, VEC>& above,
+                    const VecN<T, VEC>& below) {
+    T lv = __shfl_up_sync(FULL, cen.v[VEC - 1], 1);
+    T rv = __shfl_down_sync(FULL, cen.v[0], 1);
+    if (lane == 0) lv = warp > 0 ? s_edge[sp][r][1][warp - 1] : T(0);
+    if (lane == 31) rv = warp + 1 < NW ? s_edge[sp][r][0][warp + 1] : T(0);
+    VecN<T, VEC> o;
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+      const T l = e == 0 ? lv : cen.v[e - 1];
+      T rt = e == VEC - 1 ? rv : cen.v[e + 1];
+      if (e + 1 >= nvalid) rt = T(0);
+      const T fv = active && e < nvalid ? s_f[r * cols + col + e] : T(0);
+      const T out = helm_update(cen.v[e], l, rt, above.v[e], below.v[e], fv, a, rb, fast);
+      const bool in = e < nvalid;
+      o.v[e] = in ? out : T(0);
+      T d;
+      if (DELTA == SK_DELTA_ABS) {
+        d = tabs(xsub(out, cen.v[e]));
+      } else if (DELTA == SK_DELTA_SQUARE) {
+        const T t = xsub(out, cen.v[e]);
+        d = xmul(t, t);
+      } else {
+        d = out;
+      }
+      if (in) accm = max_nan(accm, d);
+    }
+    return o;
+  };
+  auto sedge = [&]() {  // warp-edge columns of u for the horizontal neighbours
+#pragma unroll
+    for (int r = 0; r < RMAX; ++r) {
+      if (r < R) {
+        if (lane == 0) s_edge[sp][r][0][warp] = u[r].v[0];
+        if (lane == 31) s_edge[sp][r][1][warp] = u[r].v[VEC - 1];
+      }
+    }
+  };
+  // interior rows 1 .. R-2 of the next iteration into w (own rows only)
+  auto interior = [&]() {
+#pragma unroll
+    for (int r = 1; r < RMAX - 1; ++r)
+      if (r < R - 1) w[r] = update(r, u[r], u[r - 1], u[r + 1]);
+  };
+  // first and last rows (the halo rows up / dn), then w becomes u
+  auto edges = [&]() {
+    w[0] = update(0, u[0], up, R > 1 ? u[RMAX > 1 ? 1 : 0] : dn);
+#pragma unroll
+    for (int r = 1; r < RMAX; ++r)
+      if (r == R - 1) w[r] = update(r, u[r], u[r - 1], dn);
+#pragma unroll
+    for (int r = 0; r < RMAX; ++r) u[r] = w[r];
+  };
+  // iteration `it` (normally 1) in full
+  sedge();
+  __syncthreads();
+  interior();
+  edges();
+  for (;;) {
+    sp = (int)(it & 1);  // u holds u(it)
+    if (active) {  // this band's edge rows of `it` for the neighbours
+      T* x = xbuf + ((long long)((it & 1) * nb + blockIdx.x) * 2) * a.xpitch;
+      stN<T, VEC>(x + col, u[0]);
+#pragma unroll
+      for (int r = 0; r < RMAX; ++r)
+        if (r == R - 1) stN<T, VEC>(x + a.xpitch + col, u[r]);
+    }
+    sedge();  // made visible by the block reduce's barriers
+    const bool amax = kAmax && a.L.nparts == 1;
+    if (amax) res_arrive<BLOCK, true>(a.L, it, (double)accm, cnt, parts, nb, sh);
+    else res_arrive<BLOCK, false>(a.L, it, (double)accm, cnt, parts, nb, sh);
+    accm = -INFINITY;
+    interior();  // speculative: iteration it+1's own rows, while the grid arrives
+    const long long cur = it;
+    auto prefetch = [&]() {
+      if (!active) return;
+      const T* xb = xbuf + (long long)((cur & 1) * nb) * 2 * a.xpitch;
+      if (blockIdx.x > 0 && !(r0 == 0)) {
+        const T* p = xb + ((long long)(blockIdx.x - 1) * 2 + 1) * a.xpitch + col;
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) up.v[e] = __ldcg(p + e);
+      } else {
+        up = zeroN<T, VEC>();
+      }
+      if (r1 < rows) {
+        const T* p = xb + ((long long)(blockIdx.x + 1) * 2) * a.xpitch + col;
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) dn.v[e] = __ldcg(p + e);
+      } else {
+        dn = zeroN<T, VEC>();
+      }
+    };
+    const int stop = amax ? res_wait<BLOCK, true>(a.L, it, cnt, parts, nb, sh, prefetch)
+                          : res_wait<BLOCK, false>(a.L, it, cnt, parts, nb, sh, prefetch);
+    if (stop) {  // iteration `it` is the result (the speculative rows are dropped)
+      if (active) {
+        T* out = static_cast<T*>(g.buf[it & 1]) + (long long)g.halo_top * g.pitch;
+#pragma unroll
+        for (int r = 0; r < RMAX; ++r)
+          if (r < R) stN<T, VEC>(out + (long long)(r0 + r) * g.pitch + col, u[r]);
+      }
+      return;
+    }
+    edges();
+    ++it;
+  }
+}
+
 #include "sk_helm_tma.cuh"
 
 // ---------------------------------------------------------------- host side
@@ -837,8 +1070,25 @@ constexpr int kResRows = 8;  // RMAX: rows per band (registers)
 template <typename T>
 using ResFn = void (*)(const HelmArgs<T>, T*, unsigned*, double*);
 
+bool res_split() {
+  static const bool v = [] {
+    const char* e = getenv("SK_RES_SPLIT");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
 template <typename T, int BLOCK, int VEC>
 ResFn<T> pick_res_b(int delta, int reduce) {
+  // (1024-thread bands would spill the doubled row state at 64 registers)
+  if constexpr (BLOCK <= 512) {
+    if (reduce == SK_REDUCE_MAX && res_split()) {
+      if (delta == SK_DELTA_NONE) return helm_resident_split<T, BLOCK, VEC, kResRows, SK_DELTA_NONE>;
+      if (delta == SK_DELTA_ABS) return helm_resident_split<T, BLOCK, VEC, kResRows, SK_DELTA_ABS>;
+      if (delta == SK_DELTA_SQUARE)
+        return helm_resident_split<T, BLOCK, VEC, kResRows, SK_DELTA_SQUARE>;
+    }
+  }
 #define SK_R(D, R) \
   if (delta == D && reduce == R) return helm_resident<T, BLOCK, VEC, kResRows, D, R>;
   SK_R(SK_DELTA_NONE, SK_REDUCE_SUM)
