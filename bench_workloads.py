@@ -27,31 +27,51 @@ def fp64_peak():
     return 18.5e12, 1.25e12, "fallback (nominal)"
 
 
-# Per active flagged pixel and iteration the restore search does 18 steps x 2
-# evaluations of F, each 8 ring terms of (sub, mul, add, sqrt, mul, add) plus
-# beta*s, plus the step bookkeeping: ~1550 DP add/mul + 288 IEEE sqrt.  In
-# DFMA-equivalents (one IEEE DSQRT costs dfma_rate / dsqrt_rate of them):
+# Per active flagged pixel and iteration the reference's search does 18 steps
+# x 2 evaluations of F, each 8 ring terms of (sub, mul, add, sqrt, mul, add)
+# plus beta*s, plus the step bookkeeping: ~1550 DP add/mul + 288 IEEE sqrt
+# (SURVEY.md 8(d)).  In DFMA-equivalents (one IEEE DSQRT costs
+# dfma_rate / dsqrt_rate of them):
 RESTORE_DP_OPS = 1550
 RESTORE_SQRT = 288
+SM_MAX_HZ = 1.965e9  # B200 boost clock (the bench's clocks line reports the live one)
 
 
-def restore_roofline(flagged, t_iter1_ms):
+def restore_roofline(flagged, t_iter1_ms, workload):
+    """Roofline of restore iteration 1 (every flagged pixel active).
+
+    The kernel certifies most ternary-search comparisons with an exact fp32
+    bracket and evaluates only the rest in fp64 (sk_restore.cu), so it no
+    longer executes the reference's fp64 work: its limiter is instruction
+    issue.  Reported: the issue roofline (warp instructions per flagged
+    pixel from the committed ncu capture, profiles/restore_counts.json, over
+    the live CUDA-event time of the launch) as the headline; beside it the
+    fp64 pipe fraction the kernel executes and the reference-equivalent fp64
+    rate (the reference's per-pixel work over the same time: > 1 means the
+    exact filter saved more fp64 work than the pipe could have done)."""
     dfma, dsq, src = fp64_peak()
     eq = RESTORE_DP_OPS + RESTORE_SQRT * dfma / dsq
-    achieved = flagged * eq / (t_iter1_ms / 1e3)
-    return {"bound": "fp64", "achieved": achieved / 1e12, "peak": dfma / 1e12,
-            "unit": "TDFMA-eq/s", "frac": achieved / dfma, "traffic": None,
+    cnt = json.load(open(os.path.join(ROOT, "profiles", "restore_counts.json")))[workload]
+    t = t_iter1_ms / 1e3
+    issue_peak = 148 * 4 * SM_MAX_HZ  # warp instructions / s (one per scheduler per clock)
+    issued = flagged * cnt["warp_inst_per_pixel"] / t
+    return {"bound": "issue", "achieved": issued / 1e9, "peak": issue_peak / 1e9,
+            "unit": "Gwarp-inst/s", "frac": issued / issue_peak, "traffic": None,
             "kernel": "restore_sweep (iteration 1: every flagged pixel active)",
-            "work_per_unit": f"{eq:.0f} DFMA-eq per flagged pixel-iteration "
-                             f"({RESTORE_DP_OPS} DP add/mul + {RESTORE_SQRT} DSQRT)",
-            "avg_kernel_ms": t_iter1_ms, "peak_source": src,
-            # the DFMA-equivalent count above is a calibrated model (DSQRT
-            # converted at the measured DFMA/DSQRT rate ratio); the hardware
-            # counter beside it: the FP64 pipe is busy 70% of the kernel's
-            # cycles (profiles/r01c_ncu_restore.json), the remainder being the
-            # DSQRT iterations' non-FP64 instructions and the loop's barriers
-            "fp64_pipe_active": 0.70,
-            "fp64_pipe_source": "ncu sm__pipe_fp64_cycles_active, profiles/r01c_ncu_restore.json"}
+            "work_per_unit": f"{cnt['warp_inst_per_pixel']} warp instructions per flagged "
+                             f"pixel-iteration (ncu, profiles/restore_counts.json)",
+            "avg_kernel_ms": t_iter1_ms,
+            "peak_source": "148 SMs x 4 schedulers x 1 warp-instruction/clock at 1965 MHz",
+            "issue_active_ncu": cnt["issue_active"],
+            "fp64_executed": {"dp_inst_per_pixel": cnt["dp_inst_per_pixel"],
+                              "frac": flagged * cnt["dp_inst_per_pixel"] / t / dfma,
+                              "pipe_active_ncu": cnt["fp64_pipe_active"]},
+            "fp64_reference_equivalent": {
+                "work_per_unit": f"{eq:.0f} DFMA-eq per flagged pixel-iteration "
+                                 f"({RESTORE_DP_OPS} DP add/mul + {RESTORE_SQRT} DSQRT, the "
+                                 f"reference's search)",
+                "achieved": flagged * eq / t / 1e12, "peak": dfma / 1e12, "unit": "TDFMA-eq/s",
+                "frac": flagged * eq / t / dfma, "peak_source": src}}
 
 
 def _traffic(key, units=1):
@@ -403,7 +423,7 @@ def c3(args, ClockSampler, measured_peaks, local=0):
         "gpu_launches": None,
         "e2e": {"value": 1.0 / e2e_s, "unit": "images/s", "h2d_bytes_per_step": noisy.size,
                 "d2h_bytes_per_step": 8 * noisy.size},
-        "roofline": restore_roofline(flagged, t1),
+        "roofline": restore_roofline(flagged, t1, "c3"),
         "cpu_baseline": {"value": 1.0 / cpu_s, "unit": "images/s", "cores": 1, "kind": "port",
                          "sample": "oracle AMF + 3 restore sweeps on a 1024^2 image "
                                    "(same generator), extrapolated to 4096^2 x 100 iterations "
@@ -551,7 +571,7 @@ def c5(args, ClockSampler, measured_peaks, local=0, world=1, rank=0, width=32):
                         f"ordered farm at batch granularity (2 workers per GPU, batches of "
                         f"{max(1, width // 2)}), fp64 results DMA'd into recycled pinned host "
                         f"frames handed to the writer in stream order"},
-        "roofline": restore_roofline(int(counts.sum()), t1),
+        "roofline": restore_roofline(int(counts.sum()), t1, "c5"),
         "cpu_baseline": cpu_line,
         "clocks": clk.summary(),
     })

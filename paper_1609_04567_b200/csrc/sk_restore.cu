@@ -8,12 +8,16 @@
 // minimise F(u) = beta * sum_ring w * sqrt((u - v)^2 + eps), with w = 1 for a
 // flagged neighbour, 2 for a clean one, and off-image neighbours skipped (the
 // block route's weight-0 terms add +0.0, which leaves the sum unchanged).
-// Clean pixels never change.  All arithmetic is fp64 in the reference's
-// order with round-to-nearest intrinsics and IEEE sqrt; (hi - lo) / 3.0 uses
-// the exact 3-op division by a constant.  Result: bit-identical grids.
+// Clean pixels never change.  Every value the reference computes is computed
+// in fp64 in the reference's order with round-to-nearest intrinsics and IEEE
+// sqrt; (hi - lo) / 3.0 uses the exact 3-op division by a constant.  Result:
+// bit-identical grids.
 //
-// FP64-pipe-bound (~1.5k flops + 288 sqrt per pixel-iteration), so work is
-// cut exactly, not approximately:
+// The reference's search costs ~1.5k fp64 flops + 288 sqrt per pixel-
+// iteration; work is cut exactly, not approximately:
+//  * comparison filter: most F(m1) <= F(m2) outcomes are certified by an
+//    fp32 bracket of both sides (bound_decide); only the others are
+//    evaluated in fp64, compacted per warp (restore_sweep, phase 2).
 //  * flagged list: only flagged pixels are visited (built once per run by a
 //    deterministic count/scan/scatter; in pixel order, so each partition's
 //    pixels are a contiguous sub-range).
@@ -62,40 +66,123 @@ struct FrameStat {
 // F(u) = beta * sum over the 8 ring terms, in ring order, of w * sqrt((u-v)^2 + eps).
 // Off-image neighbours carry weight 0 exactly as in the block route
 // (apps/denoise.py:230-233): they add +0.0, which leaves the sum unchanged.
-__device__ __forceinline__ double F_eval(double u, const double (&v)[8], const double (&w)[8],
-                                         double eps, double beta) {
-  double s = 0.0;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const double t = xsub(u, v[k]);
-    s = xadd(s, xmul(w[k], xsqrt(xadd(xmul(t, t), eps))));
-  }
-  return xmul(beta, s);
-}
+// Each term w * sqrt((u - v)^2 + eps) is an independent fp64 product and the
+// owner adds its pixel's 8 terms in ring order -- the reference's sum -- so
+// the terms may be computed by any lane (restore_sweep, phase 2).
 
-__device__ double restore_pixel(const RestoreArgs& a, const double* front, long long fp, int i,
-                                int j, int rlo, int rhi) {
-  double v[8], w[8];
+// ---- exact comparison filter.  The search only needs the OUTCOME of
+// F(m1) <= F(m2) per step, F = fl(beta * S), S = sum_k w_k g(u - v_k),
+// g(t) = sqrt(t^2 + eps).  Since |t| <= g(t) <= |t| + min(sqrt(eps),
+// eps / (2|t|)), fp32 sums of w|t| bracket S with a provable slack; when the
+// brackets of S(m1) and S(m2) do not overlap the outcome is known exactly
+// (beta > 0, rounding is monotone, and the gap dwarfs fp64 rounding), and
+// only overlapping (close) comparisons evaluate F in fp64.  Results stay
+// bit-identical; SK_RESTORE_FILTER=0 at build time evaluates every step.
+//
+// Bracket, per pixel and side (a_k = |fl32(u32 - v32_k)|, u32 / v32_k the
+// fp32 roundings of u / v_k):
+//   | |t_k| - a_k | <= et = 2^-22 (256 + max_k |v32_k|)      (u in [0, 255])
+//   L = sum w_k a_k (fp32, rel. error < 2^-20),  W = sum w_k
+//   y_k = the fp32 with bits 0x7F000000 - bits(a_k) = 2^-E (1.5 - m/2) for
+//       a_k = 2^E m, m in [1, 2): the chord of the convex 1/m, so
+//       1/a_k <= y_k <= 1.125/a_k (one integer subtraction)
+//   C = sum w_k min(sqrt_eps, eps/2 * y_k):  when a_k >= 64 et,
+//       eps/(2|t_k|) <= eps/(2(a_k - et)) <= (64/63) eps/2 * y_k; below that
+//       eps/2 * y_k > eps/(128 et) >= sqrt(eps) (the filter is on only when
+//       128 et <= sqrt(eps)) and the min is sqrt_eps: (64/63) C bounds the
+//       slack sum (fp32 rounding included: factor 1 + 2^-5 below).
+//   L - W et - 2^-20 L  <=  S  <=  L + (1 + 2^-5) C + W et + 2^-20 L
+// S1 < S2 is certain when fl(L1 + C1' + 3 W et + 2^-18 (L1 + C1' + L2)) < L2,
+// C1' = (1 + 2^-5) C1 (the extra margin absorbs that expression's rounding).
+#ifndef SK_RESTORE_FILTER
+#define SK_RESTORE_FILTER 1
+#endif
+constexpr bool kFilter = SK_RESTORE_FILTER != 0;
+// Warp-level compaction of the exact comparisons: a warp's 32 lanes run 32
+// pixels' searches in lockstep; when k lanes of a warp are left undecided by
+// the filter, their 16 k terms (k comparisons x 2 sides x 8 ring terms) are
+// spread over the warp's 32 lanes (ceil(k / 2) terms per lane) and each
+// owner adds up its own terms; only when many lanes are undecided (k >
+// kDirect) does every undecided lane evaluate its own comparison.  Ring
+// values, weights and terms live in shared memory so that any lane can
+// compute any term; rows are padded to odd lengths (bank spread).
+#ifndef SK_RESTORE_DIRECT
+#define SK_RESTORE_DIRECT 12
+#endif
+constexpr int kDirect = SK_RESTORE_DIRECT;
+static_assert(kDirect >= 1 && kDirect <= 32, "SK_RESTORE_DIRECT must be in [1, 32]");
+constexpr int kRingPad = 9;  // doubles per ring row
+constexpr int kTermPad = 17; // doubles per term row (2 x 8 + 1)
+#ifndef SK_RESTORE_MINB
+#define SK_RESTORE_MINB 8
+#endif
+constexpr int kMinBlocks = SK_RESTORE_MINB;  // resident CTAs per SM (register cap)
+
+struct Ring {
+  float v32[8], wf[8];
+  float wet3;   // 3 W et, rounded up
+  bool fil;     // the bound filter applies to this pixel
+};
+
+__device__ __forceinline__ void load_ring(const RestoreArgs& a, const double* front, long long fp,
+                                          int i, int j, int rlo, int rhi, float sqrt_eps_dn,
+                                          double (*ring)[kRingPad],
+                                          unsigned short (*whi)[kRingPad], Ring& r) {
+  float vmax = 0.0f, wsum = 0.0f;
+  bool finite = true;
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
-    const int di = k < 3 ? -1 : (k < 5 ? 0 : 1);               // _RING order
+    const int di = k < 3 ? -1 : (k < 5 ? 0 : 1);  // _RING order
     const int dj = k < 3 ? k - 1 : (k < 5 ? (k == 3 ? -1 : 1) : k - 6);
     const int ni = i + di, nj = j + dj;
     const bool in = ni >= rlo && ni < rhi && nj >= 0 && nj < a.cols;
-    v[k] = in ? front[(long long)ni * fp + nj] : 0.0;
-    w[k] = in ? (a.mask[(long long)ni * a.mask_pitch + nj] == 1 ? 1.0 : 2.0) : 0.0;
+    const double v = in ? front[(long long)ni * fp + nj] : 0.0;
+    ring[threadIdx.x][k] = v;
+    const bool flagged = in && a.mask[(long long)ni * a.mask_pitch + nj] == 1;
+    r.wf[k] = in ? (flagged ? 1.0f : 2.0f) : 0.0f;
+    whi[threadIdx.x][k] = in ? (flagged ? 0x3FF0 : 0x4000) : 0;  // 1.0 / 2.0 / 0.0, bits 48-63
+    r.v32[k] = __double2float_rn(v);
+    finite = finite && isfinite(r.v32[k]);
+    vmax = fmaxf(vmax, fabsf(r.v32[k]));
+    wsum += r.wf[k];
   }
-  const double r3 = __drcp_rn(3.0);
-  double lo = 0.0, hi = 255.0;
-#pragma unroll 1
-  for (int s = 0; s < kSteps; ++s) {
-    const double third = div_const(xsub(hi, lo), 3.0, r3);
-    const double m1 = xadd(lo, third);
-    const double m2 = xsub(hi, third);
-    if (F_eval(m1, v, w, a.eps, a.beta) <= F_eval(m2, v, w, a.eps, a.beta)) hi = m2;
-    else lo = m1;
+  const float et = __fmul_ru(__fadd_ru(256.0f, vmax), 1.0f / 4194304.0f);  // 2^-22
+  r.wet3 = __fmul_ru(__fmul_ru(3.0f, wsum), et);
+  r.fil = kFilter && finite && __fmul_ru(128.0f, et) <= sqrt_eps_dn;
+}
+
+// 1: F(m1) <= F(m2) certainly, 0: F(m1) > F(m2) certainly, -1: undecided.
+// Only the side with the smaller L can be certified smaller, so the slack
+// is summed for that side alone, as eps/2 * sum w min(kq, y) with
+// kq >= sqrt_eps / (eps/2) (one min and one FMA per term).
+__device__ __forceinline__ int bound_decide(float u1, float u2, const Ring& r, float kq,
+                                            float eh) {
+  // two partial sums per side halve the dependent FMA chains (any order of
+  // the 8 non-negative terms keeps the 2^-20 bound)
+  float l1a = 0.0f, l1b = 0.0f, l2a = 0.0f, l2b = 0.0f;
+#pragma unroll
+  for (int k = 0; k < 8; k += 2) {
+    l1a = fmaf(r.wf[k], fabsf(u1 - r.v32[k]), l1a);
+    l2a = fmaf(r.wf[k], fabsf(u2 - r.v32[k]), l2a);
+    l1b = fmaf(r.wf[k + 1], fabsf(u1 - r.v32[k + 1]), l1b);
+    l2b = fmaf(r.wf[k + 1], fabsf(u2 - r.v32[k + 1]), l2b);
   }
-  return xmul(0.5, xadd(lo, hi));
+  const float l1 = l1a + l1b, l2 = l2a + l2b;
+  const bool one = l1 <= l2;
+  const float us = one ? u1 : u2, ls = one ? l1 : l2, lb = one ? l2 : l1;
+  float ca = 0.0f, cb = 0.0f;
+#pragma unroll
+  for (int k = 0; k < 8; k += 2) {
+    const float ya = __int_as_float(0x7F000000 - __float_as_int(fabsf(us - r.v32[k])));  // >= 1/a
+    const float yb = __int_as_float(0x7F000000 - __float_as_int(fabsf(us - r.v32[k + 1])));
+    ca = fmaf(r.wf[k], fminf(kq, ya), ca);
+    cb = fmaf(r.wf[k + 1], fminf(kq, yb), cb);
+  }
+  float c = ca + cb;
+  c = __fmul_ru(c, eh);  // eh >= (1 + 2^-5) eps / 2
+  constexpr float kRel = 1.0f / 262144.0f;  // 2^-18
+  if (ls + c + r.wet3 + kRel * (ls + c + lb) < lb) return one ? 1 : 0;
+  return -1;
 }
 
 // Cross-frame barrier for batched restores: the last CTA folds every active
@@ -158,12 +245,26 @@ __device__ long long frames_barrier(const RestoreArgs& a, long long it, double* 
 }
 
 template <bool FRAMES>
-__global__ void __launch_bounds__(kRB, 6) restore_sweep(const __grid_constant__ RestoreArgs a) {
+__global__ void __launch_bounds__(kRB, kMinBlocks) restore_sweep(const __grid_constant__ RestoreArgs a) {
   __shared__ double sh[kRB / 32];
   __shared__ double s_delta[kCh];
   __shared__ short s_queue[kCh];
   __shared__ int s_qlen;
+  __shared__ int s_take;
+  __shared__ double s_ring[kRB][kRingPad];  // ring values of the round's pixels
+  __shared__ unsigned short s_whi[kRB][kRingPad];  // their weights (top 16 bits)
+  __shared__ double s_m[kRB][2];            // m1, m2 of undecided comparisons
+  __shared__ double s_T[kRB / 32 * kDirect][kTermPad];  // their terms, by rank
+  __shared__ unsigned char s_xq[kRB];       // undecided lanes, per warp
   __shared__ int s_chunk;
+  // bound-filter constants (see bound_decide); off unless beta > 0, eps >= 0
+  const bool fil_ok = kFilter && a.beta > 0.0 && a.eps >= 0.0 && isfinite(a.beta) &&
+                      isfinite(a.eps);
+  const float sqrt_eps_dn = fil_ok ? __fsqrt_rd(__double2float_rd(a.eps)) : -1.0f;
+  const float eps_half_up = __double2float_ru(xmul(a.eps, 0.5));
+  const float kq = __fdiv_ru(__fsqrt_ru(__double2float_ru(a.eps)), eps_half_up);
+  const float eh = __fmul_ru(eps_half_up, 1.03125f);
+  const double r3 = __drcp_rn(3.0);
   for (long long it = loop_enter(a.L); it != 0;
        it = FRAMES ? frames_barrier(a, it, sh) : loop_next<kRB>(a.L, it, sh)) {
   const double* front = it == 1 ? a.src : a.buf[(it - 1) & 1];
@@ -184,7 +285,10 @@ __global__ void __launch_bounds__(kRB, 6) restore_sweep(const __grid_constant__ 
     const int rhi = FRAMES ? rlo + a.frame_rows : a.rows;
     const int e0 = a.part_off[p] + (c - pch[p]) * kCh;
     const int e1 = min(e0 + kCh, a.part_off[p + 1]);
-    if (threadIdx.x == 0) s_qlen = 0;
+    if (threadIdx.x == 0) {
+      s_qlen = 0;
+      s_take = 0;
+    }
     __syncthreads();
     // phase 1: classify; inactive entries are settled immediately
 #pragma unroll
@@ -220,18 +324,96 @@ __global__ void __launch_bounds__(kRB, 6) restore_sweep(const __grid_constant__ 
       }
     }
     __syncthreads();
-    // phase 2: drain the active queue (any thread may take any entry; each
-    // result and |delta| goes to the entry's own position)
+    // phase 2: each warp drains the active queue 32 entries at a time, one
+    // per lane, independently of the other warps (a result and its |delta|
+    // go to the entry's own position)
     const int qlen = s_qlen;
-    for (int q = threadIdx.x; q < qlen; q += kRB) {
-      const int pos = s_queue[q];
-      const int pix = a.list[e0 + pos];
-      const int i = pix / a.cols, j = pix - i * a.cols;
-      const double old = front[(long long)i * fp + j];
-      const double nv = restore_pixel(a, front, fp, i, j, rlo, rhi);
-      back[(long long)i * a.pitch + j] = nv;
-      ccur[pix] = nv != old;
-      s_delta[pos] = fabs(xsub(nv, old));
+    for (;;) {
+      int base = 0;
+      if ((threadIdx.x & 31) == 0) base = atomicAdd(&s_take, 32);
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (base >= qlen) break;
+      const int q = base + (int)(threadIdx.x & 31);
+      const bool has = q < qlen;
+      int pos = 0, pix = 0;
+      double lo = 0.0, hi = 255.0, old = 0.0;
+      Ring r;
+      r.fil = false;
+      if (has) {
+        pos = s_queue[q];
+        pix = a.list[e0 + pos];
+        const int i = pix / a.cols, j = pix - i * a.cols;
+        old = front[(long long)i * fp + j];
+        load_ring(a, front, fp, i, j, rlo, rhi, sqrt_eps_dn, s_ring, s_whi, r);
+      }
+#pragma unroll 1
+      for (int step = 0; step < kSteps; ++step) {
+        const double third = div_const(xsub(hi, lo), 3.0, r3);
+        const double m1 = xadd(lo, third);
+        const double m2 = xsub(hi, third);
+        int d = 1;
+        if (has) {
+          d = r.fil ? bound_decide(__double2float_rn(m1), __double2float_rn(m2), r, kq, eh) : -1;
+        }
+        const bool und = d < 0;
+        const unsigned bal = __ballot_sync(0xffffffffu, und);
+        bool le = d != 0;
+        if (bal) {
+          const int k = __popc(bal);
+          const unsigned lane = threadIdx.x & 31;
+          const int wb = threadIdx.x & ~31;  // this warp's first slot
+          if (k > kDirect) {
+            if (und) {
+              double s1 = 0.0, s2 = 0.0;
+#pragma unroll 2
+              for (int kk = 0; kk < 8; ++kk) {
+                const double v = s_ring[threadIdx.x][kk];
+                const double w = __hiloint2double((int)s_whi[threadIdx.x][kk] << 16, 0);
+                const double t1 = xsub(m1, v), t2 = xsub(m2, v);
+                s1 = xadd(s1, xmul(w, xsqrt(xadd(xmul(t1, t1), a.eps))));
+                s2 = xadd(s2, xmul(w, xsqrt(xadd(xmul(t2, t2), a.eps))));
+              }
+              le = xmul(a.beta, s1) <= xmul(a.beta, s2);
+            }
+          } else {
+            const int tb = (wb >> 5) * kDirect;  // this warp's term rows
+            const int rank = __popc(bal & ((1u << lane) - 1u));
+            if (und) {
+              s_xq[wb + rank] = (unsigned char)threadIdx.x;
+              s_m[threadIdx.x][0] = m1;
+              s_m[threadIdx.x][1] = m2;
+            }
+            __syncwarp();
+            for (int x = lane; x < 16 * k; x += 32) {
+              const int p = s_xq[wb + (x >> 4)], side = (x >> 3) & 1, kk = x & 7;
+              const double t = xsub(s_m[p][side], s_ring[p][kk]);
+              s_T[tb + (x >> 4)][side * 8 + kk] =
+                  xmul(__hiloint2double((int)s_whi[p][kk] << 16, 0), xsqrt(xadd(xmul(t, t), a.eps)));
+            }
+            __syncwarp();
+            if (und) {
+              double s1 = 0.0, s2 = 0.0;
+#pragma unroll
+              for (int kk = 0; kk < 8; ++kk) {
+                s1 = xadd(s1, s_T[tb + rank][kk]);
+                s2 = xadd(s2, s_T[tb + rank][8 + kk]);
+              }
+              le = xmul(a.beta, s1) <= xmul(a.beta, s2);
+            }
+            __syncwarp();  // s_xq / s_m / s_T reuse next step
+          }
+        }
+        if (le) hi = m2;
+        else lo = m1;
+      }
+      if (has) {
+        const double nv = xmul(0.5, xadd(lo, hi));
+        const int i = pix / a.cols, j = pix - i * a.cols;
+        back[(long long)i * a.pitch + j] = nv;
+        ccur[pix] = nv != old;
+        s_delta[pos] = fabs(xsub(nv, old));
+      }
+      __syncwarp();  // the lanes' shared rows are reused by the next round
     }
     __syncthreads();
     double t = 0.0;
