@@ -52,7 +52,6 @@ NVCC_FLAGS = [
     "-fmad=false",
     "-Xcompiler", "-fPIC,-O2",
     "-Xptxas", "-v",
-    "-ldl",
 ]
 
 
@@ -100,23 +99,50 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
+def _compile(src: str, obj: str) -> subprocess.CompletedProcess:
+    cmd = [nvcc(), *NVCC_FLAGS, "-I", GEN, "-c", "-o", obj, os.path.join(CSRC, src)]
+    return subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
+
+
 def build(verbose: bool = False, force: bool = False) -> str:
+    """Compile every source to an object in parallel (no cross-file device
+    symbols, so no relocatable device code), then link the shared library."""
+    from concurrent.futures import ThreadPoolExecutor
+
     out = lib_path()
     if not force and not needs_build():
         return out
     os.makedirs(LIBDIR, exist_ok=True)
     write_jit_headers()
+    objdir = os.path.join(LIBDIR, "obj")
+    os.makedirs(objdir, exist_ok=True)
+    objs = [os.path.join(objdir, s.replace(".cu", ".o")) for s in SOURCES]
+    # an object is reused only when it is newer than its source and every
+    # header (force rebuilds everything)
+    hdrs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if not f.endswith(".cu")]
+    hdrs += [os.path.join(ROOT, "include", "stencilkit_b200.h"), os.path.abspath(__file__)]
+    newest_hdr = max(os.path.getmtime(h) for h in hdrs if os.path.exists(h))
+    todo = [(s, o) for s, o in zip(SOURCES, objs)
+            if force or not os.path.exists(o)
+            or os.path.getmtime(o) < max(newest_hdr, os.path.getmtime(os.path.join(CSRC, s)))]
+    with ThreadPoolExecutor(max_workers=max(1, min(len(todo), os.cpu_count() or 1))) as pool:
+        results = list(pool.map(lambda so: _compile(*so), todo))
+    log = "".join(r.stdout + r.stderr for r in results)
+    bad = [so[0] for so, r in zip(todo, results) if r.returncode != 0]
+    if bad:
+        sys.stderr.write(log)
+        raise RuntimeError(f"nvcc failed building {LIBNAME} ({', '.join(bad)})")
     tmp = out + ".tmp"
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", GEN, "-shared", "-o", tmp,
-           *[os.path.join(CSRC, s) for s in SOURCES]]
-    res = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
+    res = subprocess.run([nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
+                          "-o", tmp, *objs, "-ldl"],
+                         cwd=CSRC, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed building " + LIBNAME)
+        raise RuntimeError("nvcc failed linking " + LIBNAME)
     if verbose:
-        sys.stderr.write(res.stderr)
+        sys.stderr.write(log)
     with open(os.path.join(LIBDIR, "ptxas.log"), "w") as fh:
-        fh.write(res.stderr)
+        fh.write(log)
     os.replace(tmp, out)
     return out
 

@@ -297,7 +297,18 @@ __device__ __noinline__ int fold_and_decide(const LoopCtl& L, long long it, doub
     const int c0 = L.part_chunk_dev ? L.part_chunk_dev[p] : L.part_chunk[p];
     const int c1 = L.part_chunk_dev ? L.part_chunk_dev[p + 1] : L.part_chunk[p + 1];
     double t = neutral;
-    for (int c = c0 + (int)threadIdx.x; c < c1; c += BLOCK) t = comb(t, __ldcg(&L.partials[c]));
+    // 8 partials in flight per thread, combined in the same (strided) order
+    // as one at a time: a MAX combine's NaN branches otherwise serialise one
+    // L2 round trip per partial (~45 us per fold at 16k chunks)
+    int c = c0 + (int)threadIdx.x;
+    for (; c + 7 * BLOCK < c1; c += 8 * BLOCK) {
+      double v8[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v8[k] = __ldcg(&L.partials[c + k * BLOCK]);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) t = comb(t, v8[k]);
+    }
+    for (; c < c1; c += BLOCK) t = comb(t, __ldcg(&L.partials[c]));
     const double v = block_reduce_c<BLOCK>(comb, neutral, t, sh);
     if (threadIdx.x == 0) acc = comb.fold(acc, v);
   }
