@@ -540,7 +540,7 @@ __device__ __forceinline__ int res_step(const LoopCtl& L, long long it, double m
 // VEC contiguous elements per thread for the resident loop (VEC = 4: one
 // 16-byte vector for float, two for double; 1 or 2: scalar accesses)
 template <typename T, int V>
-struct VecN {
+struct alignas(sizeof(T) * V <= 16 ? sizeof(T) * V : 16) VecN {
   T v[V];
 };
 template <typename T, int V>
@@ -841,7 +841,8 @@ __global__ void __launch_bounds__(BLOCK, 1) helm_resident_split(const __grid_con
   // read parity t while the fastest may already write parity t+1
   __shared__ T s_edge[2][RMAX][2][NW];
   extern __shared__ __align__(16) unsigned char s_dyn[];
-  T* s_f = reinterpret_cast<T*>(s_dyn);
+  T* s_f = reinterpret_cast<T*>(s_dyn);  // f of this band, RMAX rows x kFP
+  constexpr int kFP = BLOCK * VEC;
   const Sweep2D& g = a.g;
   long long it = loop_enter(a.L);
   if (it == 0) return;
@@ -866,11 +867,12 @@ __global__ void __launch_bounds__(BLOCK, 1) helm_resident_split(const __grid_con
   for (int r = 0; r < RMAX; ++r) {
     u[r] = (active && r < R) ? ldgN<T, VEC>(src + (long long)(r0 + r) * g.src_pitch + col) : zeroN<T, VEC>();
     w[r] = u[r];
-    if (active && r < R) {
-      const VecN<T, VEC> fv = ldgN<T, VEC>(env + (long long)(r0 + r) * g.env_pitch + col);
+    if (r < R) {  // s_f rows are BLOCK*VEC long: every thread owns a whole vector
+      VecN<T, VEC> fv = active ? ldgN<T, VEC>(env + (long long)(r0 + r) * g.env_pitch + col) : zeroN<T, VEC>();
 #pragma unroll
       for (int e = 0; e < VEC; ++e)
-        if (e < nvalid) s_f[r * cols + col + e] = fv.v[e];
+        if (e >= nvalid) fv.v[e] = T(0);
+      *reinterpret_cast<VecN<T, VEC>*>(s_f + r * kFP + col) = fv;
     }
   }
   VecN<T, VEC> up = (active && !(r0 == 0 && top_zero)) ? ldgN<T, VEC>(src + (long long)(r0 - 1) * g.src_pitch + col)
@@ -879,20 +881,41 @@ __global__ void __launch_bounds__(BLOCK, 1) helm_resident_split(const __grid_con
                                                       : zeroN<T, VEC>();
   T accm = -INFINITY;
   int sp = (int)((it - 1) & 1);  // s_edge slot of the state being updated: u(t) -> t & 1
+  // one row's update, the VEC elements as one vector: a single exact-division
+  // check per row (helmholtz_sweep's form; bit-identical), f as one shared
+  // vector load, the run constants in registers
+  const T ax = a.ax, ay = a.ay, bb = a.b, keep = a.keep, relax = a.relax;
+  const bool has_lw = warp > 0, has_rw = warp + 1 < NW;
   auto update = [&](int r, const VecN<T, VEC>& cen, const VecN<T, VEC>& above,
                     const VecN<T, VEC>& below) {
     T lv = __shfl_up_sync(FULL, cen.v[VEC - 1], 1);
     T rv = __shfl_down_sync(FULL, cen.v[0], 1);
-    if (lane == 0) lv = warp > 0 ? s_edge[sp][r][1][warp - 1] : T(0);
-    if (lane == 31) rv = warp + 1 < NW ? s_edge[sp][r][0][warp + 1] : T(0);
-    VecN<T, VEC> o;
+    if (lane == 0) lv = has_lw ? s_edge[sp][r][1][warp - 1] : T(0);
+    if (lane == 31) rv = has_rw ? s_edge[sp][r][0][warp + 1] : T(0);
+    const VecN<T, VEC> fv = *reinterpret_cast<const VecN<T, VEC>*>(s_f + r * kFP + col);
+    T num[VEC];
+    bool ok = fast;
 #pragma unroll
     for (int e = 0; e < VEC; ++e) {
       const T l = e == 0 ? lv : cen.v[e - 1];
       T rt = e == VEC - 1 ? rv : cen.v[e + 1];
       if (e + 1 >= nvalid) rt = T(0);
-      const T fv = active && e < nvalid ? s_f[r * cols + col + e] : T(0);
-      const T out = helm_update(cen.v[e], l, rt, above.v[e], below.v[e], fv, a, rb, fast);
+      const T t3 = xadd(fv.v[e], xmul(ax, xadd(l, rt)));
+      num[e] = xmul(relax, xadd(t3, xmul(ay, xadd(above.v[e], below.v[e]))));
+      ok = ok && div_safe(num[e]);
+    }
+    T q[VEC];
+    if (ok) {
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) q[e] = div_const(num[e], bb, rb);
+    } else {
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) q[e] = xdiv(num[e], bb);
+    }
+    VecN<T, VEC> o;
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+      const T out = xadd(xmul(keep, cen.v[e]), q[e]);
       const bool in = e < nvalid;
       o.v[e] = in ? out : T(0);
       T d;
@@ -1151,7 +1174,8 @@ int launch_resident(sk_run* r, const LoopCtl& L, cudaStream_t s, const HelmArgs<
     nb += (pr + band - 1) / band;
     L2.part_chunk[i + 1] = nb;
   }
-  const size_t dyn = (size_t)band * p.cols * sizeof(T);
+  // f rows padded to the CTA's width (the split kernel reads whole vectors)
+  const size_t dyn = (size_t)band * block * vec * sizeof(T);
   if (dyn > 200 * 1024) return SK_ERR_UNSUPPORTED;
   SK_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
