@@ -1010,6 +1010,294 @@ __global__ void __launch_bounds__(BLOCK, 1) helm_resident_split(const __grid_con
   }
 }
 
+// ---- barrier-free resident loop (fp32, one partition, MAX of |delta| or delta^2)
+// helm_resident_split without the grid barrier.  Every value a band sends
+// carries its iteration in the same 8-byte word ("LL" words: tag << 32 |
+// fp32 bits), stored with one relaxed 8-byte store and polled with relaxed
+// loads until the tag matches -- no fence, no counter, one L2 round trip:
+//  * halo rows: the band's first / last row of iteration t go to an
+//    exchange slot (t & 1); the neighbours poll them to compute t+1;
+//  * reduce partials: the band's MAX of iteration t goes to parts[t % 4][band].
+// The loop decision for iteration t is taken while computing t+1 (one
+// iteration of lag): warp 0 issues the loads of all partials of t at the
+// start of t+1, checks their tags after the update and folds them, and the
+// CTA barrier that ends t+1 hands the decision to every warp.  If the loop
+// stops at t, the speculative u(t+1) is dropped and u(t) written.  Safety
+// of the reused slots: a band publishes into halo slot t & 1 only after it
+// read its neighbours' rows of t-1, which they sent after consuming its rows
+// of t-2; partial slot t % 4 is rewritten at t+4, after every band has
+// published t+2, i.e. after every band folded t (read at t+1).  Tags are
+// run-unique (tag_base advances by max_it + 4 per launch), so no buffer
+// needs clearing between launches.  Every value is helm_resident_split's op
+// for op and the MAX is order-free (non-negative floats order as their bits,
+// NaN above +inf): bit-identical, same iteration count.
+__device__ __forceinline__ unsigned long long ll_pack(unsigned tag, float v) {
+  return ((unsigned long long)tag << 32) | __float_as_uint(v);
+}
+__device__ __forceinline__ void ll_st2(unsigned long long* p, unsigned long long a, unsigned long long b) {
+  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+__device__ __forceinline__ void ll_st1(unsigned long long* p, unsigned long long a) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(a) : "memory");
+}
+__device__ __forceinline__ unsigned long long ll_ld1(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <int VEC>
+__device__ __forceinline__ void ll_store_row(unsigned long long* p, unsigned tag, const VecN<float, VEC>& x) {
+  if constexpr (VEC == 1) {
+    ll_st1(p, ll_pack(tag, x.v[0]));
+  } else {
+#pragma unroll
+    for (int e = 0; e < VEC; e += 2) ll_st2(p + e, ll_pack(tag, x.v[e]), ll_pack(tag, x.v[e + 1]));
+  }
+}
+
+// poll until every element of this thread's slice carries `tag`
+template <int VEC>
+__device__ __forceinline__ VecN<float, VEC> ll_load_row(const unsigned long long* p, unsigned tag) {
+  VecN<float, VEC> r;
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) {
+    unsigned long long v = ll_ld1(p + e);
+    while ((unsigned)(v >> 32) != tag) v = ll_ld1(p + e);
+    r.v[e] = __uint_as_float((unsigned)v);
+  }
+  return r;
+}
+
+template <int BLOCK, int VEC, int RMAX, int DELTA>
+__global__ void __launch_bounds__(BLOCK, 1) helm_resident_ll(const __grid_constant__ HelmArgs<float> a,
+                                                             unsigned long long* xbuf, unsigned long long* parts,
+                                                             unsigned tag_base) {
+  using T = float;
+  constexpr unsigned FULL = 0xffffffffu;
+  constexpr int NW = BLOCK / 32;
+  constexpr int kPS = 4;  // partial slots
+  __shared__ T s_edge[2][RMAX][2][NW];
+  __shared__ unsigned s_max[3];
+  __shared__ int s_dec[2];
+  __shared__ float s_val[2];
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  T* s_f = reinterpret_cast<T*>(s_dyn);  // f of this band, RMAX rows x kFP
+  constexpr int kFP = BLOCK * VEC;
+  const Sweep2D& g = a.g;
+  long long it = loop_enter(a.L);
+  if (it == 0) return;
+  const int cols = g.cols, rows = g.rows;
+  int cb, r0, r1;
+  chunk_geom(a.L, g, blockIdx.x, &cb, &r0, &r1);
+  const int R = r1 - r0;
+  const int nb = gridDim.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int col = threadIdx.x * VEC;
+  const int nvalid = cols - col;
+  const bool active = nvalid > 0;
+  const T rb = rcp_rn(a.b);
+  const bool fast = a.fast_div != 0;
+  const bool top_zero = !g.halo_top, bot_zero = !g.halo_bottom;
+  const bool has_up = !(r0 == 0 && top_zero), has_dn = !(r1 == rows && bot_zero);
+  const long long xp = a.xpitch;
+  if (threadIdx.x < 3) s_max[threadIdx.x] = 0u;
+
+  // RMAX is the band height: every band but the last has exactly RMAX rows,
+  // the last band's rows >= R are held at zero (the Dirichlet rows below
+  // the grid), so every row index below is static -- no local-memory arrays
+  VecN<T, VEC> u[RMAX], w[RMAX];
+  const T* src = static_cast<const T*>(g.src) + (long long)g.halo_top * g.src_pitch;
+  const T* env = static_cast<const T*>(g.env) + (long long)g.halo_top * g.env_pitch;
+#pragma unroll
+  for (int r = 0; r < RMAX; ++r) {
+    u[r] = (active && r < R) ? ldgN<T, VEC>(src + (long long)(r0 + r) * g.src_pitch + col) : zeroN<T, VEC>();
+    w[r] = u[r];
+    {
+      VecN<T, VEC> fv = (active && r < R) ? ldgN<T, VEC>(env + (long long)(r0 + r) * g.env_pitch + col) : zeroN<T, VEC>();
+#pragma unroll
+      for (int e = 0; e < VEC; ++e)
+        if (e >= nvalid) fv.v[e] = T(0);
+      *reinterpret_cast<VecN<T, VEC>*>(s_f + r * kFP + col) = fv;
+    }
+  }
+  VecN<T, VEC> up = (active && has_up) ? ldgN<T, VEC>(src + (long long)(r0 - 1) * g.src_pitch + col) : zeroN<T, VEC>();
+  VecN<T, VEC> dn = (active && has_dn) ? ldgN<T, VEC>(src + (long long)r1 * g.src_pitch + col) : zeroN<T, VEC>();
+  T accm = -INFINITY;
+  int sp = (int)((it - 1) & 1);
+  const T ax = a.ax, ay = a.ay, bb = a.b, keep = a.keep, relax = a.relax;
+  const bool has_lw = warp > 0, has_rw = warp + 1 < NW;
+  auto update = [&](int r, const VecN<T, VEC>& cen, const VecN<T, VEC>& above,
+                    const VecN<T, VEC>& below) {
+    const bool vr = r < R;  // a real row (else a zero row of the last band)
+    T lv = __shfl_up_sync(FULL, cen.v[VEC - 1], 1);
+    T rv = __shfl_down_sync(FULL, cen.v[0], 1);
+    if (lane == 0) lv = has_lw ? s_edge[sp][r][1][warp - 1] : T(0);
+    if (lane == 31) rv = has_rw ? s_edge[sp][r][0][warp + 1] : T(0);
+    const VecN<T, VEC> fv = *reinterpret_cast<const VecN<T, VEC>*>(s_f + r * kFP + col);
+    T num[VEC];
+    bool ok = fast;
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+      const T l = e == 0 ? lv : cen.v[e - 1];
+      T rt = e == VEC - 1 ? rv : cen.v[e + 1];
+      if (e + 1 >= nvalid) rt = T(0);
+      const T t3 = xadd(fv.v[e], xmul(ax, xadd(l, rt)));
+      num[e] = xmul(relax, xadd(t3, xmul(ay, xadd(above.v[e], below.v[e]))));
+      ok = ok && div_safe(num[e]);
+    }
+    T q[VEC];
+    if (ok) {
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) q[e] = div_const(num[e], bb, rb);
+    } else {
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) q[e] = xdiv(num[e], bb);
+    }
+    VecN<T, VEC> o;
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+      const T out = xadd(xmul(keep, cen.v[e]), q[e]);
+      const bool in = e < nvalid && vr;
+      o.v[e] = in ? out : T(0);
+      T d;
+      if (DELTA == SK_DELTA_ABS) {
+        d = tabs(xsub(out, cen.v[e]));
+      } else {
+        const T t = xsub(out, cen.v[e]);
+        d = xmul(t, t);
+      }
+      if (in) accm = max_nan(accm, d);
+    }
+    return o;
+  };
+  auto sedge = [&](int slot, const VecN<T, VEC>* x) {
+#pragma unroll
+    for (int r = 0; r < RMAX; ++r) {
+      if (lane == 0) s_edge[slot][r][0][warp] = x[r].v[0];
+      if (lane == 31) s_edge[slot][r][1][warp] = x[r].v[VEC - 1];
+    }
+  };
+  auto interior = [&]() {
+#pragma unroll
+    for (int r = 1; r < RMAX - 1; ++r) w[r] = update(r, u[r], u[r - 1], u[r + 1]);
+  };
+  auto edges = [&]() {
+    if constexpr (RMAX == 1) {
+      w[0] = update(0, u[0], up, dn);
+    } else {
+      w[0] = update(0, u[0], up, u[1]);
+      w[RMAX - 1] = update(RMAX - 1, u[RMAX - 1], u[RMAX - 2], dn);
+    }
+  };
+  // publish w = u(t): halo rows to the exchange slot, warp-edge columns to
+  // s_edge, and the warp maxima into s_max[t % 3]
+  auto publish = [&](long long t) {
+    const unsigned tag = tag_base + (unsigned)t;
+    if (active) {
+      unsigned long long* x = xbuf + ((long long)((t & 1) * nb + blockIdx.x) * 2) * xp + col;
+      ll_store_row<VEC>(x, tag, w[0]);
+      // (the last band's row RMAX-1 may be a zero row: nobody reads it)
+      ll_store_row<VEC>(x + xp, tag, w[RMAX - 1]);
+    }
+    sedge((int)(t & 1), w);
+    T m = accm;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = max_nan(m, __shfl_xor_sync(FULL, m, o));
+    // no valid element: -inf -> 0, the identity of a non-negative max
+    if (lane == 0 && !(m < T(0))) atomicMax(&s_max[t % 3], __float_as_uint(m));
+    accm = -INFINITY;
+  };
+  // the CTA's partial of t (after the barrier that completed s_max[t % 3])
+  auto send_partial = [&](long long t) {
+    if (threadIdx.x == 0) {
+      ll_st1(parts + (long long)(t % kPS) * nb + blockIdx.x, ll_pack(tag_base + (unsigned)t, __uint_as_float(s_max[t % 3])));
+      s_max[(t + 2) % 3] = 0u;  // slot of t+2 (t-1's partial went out last iteration)
+    }
+  };
+  // iteration `it` in full (its halo rows come straight from the input)
+  sedge(sp, u);
+  __syncthreads();
+  interior();
+  edges();
+  publish(it);
+  __syncthreads();
+  send_partial(it);
+  for (;;) {
+    // u <- u(it); compute u(it + 1) while deciding iteration `it`
+#pragma unroll
+    for (int r = 0; r < RMAX; ++r) u[r] = w[r];
+    sp = (int)(it & 1);
+    const unsigned tag = tag_base + (unsigned)it;
+    // warp 0: the partials of `it` (published one CTA barrier ago by this
+    // band, a little earlier or later by the others)
+    constexpr int kPL = 8;  // up to 256 bands
+    unsigned long long pv[kPL];
+    if (warp == 0) {
+      const unsigned long long* ps = parts + (long long)(it % kPS) * nb;
+#pragma unroll
+      for (int k = 0; k < kPL; ++k) {
+        const int c = lane + 32 * k;
+        pv[k] = c < nb ? ll_ld1(ps + c) : 0ull;
+      }
+    }
+    interior();
+    if (active) {
+      const unsigned long long* xb = xbuf + (long long)((it & 1) * nb) * 2 * xp + col;
+      up = has_up ? ll_load_row<VEC>(xb + ((long long)(blockIdx.x - 1) * 2 + 1) * xp, tag) : zeroN<T, VEC>();
+      dn = has_dn ? ll_load_row<VEC>(xb + ((long long)(blockIdx.x + 1) * 2) * xp, tag) : zeroN<T, VEC>();
+    }
+    edges();
+    publish(it + 1);
+    if (warp == 0) {
+      const unsigned long long* ps = parts + (long long)(it % kPS) * nb;
+      unsigned m = 0u;
+#pragma unroll
+      for (int k = 0; k < kPL; ++k) {
+        const int c = lane + 32 * k;
+        if (c < nb) {
+          while ((unsigned)(pv[k] >> 32) != tag) pv[k] = ll_ld1(ps + c);
+          const unsigned b = (unsigned)pv[k];
+          m = b > m ? b : m;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const unsigned x = __shfl_xor_sync(FULL, m, o);
+        m = x > m ? x : m;
+      }
+      if (lane == 0) {
+        const OpCombine comb{SK_REDUCE_MAX};
+        const double acc = comb.fold(a.L.identity, (double)__uint_as_float(m));
+        const int c = eval_cond(a.L.cond, acc, it, a.L.flagged_dev);
+        const int capped = it >= a.L.cond.max_it;
+        s_dec[it & 1] = c || capped;
+        if ((c || capped) && blockIdx.x == 0) {
+          Status* st = a.L.st;
+          st->value = acc;
+          st->cond_true = c;
+          st->exhausted = !c && capped;
+          st->iter = it;
+          st->stop = 1;
+          __threadfence();
+        }
+      }
+    }
+    __syncthreads();
+    if (s_dec[it & 1]) {  // iteration `it` is the result (u(it+1) is dropped)
+      if (active) {
+        T* out = static_cast<T*>(g.buf[it & 1]) + (long long)g.halo_top * g.pitch;
+#pragma unroll
+        for (int r = 0; r < RMAX; ++r)
+          if (r < R) stN<T, VEC>(out + (long long)(r0 + r) * g.pitch + col, u[r]);
+      }
+      return;
+    }
+    send_partial(it + 1);
+    ++it;
+  }
+}
+
 #include "sk_helm_tma.cuh"
 
 // ---------------------------------------------------------------- host side
@@ -1133,6 +1421,103 @@ ResFn<T> pick_res_b(int delta, int reduce) {
   return nullptr;
 }
 
+using ResLLFn = void (*)(const HelmArgs<float>, unsigned long long*, unsigned long long*, unsigned);
+
+template <int RMAX>
+ResLLFn pick_res_ll(int delta) {
+  if (delta == SK_DELTA_ABS) return helm_resident_ll<512, 2, RMAX, SK_DELTA_ABS>;
+  if (delta == SK_DELTA_SQUARE) return helm_resident_ll<512, 2, RMAX, SK_DELTA_SQUARE>;
+  return nullptr;
+}
+
+ResLLFn pick_res_ll_band(int band, int delta) {
+  switch (band) {
+    case 1: return pick_res_ll<1>(delta);
+    case 2: return pick_res_ll<2>(delta);
+    case 3: return pick_res_ll<3>(delta);
+    case 4: return pick_res_ll<4>(delta);
+    case 5: return pick_res_ll<5>(delta);
+    case 6: return pick_res_ll<6>(delta);
+    case 7: return pick_res_ll<7>(delta);
+    case 8: return pick_res_ll<8>(delta);
+    default: return nullptr;
+  }
+}
+
+// helm_resident_ll: same bands as launch_resident; scratch = 4 partial
+// slots x bands | halo exchange (2 parities x bands x 2 rows x cols) of
+// 8-byte tagged words.  The scratch belongs to the stream, not the run: runs
+// on one stream execute in order, so every run on it reuses one buffer that
+// is never cleared -- tags are unique over its lifetime (tag_base + it, the
+// base advancing by max_it + 8 per launch) -- and a C1 solve costs no
+// allocation, memset or occupancy query.
+struct LLScratch {
+  void* p = nullptr;
+  size_t bytes = 0;
+  long long epoch = 0;
+};
+
+int launch_resident_ll(sk_run* r, const LoopCtl& L, cudaStream_t s, const HelmArgs<float>& base, int block) {
+  const sk_plan& p = r->plan;
+  if (block != 512) return SK_ERR_UNSUPPORTED;  // (1024 threads would spill)
+  const int sms = device_sms(r->device);
+  int band = (int)((p.rows + sms - 1) / sms);
+  if (band < 1) band = 1;
+  ResLLFn fn = pick_res_ll_band(band, p.delta_op);
+  if (!fn) return SK_ERR_UNSUPPORTED;
+  const int nb = (p.rows + band - 1) / band;
+  if (nb > 256) return SK_ERR_UNSUPPORTED;  // warp 0 folds <= 8 partials per lane
+  const size_t dyn = (size_t)band * block * 2 * sizeof(float);
+  static std::mutex mu;
+  static std::map<std::pair<const void*, size_t>, int> occ_cache;
+  static std::map<std::pair<int, cudaStream_t>, LLScratch> scratch;
+  std::lock_guard<std::mutex> lk(mu);
+  const auto okey = std::make_pair(reinterpret_cast<const void*>(fn), dyn);
+  auto oit = occ_cache.find(okey);
+  if (oit == occ_cache.end()) {
+    SK_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)dyn));
+    int occ = 0;
+    SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, reinterpret_cast<const void*>(fn), block, dyn));
+    oit = occ_cache.emplace(okey, occ).first;
+  }
+  if (oit->second < 1 || nb > oit->second * sms) return SK_ERR_UNSUPPORTED;
+  const long long cpad = (p.cols + 3) / 4 * 4;
+  const size_t pbytes = (size_t)4 * nb * 8;
+  const size_t bytes = pbytes + (size_t)2 * nb * 2 * cpad * 8;
+  const long long span = L.cond.max_it + 8;
+  LLScratch& sc = scratch[std::make_pair(r->device, s)];
+  bool clear = false;
+  if (!sc.p || sc.bytes < bytes) {
+    if (sc.p) SK_CUDA(cudaFreeAsync(sc.p, s));
+    sc.p = nullptr;
+    SK_CUDA(cudaMallocAsync(&sc.p, bytes, s));
+    sc.bytes = bytes;
+    clear = true;
+  }
+  if (sc.epoch < 1 || sc.epoch + span >= (1ll << 32)) clear = true;
+  if (clear) {
+    SK_CUDA(cudaMemsetAsync(sc.p, 0, sc.bytes, s));
+    sc.epoch = 1;
+  }
+  const unsigned tag_base = (unsigned)sc.epoch;
+  sc.epoch += span;
+  HelmArgs<float> a = base;
+  a.g.colblocks = 1;
+  a.g.chunk_rows = band;
+  a.xpitch = cpad;
+  a.L = L;
+  a.L.part_chunk[0] = 0;
+  a.L.part_chunk[1] = nb;
+  a.L.ring = nullptr;
+  unsigned long long* parts = static_cast<unsigned long long*>(sc.p);
+  unsigned long long* xbuf = reinterpret_cast<unsigned long long*>(static_cast<char*>(sc.p) + pbytes);
+  unsigned tb = tag_base;
+  void* params[] = {&a, &xbuf, &parts, &tb};
+  SK_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(fn), nb, block, params, dyn, s));
+  return SK_OK;
+}
+
 // Register-resident whole-loop launch (see helm_resident) when the grid fits
 // on chip: one band of <= kResRows rows per co-resident CTA, f in shared
 // memory.  Returns SK_ERR_UNSUPPORTED (nothing launched) otherwise.
@@ -1155,6 +1540,16 @@ int launch_resident(sk_run* r, const LoopCtl& L, cudaStream_t s, const HelmArgs<
   if (p.cols <= 1024 && (want == 1 || want == 4)) {
     vec = want;
     block = 1024 / want;
+  }
+  // barrier-free form (helm_resident_ll): fp32, one partition, MAX of
+  // |delta| or delta^2, 2 columns per thread; SK_RES_LL=0 turns it off
+  const char* ll_env = getenv("SK_RES_LL");
+  if constexpr (sizeof(T) == 4) {
+    if (!(ll_env && ll_env[0] == '0') && vec == 2 && r->nparts == 1 && p.reduce_op == SK_REDUCE_MAX &&
+        (p.delta_op == SK_DELTA_ABS || p.delta_op == SK_DELTA_SQUARE) && L.cond.max_it < (1ll << 30)) {
+      const int rc = launch_resident_ll(r, L, s, base, block);
+      if (rc != SK_ERR_UNSUPPORTED) return rc;
+    }
   }
   ResFn<T> fn = block == 256   ? pick_res_b<T, 256, 4>(p.delta_op, p.reduce_op)
                 : block == 512 ? pick_res_b<T, 512, 2>(p.delta_op, p.reduce_op)
@@ -1491,7 +1886,7 @@ void teardown(sk_run* r) {
     free(r->aux[5]);
     r->aux[5] = nullptr;
   }
-  for (int i : {6, 7})
+  for (int i : {6, 7})  // 6: fix-up status, 7: resident scratch
     if (r->aux[i]) {
       cudaFreeAsync(r->aux[i], r->stream);
       r->aux[i] = nullptr;
