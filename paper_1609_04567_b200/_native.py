@@ -154,12 +154,20 @@ def check(rc: int):
         raise NativeError(rc, msg)
 
 
-def require_cuda():
-    """Raise DeviceUnavailable unless a CUDA device and the library are present."""
-    import torch
+_cuda_ok = False
 
-    if not torch.cuda.is_available():
-        raise DeviceUnavailable("no CUDA device: stencilkit_b200 runs only on the GPU")
+
+def require_cuda():
+    """Raise DeviceUnavailable unless a CUDA device and the library are present
+    (the device check runs until it first succeeds: it is per-call overhead
+    on every loop)."""
+    global _cuda_ok
+    if not _cuda_ok:
+        import torch
+
+        if not torch.cuda.is_available():
+            raise DeviceUnavailable("no CUDA device: stencilkit_b200 runs only on the GPU")
+        _cuda_ok = True
     return load()
 
 

@@ -529,13 +529,19 @@ class DeviceExecutor(Executor):
             delta = delta_kind(plan.delta)
         group = self._group
         owns = group is None
-        stream = group.stream if group is not None else torch.cuda.current_stream()
+        cur = torch.cuda.current_stream()
+        stream = group.stream if group is not None else cur
         if group is not None:
             # the run's stream starts after whatever the caller enqueued on
             # its current stream (e.g. a non-blocking upload of the inputs)
-            stream.wait_stream(torch.cuda.current_stream())
+            stream.wait_stream(cur)
             group.start_run()
         try:
+            if stream == cur:  # (the stream context costs several us per loop)
+                if prog is not None:
+                    return self._begin_jit(lib, plan, grid, prog, rows, cols, P, stream, group, owns)
+                return self._begin_on(lib, plan, grid, dk, rows, cols, P, reduce, delta,
+                                      stream, group, owns)
             with torch.cuda.stream(stream):
                 if prog is not None:
                     return self._begin_jit(lib, plan, grid, prog, rows, cols, P, stream, group, owns)

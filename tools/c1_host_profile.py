@@ -39,4 +39,4 @@ pr.enable()
 for _ in range(100):
     solve()
 pr.disable()
-pstats.Stats(pr).sort_stats("cumtime").print_stats(40)
+pstats.Stats(pr).sort_stats("tottime").print_stats(45)
