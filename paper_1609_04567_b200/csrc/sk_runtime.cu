@@ -186,6 +186,26 @@ static LoopCtl make_ctl(sk_run* r, const sk_cond* c, bool graph, cudaGraphCondit
   return L;
 }
 
+// Status read-back through a pinned, per-thread staging block: a copy into
+// pageable stack memory is a staged, synchronous driver copy on top of the
+// stream synchronise (~10 us per loop on the C1 path).
+static int read_status(sk_run* r, Status* out) {
+  thread_local Status* pinned = nullptr;
+  if (!pinned && cudaMallocHost(reinterpret_cast<void**>(&pinned), sizeof(Status)) != cudaSuccess) {
+    pinned = nullptr;
+    cudaGetLastError();
+  }
+  if (pinned) {
+    SK_CUDA(cudaMemcpyAsync(pinned, r->d_status, sizeof(Status), cudaMemcpyDeviceToHost, r->stream));
+    SK_CUDA(cudaStreamSynchronize(r->stream));
+    *out = *pinned;
+  } else {
+    SK_CUDA(cudaMemcpyAsync(out, r->d_status, sizeof(Status), cudaMemcpyDeviceToHost, r->stream));
+    SK_CUDA(cudaStreamSynchronize(r->stream));
+  }
+  return SK_OK;
+}
+
 static int launch_timed(sk_run* r, const LoopCtl& L0) {
   LoopCtl L = L0;
   L.peer.seq = (unsigned)(r->launched + 1);  // this launch's sequence number
@@ -490,14 +510,12 @@ int sk_run_loop(sk_run* r, const sk_cond* c, int64_t* iterations, double* final_
       for (int i = 0; i < batch; ++i)
         if ((rc = launch_timed(r, L))) return rc;
       Status st;
-      SK_CUDA(cudaMemcpyAsync(&st, r->d_status, sizeof(Status), cudaMemcpyDeviceToHost, r->stream));
-      SK_CUDA(cudaStreamSynchronize(r->stream));
+      if (int rs = read_status(r, &st)) return rs;
       if (st.stop) break;
     }
   }
   Status st;
-  SK_CUDA(cudaMemcpyAsync(&st, r->d_status, sizeof(Status), cudaMemcpyDeviceToHost, r->stream));
-  SK_CUDA(cudaStreamSynchronize(r->stream));
+  if (int rs = read_status(r, &st)) return rs;
   if (!st.stop) {
     set_error("sk_run_loop: device loop ended without a decision");
     return SK_ERR_STATE;
@@ -590,8 +608,7 @@ int sk_run_kernel_time(sk_run* r, double* total_ms, int64_t* launches) {
   // Only sweeps that computed an iteration count (over-launched no-ops after
   // the device-decided stop are excluded).
   Status st;
-  SK_CUDA(cudaMemcpyAsync(&st, r->d_status, sizeof(Status), cudaMemcpyDeviceToHost, r->stream));
-  SK_CUDA(cudaStreamSynchronize(r->stream));
+  if (int rs = read_status(r, &st)) return rs;
   double tot = 0;
   long long n = 0;
   for (size_t i = 0; i < r->t_start.size(); ++i) {
@@ -737,8 +754,7 @@ int sk_run_status(sk_run* r, int64_t* iterations, double* value, int32_t* stoppe
     return SK_ERR_ARG;
   }
   Status st;
-  SK_CUDA(cudaMemcpyAsync(&st, r->d_status, sizeof(Status), cudaMemcpyDeviceToHost, r->stream));
-  SK_CUDA(cudaStreamSynchronize(r->stream));
+  if (int rs = read_status(r, &st)) return rs;
   if (iterations) *iterations = st.iter;
   if (value) *value = r->combined ? st.gvalue : st.value;
   if (stopped) *stopped = st.stop;
