@@ -1241,11 +1241,27 @@ __global__ void __launch_bounds__(BLOCK, 1) helm_resident_ll(const __grid_consta
         pv[k] = c < nb ? ll_ld1(ps + c) : 0ull;
       }
     }
+    // the neighbours' rows of `it`: first loads issued before the interior
+    // update (usually already tagged `it` when they land), polled after it
+    const unsigned long long* xb = xbuf + (long long)((it & 1) * nb) * 2 * xp + col;
+    const unsigned long long* pu = xb + ((long long)(blockIdx.x - 1) * 2 + 1) * xp;
+    const unsigned long long* pd = xb + ((long long)(blockIdx.x + 1) * 2) * xp;
+    const bool lu = active && has_up, ld = active && has_dn;
+    unsigned long long wu[VEC], wd[VEC];
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+      wu[e] = lu ? ll_ld1(pu + e) : 0ull;
+      wd[e] = ld ? ll_ld1(pd + e) : 0ull;
+    }
     interior();
-    if (active) {
-      const unsigned long long* xb = xbuf + (long long)((it & 1) * nb) * 2 * xp + col;
-      up = has_up ? ll_load_row<VEC>(xb + ((long long)(blockIdx.x - 1) * 2 + 1) * xp, tag) : zeroN<T, VEC>();
-      dn = has_dn ? ll_load_row<VEC>(xb + ((long long)(blockIdx.x + 1) * 2) * xp, tag) : zeroN<T, VEC>();
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+      if (lu)
+        while ((unsigned)(wu[e] >> 32) != tag) wu[e] = ll_ld1(pu + e);
+      if (ld)
+        while ((unsigned)(wd[e] >> 32) != tag) wd[e] = ll_ld1(pd + e);
+      up.v[e] = lu ? __uint_as_float((unsigned)wu[e]) : T(0);
+      dn.v[e] = ld ? __uint_as_float((unsigned)wd[e]) : T(0);
     }
     edges();
     publish(it + 1);
