@@ -1021,13 +1021,16 @@ __global__ void __launch_bounds__(BLOCK, 1) helm_resident_split(const __grid_con
 // The loop decision for iteration t is taken while computing t+1 (one
 // iteration of lag): warp 0 issues the loads of all partials of t at the
 // start of t+1, checks their tags after the update and folds them, and the
-// CTA barrier that ends t+1 hands the decision to every warp.  If the loop
+// CTA barrier that ends t+1 hands the decision to every warp (spreading
+// the fold over warps 0..7 measured slower: 168 vs 154 us per C1 solve --
+// eight warps then wait on late partials instead of one).  The neighbours'
+// halo words are loaded before the interior update and polled after it.  If the loop
 // stops at t, the speculative u(t+1) is dropped and u(t) written.  Safety
 // of the reused slots: a band publishes into halo slot t & 1 only after it
 // read its neighbours' rows of t-1, which they sent after consuming its rows
 // of t-2; partial slot t % 4 is rewritten at t+4, after every band has
 // published t+2, i.e. after every band folded t (read at t+1).  Tags are
-// run-unique (tag_base advances by max_it + 4 per launch), so no buffer
+// run-unique (tag_base advances by max_it + 8 per launch), so no buffer
 // needs clearing between launches.  Every value is helm_resident_split's op
 // for op and the MAX is order-free (non-negative floats order as their bits,
 // NaN above +inf): bit-identical, same iteration count.
