@@ -1023,7 +1023,8 @@ __global__ void __launch_bounds__(BLOCK, 1) helm_resident_split(const __grid_con
 // start of t+1, checks their tags after the update and folds them, and the
 // CTA barrier that ends t+1 hands the decision to every warp (spreading
 // the fold over warps 0..7 measured slower: 168 vs 154 us per C1 solve --
-// eight warps then wait on late partials instead of one).  The neighbours'
+// eight warps then wait on late partials instead of one; deciding two
+// iterations late with u(t-1) kept in registers: 156 vs 154 us).  The neighbours'
 // halo words are loaded before the interior update and polled after it.  If the loop
 // stops at t, the speculative u(t+1) is dropped and u(t) written.  Safety
 // of the reused slots: a band publishes into halo slot t & 1 only after it
