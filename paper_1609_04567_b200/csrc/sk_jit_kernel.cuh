@@ -38,6 +38,23 @@ constexpr int kJitTWP = SK_TW + 2 * kJitKA;
 constexpr int kJitTileElems = (SK_TH + 2 * SK_K) * kJitTWP;
 constexpr int kJitElemMax = sizeof(sk_in_t) > sizeof(sk_val_t) ? sizeof(sk_in_t) : sizeof(sk_val_t);
 
+// A thread's running max starts at the type's lowest value and folds every
+// element with one NaN-propagating max (max.NaN for float): the same value
+// as folding from the first element with jit_lmax, NaN for NaN (the payload
+// is not observable), without a per-element first-element flag.
+template <class T>
+__device__ __forceinline__ T jit_lowest() {
+  if constexpr (sizeof(T) == 1) return T(0);  // bool
+  else if constexpr (sizeof(T) == 8 && T(0.5) == T(0)) return (T)(-0x7fffffffffffffffll - 1);
+  else return (T)(-INFINITY);
+}
+template <class T>
+__device__ __forceinline__ T jit_max_fast(T a, T b) {
+  if constexpr (sizeof(T) == 4) return max_nan(a, b);
+  else if constexpr (sizeof(T) == 8 && T(0.5) != T(0)) return max_nan(a, b);
+  else return b > a ? b : a;
+}
+
 template <class T>
 __device__ __forceinline__ T jit_lmax(T a, T b) {  // NaN-propagating, as rmax
   return (a != a) ? a : ((b != b) ? b : (b > a ? b : a));
@@ -232,6 +249,9 @@ __device__ __forceinline__ void jit_rows(const JitArgs& a, const V* tile, const 
   const long long estep = (long long)RS * a.env.pitch[0];
   sk_val_t* bp = back + (long long)(t0 + ty) * g.pitch + gj;
   const long long bstep = (long long)RS * g.pitch;
+#ifdef SK_LOCAL_MAX
+  if (ty < nr) st.lany = true;
+#endif
   for (int lr = ty; lr < nr; lr += RS) {
     SkErr err;
     sk_val_t nw;
@@ -246,8 +266,7 @@ __device__ __forceinline__ void jit_rows(const JitArgs& a, const V* tile, const 
     *bp = nw;
     if (err.code) jit_fail(a.L.st, (long long)nb.i * cols + gj, err.code);
 #ifdef SK_LOCAL_MAX
-    st.lmax = st.lany ? jit_lmax(st.lmax, d) : d;
-    st.lany = true;
+    st.lmax = jit_max_fast(st.lmax, d);
 #else
     st.acc = comb(st.acc, (double)d);
 #endif
@@ -284,7 +303,7 @@ __device__ __forceinline__ void jit_sweep(const JitArgs& a, long long it, V* til
     const int c0 = cb * SK_TW;
     double acc = neutral;
 #ifdef SK_LOCAL_MAX
-    sk_delta_t lmax = 0;
+    sk_delta_t lmax = jit_lowest<sk_delta_t>();
     bool lany = false;
 #endif
     const int gj = c0 + tx;
