@@ -1084,7 +1084,6 @@ __global__ void __launch_bounds__(BLOCK, 1) helm_resident_ll(const __grid_consta
   __shared__ T s_edge[2][RMAX][2][NW];
   __shared__ unsigned s_max[3];
   __shared__ int s_dec[2];
-  __shared__ float s_val[2];
   extern __shared__ __align__(16) unsigned char s_dyn[];
   T* s_f = reinterpret_cast<T*>(s_dyn);  // f of this band, RMAX rows x kFP
   constexpr int kFP = BLOCK * VEC;
