@@ -427,24 +427,50 @@ __global__ void __launch_bounds__(kRB, kMinBlocks) restore_sweep(const __grid_co
 
 // ---- flagged-list construction: count per segment, scan, scatter (ordered)
 
-constexpr int kSeg = 4096;  // pixels per segment (one CTA)
+constexpr int kSeg = 4096;  // pixels per segment (one CTA of 256 threads x 16 pixels)
 
-__global__ void flag_count(const unsigned char* mask, long long mpitch, int rows, int cols,
-                           int* seg_count) {
-  const long long npix = (long long)rows * cols;
-  const long long s0 = (long long)blockIdx.x * kSeg;
-  int n = 0;
-  for (long long p = s0 + threadIdx.x; p < s0 + kSeg && p < npix; p += blockDim.x) {
-    const int i = (int)(p / cols), j = (int)(p - (long long)i * cols);
-    n += mask[(long long)i * mpitch + j] == 1;
+// Flags (mask byte == 1) of the 16 row-major pixels p .. p+15 as bits 0..15:
+// one 16-byte load and four byte compares when the run lies inside one
+// aligned row (the common case), byte by byte with row wrap otherwise.
+__device__ __forceinline__ unsigned flag_bits16(const unsigned char* mask, long long mpitch, int cols,
+                                                long long npix, long long p) {
+  if (p >= npix) return 0u;
+  const long long i = p / cols;
+  int j = (int)(p - i * cols);
+  const unsigned char* row = mask + i * mpitch;
+  unsigned bits = 0u;
+  if (j + 16 <= cols && p + 16 <= npix && (reinterpret_cast<unsigned long long>(row + j) & 15) == 0) {
+    const uint4 v = *reinterpret_cast<const uint4*>(row + j);
+    const unsigned w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const unsigned eq = __vcmpeq4(w[q], 0x01010101u);  // 0xff per byte equal to 1
+      bits |= ((eq & 1u) | ((eq >> 7) & 2u) | ((eq >> 14) & 4u) | ((eq >> 21) & 8u)) << (4 * q);
+    }
+  } else {
+    for (int k = 0; k < 16 && p + k < npix; ++k) {
+      bits |= (unsigned)(row[j] == 1) << k;
+      if (++j == cols) {
+        j = 0;
+        row += mpitch;
+      }
+    }
   }
+  return bits;
+}
+
+__global__ void __launch_bounds__(256) flag_count(const unsigned char* mask, long long mpitch, int rows,
+                                                  int cols, int* seg_count) {
+  const long long npix = (long long)rows * cols;
+  const long long p = (long long)blockIdx.x * kSeg + 16 * threadIdx.x;
+  int n = __popc(flag_bits16(mask, mpitch, cols, npix, p));
   n = __reduce_add_sync(0xffffffffu, n);
-  __shared__ int ws[32];
+  __shared__ int ws[8];
   if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = n;
   __syncthreads();
   if (threadIdx.x == 0) {
     int t = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += ws[w];
+    for (int w = 0; w < 8; ++w) t += ws[w];
     seg_count[blockIdx.x] = t;
   }
 }
@@ -483,35 +509,31 @@ __global__ void flag_scan(int* seg, int nseg) {  // exclusive, single CTA
   }
 }
 
-__global__ void flag_scatter(const unsigned char* mask, long long mpitch, int rows, int cols,
-                             const int* seg_off, int* list) {
+// Each thread owns 16 consecutive pixels of the segment: an exclusive scan of
+// the threads' flag counts gives every thread its slot run, so the list
+// comes out in pixel order with one barrier.
+__global__ void __launch_bounds__(256) flag_scatter(const unsigned char* mask, long long mpitch, int rows,
+                                                    int cols, const int* seg_off, int* list) {
   const long long npix = (long long)rows * cols;
-  const long long s0 = (long long)blockIdx.x * kSeg;
-  __shared__ int base;
-  __shared__ int wcount[32];
-  if (threadIdx.x == 0) base = seg_off[blockIdx.x];
+  const long long p = (long long)blockIdx.x * kSeg + 16 * threadIdx.x;
+  unsigned bits = flag_bits16(mask, mpitch, cols, npix, p);
+  const int n = __popc(bits);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int x = n;  // inclusive warp scan
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  __shared__ int wsum[8];
+  if (lane == 31) wsum[w] = x;
   __syncthreads();
-  for (long long p0 = s0; p0 < s0 + kSeg && p0 < npix; p0 += blockDim.x) {
-    const long long p = p0 + threadIdx.x;
-    bool f = false;
-    if (p < s0 + kSeg && p < npix) {
-      const int i = (int)(p / cols), j = (int)(p - (long long)i * cols);
-      f = mask[(long long)i * mpitch + j] == 1;
-    }
-    const unsigned bal = __ballot_sync(0xffffffffu, f);
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    if (lane == 0) wcount[w] = __popc(bal);
-    __syncthreads();
-    int before = 0;
-    for (int k = 0; k < w; ++k) before += wcount[k];
-    if (f) list[base + before + __popc(bal & ((1u << lane) - 1))] = (int)p;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int t = 0;
-      for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += wcount[k];
-      base += t;
-    }
-    __syncthreads();
+  int before = seg_off[blockIdx.x] + x - n;
+  for (int k = 0; k < w; ++k) before += wsum[k];
+  while (bits) {
+    const int b = __ffs(bits) - 1;
+    list[before++] = (int)(p + b);
+    bits &= bits - 1;
   }
 }
 
