@@ -209,21 +209,20 @@ def run_ours(args):
                                             g_u0, env=g_f, executor=executor)
         return out, rep
 
-    ex = sk.DeviceExecutor(1, timing=True)
+    # 1) value: the production path (one graph-WHILE loop per solve, the
+    #    device decides the stop; no per-sweep events, no host round trip)
+    ex = sk.DeviceExecutor(1)
     for _ in range(args.warmup):
         out, rep = solve(ex)
     torch.cuda.synchronize()
     iters = rep.iterations
     ex.launches = 0
-    kernel_ms, kernel_n = 0.0, 0
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         start.record()
         for _ in range(args.steps):
             out, rep = solve(ex)
-            kernel_ms += ex.last_kernel_time[0]
-            kernel_n += ex.last_kernel_time[1]
             out_last = out
             del out
         stop.record()
@@ -231,6 +230,19 @@ def run_ours(args):
     ms = start.elapsed_time(stop) / args.steps
     cells = float(n) * n * rep.iterations
     value = cells / (ms / 1e3)
+    # 2) the same solves with per-sweep CUDA events on the launching stream
+    #    (batched launches): the roofline's kernel duration
+    ext = sk.DeviceExecutor(1, timing=True)
+    solve(ext)
+    kernel_ms, kernel_n = 0.0, 0
+    torch.cuda.synchronize()
+    for _ in range(max(1, min(args.steps, 3))):
+        o2, r2 = solve(ext)
+        assert r2.iterations == rep.iterations and r2.final_reduce == rep.final_reduce, r2
+        kernel_ms += ext.last_kernel_time[0]
+        kernel_n += ext.last_kernel_time[1]
+        del o2
+    torch.cuda.synchronize()
 
     # parity on the benchmark config itself: iterations, final reduce and
     # the output grid against the pinned oracle (tests/golden/golden_prod.json)
@@ -338,7 +350,11 @@ def run_ours(args):
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": "helmholtz_sweep<float> (fused stencil+|delta|+max+loop test)",
                      "alg_bytes_per_launch": alg_bytes, "avg_kernel_ms": avg_kernel_ms,
-                     "kernel_launches_timed": kernel_n, "peak_source": peak_kind},
+                     "kernel_launches_timed": kernel_n, "peak_source": peak_kind,
+                     "timing": "per-sweep CUDA events on the launching stream over the same "
+                               "solves run with batched launches; value is the graph-WHILE "
+                               "production path (ms_per_step / iterations_per_step = "
+                               f"{ms / rep.iterations:.4f} ms per sweep there)"},
         "cpu_baseline": {"value": cpu_rate, "unit": "cell-updates/s", "cores": cores,
                          "kind": "port", "sample": sample},
         "clocks": clk.summary(),
