@@ -52,6 +52,31 @@ def run(count, do_up=True, do_down=True):
     torch.cuda.synchronize()
 
 
+def run_api(count):
+    """the C4 form: Grid.prefetch_device / prefetch_host(out=) (the public API)"""
+    def host_inputs():
+        return sk.Grid.from_tensor(h0), sk.Grid.from_tensor(hf)
+
+    nxt = tuple(g.prefetch_device() for g in host_inputs())
+    prev = None
+    for k in range(count):
+        gu, gf = nxt
+        if k + 1 < count:
+            nxt = tuple(g.prefetch_device() for g in host_inputs())
+        o, _ = sk.loop_stencil_reduce_d(1, kern, sk.abs_change(), sk.max_combinator(0.0),
+                                        sk.Condition.below(1e-4), gu, env=gf, executor=ex)
+        o.prefetch_host(out=houts[k % 2].numpy())
+        if prev is not None:
+            prev.to_array()
+        prev = o
+    prev.to_array()
+
+
+run_api(8)
+t0 = time.perf_counter()
+run_api(50)
+print(f"{'grid api':14s} {(time.perf_counter() - t0) / 50 * 1e3:.3f} ms per solve", flush=True)
+
 for name, u, d in (("bench form", True, True), ("no read-back", True, False), ("no upload", False, True),
                    ("neither", False, False)):
     run(8, u, d)
