@@ -1505,7 +1505,15 @@ int launch_resident_ll(sk_run* r, const LoopCtl& L, cudaStream_t s, const HelmAr
   const size_t pbytes = (size_t)4 * nb * 8;
   const size_t bytes = pbytes + (size_t)2 * nb * 2 * cpad * 8;
   const long long span = L.cond.max_it + 8;
-  LLScratch& sc = scratch[std::make_pair(r->device, s)];
+  const auto skey = std::make_pair(r->device, s);
+  if (scratch.size() >= 32 && scratch.find(skey) == scratch.end()) {
+    // many streams seen (e.g. a new stream per call): drop the cache rather
+    // than keep a buffer per stream forever (cudaFree waits for the device)
+    for (auto& kv : scratch)
+      if (kv.second.p) cudaFree(kv.second.p);
+    scratch.clear();
+  }
+  LLScratch& sc = scratch[skey];
   bool clear = false;
   if (!sc.p || sc.bytes < bytes) {
     if (sc.p) SK_CUDA(cudaFreeAsync(sc.p, s));

@@ -89,3 +89,24 @@ def test_ll_resident_back_to_back_caps():
             assert rep.iterations == cap and rep.exhausted, (rep_i, cap)
             assert rep.final_reduce == ref[cap][1]
             assert np.array_equal(got.view(np.uint32), ref[cap][0].view(np.uint32)), (rep_i, cap)
+
+
+def test_ll_resident_many_streams():
+    """Solves issued from 40 different CUDA streams (the exchange buffer is
+    cached per stream, the cache dropped past 32 streams): every result
+    equals the default-stream one."""
+    import torch
+    from paper_1609_04567_b200.apps import HelmholtzConfig
+
+    n, m = 512, 640
+    rng = np.random.default_rng(11)
+    u0 = rng.random((n, m)).astype(np.float32)
+    f = rng.random((n, m)).astype(np.float32)
+    cfg = HelmholtzConfig(rows=n, cols=m, alpha=0.5, dx=0.5, dy=0.25, relax=0.9)
+    want, rep0 = _solve(u0, f, cfg, "abs", 1e-4, 60)
+    for _ in range(40):
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            got, rep = _solve(u0, f, cfg, "abs", 1e-4, 60)
+        assert rep.iterations == rep0.iterations and rep.final_reduce == rep0.final_reduce
+        assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
