@@ -1010,7 +1010,7 @@ __global__ void __launch_bounds__(BLOCK, 1) helm_resident_split(const __grid_con
   }
 }
 
-// ---- barrier-free resident loop (fp32, one partition, MAX of |delta| or delta^2)
+// ---- barrier-free resident loop (fp32, one partition, MAX or SUM of |delta| or delta^2)
 // helm_resident_split without the grid barrier.  Every value a band sends
 // carries its iteration in the same 8-byte word ("LL" words: tag << 32 |
 // fp32 bits), stored with one relaxed 8-byte store and polled with relaxed
@@ -1073,7 +1073,7 @@ __device__ __forceinline__ VecN<float, VEC> ll_load_row(const unsigned long long
   return r;
 }
 
-template <int BLOCK, int VEC, int RMAX, int DELTA>
+template <int BLOCK, int VEC, int RMAX, int DELTA, int REDUCE>
 __global__ void __launch_bounds__(BLOCK, 1) helm_resident_ll(const __grid_constant__ HelmArgs<float> a,
                                                              unsigned long long* xbuf, unsigned long long* parts,
                                                              unsigned tag_base) {
@@ -1082,7 +1082,9 @@ __global__ void __launch_bounds__(BLOCK, 1) helm_resident_ll(const __grid_consta
   constexpr int NW = BLOCK / 32;
   constexpr int kPS = 4;  // partial slots
   __shared__ T s_edge[2][RMAX][2][NW];
+  constexpr bool SUM = REDUCE == SK_REDUCE_SUM;
   __shared__ unsigned s_max[3];
+  __shared__ double s_sum[3][NW];  // SUM: the warps' partial sums of t, by t % 3
   __shared__ int s_dec[2];
   extern __shared__ __align__(16) unsigned char s_dyn[];
   T* s_f = reinterpret_cast<T*>(s_dyn);  // f of this band, RMAX rows x kFP
@@ -1127,6 +1129,9 @@ __global__ void __launch_bounds__(BLOCK, 1) helm_resident_ll(const __grid_consta
   VecN<T, VEC> up = (active && has_up) ? ldgN<T, VEC>(src + (long long)(r0 - 1) * g.src_pitch + col) : zeroN<T, VEC>();
   VecN<T, VEC> dn = (active && has_dn) ? ldgN<T, VEC>(src + (long long)r1 * g.src_pitch + col) : zeroN<T, VEC>();
   T accm = -INFINITY;
+  double rsum[RMAX];  // SUM: each row's delta sum (added in row order at publish)
+#pragma unroll
+  for (int r = 0; r < RMAX; ++r) rsum[r] = 0.0;
   int sp = (int)((it - 1) & 1);
   const T ax = a.ax, ay = a.ay, bb = a.b, keep = a.keep, relax = a.relax;
   const bool has_lw = warp > 0, has_rw = warp + 1 < NW;
@@ -1158,6 +1163,7 @@ __global__ void __launch_bounds__(BLOCK, 1) helm_resident_ll(const __grid_consta
       for (int e = 0; e < VEC; ++e) q[e] = xdiv(num[e], bb);
     }
     VecN<T, VEC> o;
+    T dd[VEC];
 #pragma unroll
     for (int e = 0; e < VEC; ++e) {
       const T out = xadd(xmul(keep, cen.v[e]), q[e]);
@@ -1166,12 +1172,16 @@ __global__ void __launch_bounds__(BLOCK, 1) helm_resident_ll(const __grid_consta
       T d;
       if (DELTA == SK_DELTA_ABS) {
         d = tabs(xsub(out, cen.v[e]));
-      } else {
+      } else if (DELTA == SK_DELTA_SQUARE) {
         const T t = xsub(out, cen.v[e]);
         d = xmul(t, t);
+      } else {
+        d = out;
       }
-      if (in) accm = max_nan(accm, d);
+      if constexpr (SUM) dd[e] = in ? d : T(0);
+      else if (in) accm = max_nan(accm, d);
     }
+    if constexpr (SUM) rsum[r] = (double)sumN<T, VEC>(dd);  // helm_resident's row term
     return o;
   };
   auto sedge = [&](int slot, const VecN<T, VEC>* x) {
@@ -1204,18 +1214,39 @@ __global__ void __launch_bounds__(BLOCK, 1) helm_resident_ll(const __grid_consta
       ll_store_row<VEC>(x + xp, tag, w[RMAX - 1]);
     }
     sedge((int)(t & 1), w);
-    T m = accm;
+    if constexpr (SUM) {
+      // block_reduce's order: rows in order per thread, xor tree per warp,
+      // warps in order (send_partial)
+      double v = 0.0;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = max_nan(m, __shfl_xor_sync(FULL, m, o));
-    // no valid element: -inf -> 0, the identity of a non-negative max
-    if (lane == 0 && !(m < T(0))) atomicMax(&s_max[t % 3], __float_as_uint(m));
-    accm = -INFINITY;
+      for (int r = 0; r < RMAX; ++r)
+        if (r < R) v += rsum[r];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v = v + __shfl_xor_sync(FULL, v, o);
+      if (lane == 0) s_sum[t % 3][warp] = v;
+    } else {
+      T m = accm;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m = max_nan(m, __shfl_xor_sync(FULL, m, o));
+      // no valid element: -inf -> 0, the identity of a non-negative max
+      if (lane == 0 && !(m < T(0))) atomicMax(&s_max[t % 3], __float_as_uint(m));
+      accm = -INFINITY;
+    }
   };
   // the CTA's partial of t (after the barrier that completed s_max[t % 3])
   auto send_partial = [&](long long t) {
     if (threadIdx.x == 0) {
-      ll_st1(parts + (long long)(t % kPS) * nb + blockIdx.x, ll_pack(tag_base + (unsigned)t, __uint_as_float(s_max[t % 3])));
-      s_max[(t + 2) % 3] = 0u;  // slot of t+2 (t-1's partial went out last iteration)
+      const unsigned tg = tag_base + (unsigned)t;
+      if constexpr (SUM) {
+        double v = 0.0;
+        for (int w2 = 0; w2 < NW; ++w2) v = v + s_sum[t % 3][w2];
+        const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+        ll_st2(parts + ((long long)(t % kPS) * nb + blockIdx.x) * 2,
+               ((unsigned long long)tg << 32) | (bits & 0xffffffffull), ((unsigned long long)tg << 32) | (bits >> 32));
+      } else {
+        ll_st1(parts + (long long)(t % kPS) * nb + blockIdx.x, ll_pack(tg, __uint_as_float(s_max[t % 3])));
+        s_max[(t + 2) % 3] = 0u;  // slot of t+2 (t-1's partial went out last iteration)
+      }
     }
   };
   // iteration `it` in full (its halo rows come straight from the input)
@@ -1234,14 +1265,16 @@ __global__ void __launch_bounds__(BLOCK, 1) helm_resident_ll(const __grid_consta
     const unsigned tag = tag_base + (unsigned)it;
     // warp 0: the partials of `it` (published one CTA barrier ago by this
     // band, a little earlier or later by the others)
-    constexpr int kPL = 8;  // up to 256 bands
-    unsigned long long pv[kPL];
+    constexpr int kPL = 5;  // up to 160 bands (one per SM)
+    constexpr int kPW = SUM ? 2 : 1;  // tagged words per partial
+    unsigned long long pv[kPL][kPW];
+    const unsigned long long* ps = parts + (long long)(it % kPS) * nb * kPW;
     if (warp == 0) {
-      const unsigned long long* ps = parts + (long long)(it % kPS) * nb;
 #pragma unroll
       for (int k = 0; k < kPL; ++k) {
         const int c = lane + 32 * k;
-        pv[k] = c < nb ? ll_ld1(ps + c) : 0ull;
+#pragma unroll
+        for (int q = 0; q < kPW; ++q) pv[k][q] = c < nb ? ll_ld1(ps + (long long)c * kPW + q) : 0ull;
       }
     }
     // the neighbours' rows of `it`: first loads issued before the interior
@@ -1269,25 +1302,55 @@ __global__ void __launch_bounds__(BLOCK, 1) helm_resident_ll(const __grid_consta
     edges();
     publish(it + 1);
     if (warp == 0) {
-      const unsigned long long* ps = parts + (long long)(it % kPS) * nb;
-      unsigned m = 0u;
 #pragma unroll
       for (int k = 0; k < kPL; ++k) {
         const int c = lane + 32 * k;
         if (c < nb) {
-          while ((unsigned)(pv[k] >> 32) != tag) pv[k] = ll_ld1(ps + c);
-          const unsigned b = (unsigned)pv[k];
-          m = b > m ? b : m;
+#pragma unroll
+          for (int q = 0; q < kPW; ++q)
+            while ((unsigned)(pv[k][q] >> 32) != tag) pv[k][q] = ll_ld1(ps + (long long)c * kPW + q);
         }
       }
+      double acc;
+      if constexpr (SUM) {
+        // fold_and_decide's tree emulated over the CTA's NW warps: thread
+        // c holds 0.0 + partial[c] (or the neutral 0.0), xor tree per warp,
+        // warps summed in order, then identity + sum
+        double r = 0.0;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const unsigned x = __shfl_xor_sync(FULL, m, o);
-        m = x > m ? x : m;
+        for (int w2 = 0; w2 < NW; ++w2) {
+          double x = 0.0;
+          if (w2 < kPL) {
+            const int c = lane + 32 * w2;
+            if (c < nb)
+              x = 0.0 + __longlong_as_double((long long)(((pv[w2][1] & 0xffffffffull) << 32) |
+                                                           (pv[w2][0] & 0xffffffffull)));
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) x = x + __shfl_xor_sync(FULL, x, o);
+          r = r + x;
+        }
+        const OpCombine comb{SK_REDUCE_SUM};
+        acc = comb.fold(a.L.identity, r);
+      } else {
+        unsigned m = 0u;
+#pragma unroll
+        for (int k = 0; k < kPL; ++k) {
+          const int c = lane + 32 * k;
+          if (c < nb) {
+            const unsigned b = (unsigned)pv[k][0];
+            m = b > m ? b : m;
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const unsigned x = __shfl_xor_sync(FULL, m, o);
+          m = x > m ? x : m;
+        }
+        const OpCombine comb{SK_REDUCE_MAX};
+        acc = comb.fold(a.L.identity, (double)__uint_as_float(m));
       }
       if (lane == 0) {
-        const OpCombine comb{SK_REDUCE_MAX};
-        const double acc = comb.fold(a.L.identity, (double)__uint_as_float(m));
         const int c = eval_cond(a.L.cond, acc, it, a.L.flagged_dev);
         const int capped = it >= a.L.cond.max_it;
         s_dec[it & 1] = c || capped;
@@ -1443,22 +1506,27 @@ ResFn<T> pick_res_b(int delta, int reduce) {
 using ResLLFn = void (*)(const HelmArgs<float>, unsigned long long*, unsigned long long*, unsigned);
 
 template <int RMAX>
-ResLLFn pick_res_ll(int delta) {
-  if (delta == SK_DELTA_ABS) return helm_resident_ll<512, 2, RMAX, SK_DELTA_ABS>;
-  if (delta == SK_DELTA_SQUARE) return helm_resident_ll<512, 2, RMAX, SK_DELTA_SQUARE>;
+ResLLFn pick_res_ll(int delta, int reduce) {
+  if (reduce == SK_REDUCE_MAX) {  // (MAX of a non-negative delta: partials order as bits)
+    if (delta == SK_DELTA_ABS) return helm_resident_ll<512, 2, RMAX, SK_DELTA_ABS, SK_REDUCE_MAX>;
+    if (delta == SK_DELTA_SQUARE) return helm_resident_ll<512, 2, RMAX, SK_DELTA_SQUARE, SK_REDUCE_MAX>;
+  } else if (reduce == SK_REDUCE_SUM) {
+    if (delta == SK_DELTA_ABS) return helm_resident_ll<512, 2, RMAX, SK_DELTA_ABS, SK_REDUCE_SUM>;
+    if (delta == SK_DELTA_SQUARE) return helm_resident_ll<512, 2, RMAX, SK_DELTA_SQUARE, SK_REDUCE_SUM>;
+  }
   return nullptr;
 }
 
-ResLLFn pick_res_ll_band(int band, int delta) {
+ResLLFn pick_res_ll_band(int band, int delta, int reduce) {
   switch (band) {
-    case 1: return pick_res_ll<1>(delta);
-    case 2: return pick_res_ll<2>(delta);
-    case 3: return pick_res_ll<3>(delta);
-    case 4: return pick_res_ll<4>(delta);
-    case 5: return pick_res_ll<5>(delta);
-    case 6: return pick_res_ll<6>(delta);
-    case 7: return pick_res_ll<7>(delta);
-    case 8: return pick_res_ll<8>(delta);
+    case 1: return pick_res_ll<1>(delta, reduce);
+    case 2: return pick_res_ll<2>(delta, reduce);
+    case 3: return pick_res_ll<3>(delta, reduce);
+    case 4: return pick_res_ll<4>(delta, reduce);
+    case 5: return pick_res_ll<5>(delta, reduce);
+    case 6: return pick_res_ll<6>(delta, reduce);
+    case 7: return pick_res_ll<7>(delta, reduce);
+    case 8: return pick_res_ll<8>(delta, reduce);
     default: return nullptr;
   }
 }
@@ -1482,10 +1550,10 @@ int launch_resident_ll(sk_run* r, const LoopCtl& L, cudaStream_t s, const HelmAr
   const int sms = device_sms(r->device);
   int band = (int)((p.rows + sms - 1) / sms);
   if (band < 1) band = 1;
-  ResLLFn fn = pick_res_ll_band(band, p.delta_op);
+  ResLLFn fn = pick_res_ll_band(band, p.delta_op, p.reduce_op);
   if (!fn) return SK_ERR_UNSUPPORTED;
   const int nb = (p.rows + band - 1) / band;
-  if (nb > 256) return SK_ERR_UNSUPPORTED;  // warp 0 folds <= 8 partials per lane
+  if (nb > 160) return SK_ERR_UNSUPPORTED;  // warp 0 folds <= 5 partials per lane
   const size_t dyn = (size_t)band * block * 2 * sizeof(float);
   static std::mutex mu;
   static std::map<std::pair<const void*, size_t>, int> occ_cache;
@@ -1502,7 +1570,7 @@ int launch_resident_ll(sk_run* r, const LoopCtl& L, cudaStream_t s, const HelmAr
   }
   if (oit->second < 1 || nb > oit->second * sms) return SK_ERR_UNSUPPORTED;
   const long long cpad = (p.cols + 3) / 4 * 4;
-  const size_t pbytes = (size_t)4 * nb * 8;
+  const size_t pbytes = (size_t)4 * nb * 16;  // 4 slots x bands x (up to) 2 tagged words
   const size_t bytes = pbytes + (size_t)2 * nb * 2 * cpad * 8;
   const long long span = L.cond.max_it + 8;
   const auto skey = std::make_pair(r->device, s);
@@ -1568,11 +1636,12 @@ int launch_resident(sk_run* r, const LoopCtl& L, cudaStream_t s, const HelmArgs<
     vec = want;
     block = 1024 / want;
   }
-  // barrier-free form (helm_resident_ll): fp32, one partition, MAX of
-  // |delta| or delta^2, 2 columns per thread; SK_RES_LL=0 turns it off
+  // barrier-free form (helm_resident_ll): fp32, one partition, MAX or SUM
+  // of |delta| or delta^2, 2 columns per thread; SK_RES_LL=0 turns it off
   const char* ll_env = getenv("SK_RES_LL");
   if constexpr (sizeof(T) == 4) {
-    if (!(ll_env && ll_env[0] == '0') && vec == 2 && r->nparts == 1 && p.reduce_op == SK_REDUCE_MAX &&
+    if (!(ll_env && ll_env[0] == '0') && vec == 2 && r->nparts == 1 &&
+        (p.reduce_op == SK_REDUCE_MAX || p.reduce_op == SK_REDUCE_SUM) &&
         (p.delta_op == SK_DELTA_ABS || p.delta_op == SK_DELTA_SQUARE) && L.cond.max_it < (1ll << 30)) {
       const int rc = launch_resident_ll(r, L, s, base, block);
       if (rc != SK_ERR_UNSUPPORTED) return rc;

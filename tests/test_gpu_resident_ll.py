@@ -19,14 +19,15 @@ import paper_1609_04567_b200 as sk
 pytestmark = pytest.mark.gpu
 
 
-def _solve(u0, f, cfg, delta, tol, max_it, ll=True):
+def _solve(u0, f, cfg, delta, tol, max_it, ll=True, op="max"):
     from paper_1609_04567_b200.apps import helmholtz_kernel
 
     old = os.environ.get("SK_RES_LL")
     os.environ["SK_RES_LL"] = "1" if ll else "0"
     try:
         dl = sk.abs_change() if delta == "abs" else sk.Delta(lambda a, b: (a - b) ** 2, kind="square")
-        out, rep = sk.loop_stencil_reduce_d(1, helmholtz_kernel(cfg), dl, sk.max_combinator(0.0),
+        comb = sk.max_combinator(0.0) if op == "max" else sk.sum_combinator(0.0)
+        out, rep = sk.loop_stencil_reduce_d(1, helmholtz_kernel(cfg), dl, comb,
                                             sk.Condition.below(tol, max_iterations=max_it),
                                             sk.Grid(u0.shape, u0), env=sk.Grid(f.shape, f))
     finally:
@@ -110,3 +111,31 @@ def test_ll_resident_many_streams():
             got, rep = _solve(u0, f, cfg, "abs", 1e-4, 60)
         assert rep.iterations == rep0.iterations and rep.final_reduce == rep0.final_reduce
         assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("delta", ["abs", "sq"])
+def test_ll_resident_sum_matches_barrier_form(shape, delta):
+    """SUM reduces: the barrier-free loop folds the bands' partials in the
+    engine's fixed tree, so grid, iteration count and final value are
+    bit-identical to the barrier form (and within the fp32-sum tolerance of
+    the oracle's pairwise sum)."""
+    from oracle import stencil_oracle as O
+    from paper_1609_04567_b200.apps import HelmholtzConfig
+
+    n, m = shape
+    rng = np.random.default_rng(n * 13 + m)
+    u0 = rng.random((n, m)).astype(np.float32)
+    f = rng.random((n, m)).astype(np.float32)
+    cfg = HelmholtzConfig(rows=n, cols=m, alpha=0.5, dx=0.5, dy=0.25, relax=0.9)
+    tol = 1e-3 * n * m if delta == "abs" else 1e-6 * n * m
+    got, rep = _solve(u0, f, cfg, delta, tol, 60, op="sum")
+    ref, rep0 = _solve(u0, f, cfg, delta, tol, 60, ll=False, op="sum")
+    assert (rep.iterations, rep.exhausted) == (rep0.iterations, rep0.exhausted)
+    assert np.float64(rep.final_reduce).tobytes() == np.float64(rep0.final_reduce).tobytes()
+    assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
+    want, it, v, _ = O.helmholtz_loop(u0, f, O.helmholtz_consts(0.5, 0.5, 0.25, 0.9), delta=delta,
+                                      op="sum", cond=lambda val, i: val < tol, max_iterations=60)
+    assert rep.iterations == it
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+    assert rep.final_reduce == pytest.approx(v, rel=1e-5)
