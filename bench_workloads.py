@@ -394,17 +394,37 @@ def c3(args, ClockSampler, measured_peaks, local=0):
     ms = s.elapsed_time(e) / args.steps
     flagged = int(mask.tensor().sum().item())
     t1 = _restore_iter1_ms(sk, img, mask.tensor())
-    # e2e: host uint8 image in, host fp64 restored image out
+    # e2e: host uint8 image in, host fp64 restored image out, through the
+    # public API.  Headline: the image in pinned host memory (one DMA up)
+    # and the result read into a pinned host array with prefetch_host(out=)
+    # (one DMA down); drop_in: numpy in, a fresh numpy array out (pageable
+    # copies; the fresh 134 MB array's first-touch page faults dominate)
+    hin = torch.from_numpy(noisy).pin_memory()
+    hout = torch.empty(noisy.shape, dtype=torch.float64).pin_memory().numpy()
+
     def e2e():
+        gh = sk.Grid.from_tensor(hin)
+        m2 = amf_detect(gh)
+        o2, _ = restore_regularize(gh, m2)
+        o2.prefetch_host(out=hout)
+        return o2.to_array()
+
+    def e2e_drop_in():
         gh = sk.Grid.from_array(noisy)
         m2 = amf_detect(gh)
         o2, _ = restore_regularize(gh, m2)
         return o2.to_array()
 
-    e2e()
+    assert np.array_equal(e2e(), e2e_drop_in())
+    ts = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        e2e()
+        ts.append(time.perf_counter() - t0)
+    e2e_s = sorted(ts)[1]
     t0 = time.perf_counter()
-    e2e()
-    e2e_s = time.perf_counter() - t0
+    e2e_drop_in()
+    drop_s = time.perf_counter() - t0
     # CPU: the port on a 1024^2 crop of the same image family, extrapolated x16
     small = _c3_input(1024)
     t0 = time.perf_counter()
@@ -422,7 +442,12 @@ def c3(args, ClockSampler, measured_peaks, local=0):
     line.update({
         "gpu_launches": None,
         "e2e": {"value": 1.0 / e2e_s, "unit": "images/s", "h2d_bytes_per_step": noisy.size,
-                "d2h_bytes_per_step": 8 * noisy.size},
+                "d2h_bytes_per_step": 8 * noisy.size,
+                "mode": "median of 3: amf_detect + restore_regularize on a host grid over pinned "
+                        "memory, the fp64 result read into a pinned host array "
+                        "(prefetch_host(out=)); one image at a time",
+                "drop_in": {"value": 1.0 / drop_s, "mode": "numpy image in (Grid.from_array), "
+                                                          "fresh numpy array out (to_array)"}},
         "roofline": restore_roofline(flagged, t1, "c3"),
         "cpu_baseline": {"value": 1.0 / cpu_s, "unit": "images/s", "cores": 1, "kind": "port",
                          "sample": "oracle AMF + 3 restore sweeps on a 1024^2 image "
