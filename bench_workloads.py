@@ -455,7 +455,9 @@ def c3(args, ClockSampler, measured_peaks, local=0):
                                    "(x16 pixels)"},
         "clocks": clk.summary(),
     })
-    line["gpu_launches"] = 2 * (args.steps)  # one persistent launch per phase per image
+    # per image: one persistent launch per phase (AMF, restore) + the
+    # flagged-list build (count, scan, scatter, bounds)
+    line["gpu_launches"] = 6 * args.steps
     return line
 
 
@@ -600,5 +602,7 @@ def c5(args, ClockSampler, measured_peaks, local=0, world=1, rank=0, width=32):
         "cpu_baseline": cpu_line,
         "clocks": clk.summary(),
     })
-    line["gpu_launches"] = args.steps * 2 * (-(-total // B))
+    # per batch: batched AMF + one persistent restore launch + the
+    # flagged-list build (count, scan, scatter, bounds)
+    line["gpu_launches"] = args.steps * 6 * (-(-total // B))
     return line
