@@ -195,11 +195,27 @@ def _is_absent_obj(o) -> bool:
 _file_cache: dict = {}
 
 
+_node_cache: dict = {}
+
+
 def _func_node(fn):
-    """AST of a function or lambda, located in its source file."""
+    """AST of a function or lambda, located in its source file (memoised per
+    code object: the drop-in loop calls classify the same combinator / delta
+    on every call, and locating it walks the whole file's AST)."""
     code = getattr(fn, "__code__", None)
     if code is None:
         raise TranslateError(f"{fn!r} is not a Python function")
+    hit = _node_cache.get(code)
+    if hit is not None:
+        return hit
+    node = _func_node_uncached(fn, code)
+    if len(_node_cache) > 256:
+        _node_cache.clear()
+    _node_cache[code] = node
+    return node
+
+
+def _func_node_uncached(fn, code):
     fname = code.co_filename
     lines = linecache.getlines(fname)
     if not lines:
