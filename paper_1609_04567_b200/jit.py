@@ -804,8 +804,10 @@ class Translator:
             ok = f"v_{name}_ok" if name in self.absentable else None
             return self._load(name, shape, ok)
         if name in self.nonlocals:
+            _record_dep(self, "nonlocal", name, self.nonlocals[name])
             return self._pyval(self.nonlocals[name])
         if name in self.fglobals:
+            _record_dep(self, "global", name, self.fglobals[name])
             return self._pyval(self.fglobals[name])
         if hasattr(builtins, name):
             return Val("obj", obj=getattr(builtins, name))
@@ -1657,7 +1659,137 @@ def _centre_offset(c: str, ax: str):
     return 0 if m.group(1) is None else (int(m.group(2)) if m.group(1) == "+" else -int(m.group(2)))
 
 
+# ---------------------------------------------------------------- translation cache
+# Translating an elemental takes ~2 ms of Python per loop call; a drop-in
+# user calling the loop again with the same functions gets the Program back
+# from this cache.  Every global / nonlocal value the translation read is
+# recorded and re-checked on a hit (same object, or an equal immutable
+# scalar), so a rebound constant or helper re-translates; programs that read
+# any mutable value (lists, arrays, objects) are never cached.
+_dep_rec = threading.local()
+_tr_cache: dict = {}
+_IMMUT = (bool, int, float, complex, str, bytes, type(None), np.number, np.bool_, np.dtype)
+
+
+def _record_dep(tr, scope: str, name: str, value) -> None:
+    deps = getattr(_dep_rec, "deps", None)
+    if deps is not None:
+        deps.append((tr.role, tr.fn if tr.role == "helper" else None, scope, name, value))
+
+
+def _stable(v) -> bool:
+    import types
+
+    if isinstance(v, _IMMUT):
+        return True
+    if isinstance(v, (types.ModuleType, types.FunctionType, types.BuiltinFunctionType, type, np.ufunc)):
+        return True
+    from .grid import ABSENT
+
+    if v is ABSENT:  # the reference's out-of-grid sentinel (a singleton)
+        return True
+    return isinstance(v, tuple) and all(_stable(x) for x in v)
+
+
+def _same(cur, v) -> bool:
+    if cur is v:
+        return True
+    if type(cur) is not type(v):
+        return False
+    if isinstance(v, tuple):
+        return len(cur) == len(v) and all(_same(a, b) for a, b in zip(cur, v))
+    if isinstance(v, (float, complex, np.inexact)):
+        return repr(cur) == repr(v)  # -0.0 vs 0.0, NaN
+    if isinstance(v, _IMMUT):
+        return bool(cur == v)
+    return False
+
+
+def _program_key(plan, grid, dims):
+    from .patterns import combinator_kind, delta_kind
+
+    fn = plan.fn
+    if getattr(fn, "device", None) is not None:
+        return None
+    point = getattr(fn, "point", None)
+    code = getattr(point, "__code__", None)
+    if code is None:
+        return None
+    env_kind, env_grids, env_obj = _env_spec(plan.env)
+    if env_obj is not None:
+        return None
+    op, delta = plan.op, plan.delta
+    try:
+        opk = combinator_kind(op)
+    except DeviceUnsupported:
+        opk = getattr(getattr(op, "fn", None), "__code__", None)
+        if opk is None:
+            return None
+    if delta is None:
+        dk = None
+    else:
+        try:
+            dk = delta_kind(delta)
+        except DeviceUnsupported:
+            dk = getattr(getattr(delta, "fn", None), "__code__", None)
+            if dk is None:
+                return None
+    pad, ident = fn.pad_value, op.identity
+    if not (_stable(pad) and _stable(ident)):
+        return None
+    return (code, plan.k, bool(plan.indexed), fn.pad_mode, type(pad), repr(pad), grid_dtype(grid),
+            tuple(grid_dtype(g) for g in env_grids), env_kind, grid.ndim, tuple(grid.dims),
+            tuple(dims) if dims is not None else None, opk, dk, type(ident), repr(ident),
+            os.environ.get("SK_JIT_MINB"), os.environ.get("SK_JIT_SMEM_KB"))
+
+
+def _deps_valid(deps, plan) -> bool:
+    roles = {"elemental": plan.fn.point, "combine": getattr(plan.op, "fn", None),
+             "delta": getattr(plan.delta, "fn", None)}
+    for role, fobj, scope, name, val in deps:
+        f = fobj if role == "helper" else roles.get(role)
+        if f is None:
+            return False
+        if scope == "global":
+            g = getattr(f, "__globals__", None)
+            if g is None or name not in g:
+                return False
+            cur = g[name]
+        else:
+            code = getattr(f, "__code__", None)
+            if code is None or name not in code.co_freevars or f.__closure__ is None:
+                return False
+            try:
+                cur = f.__closure__[code.co_freevars.index(name)].cell_contents
+            except ValueError:  # an empty cell
+                return False
+        if not _same(cur, val):
+            return False
+    return True
+
+
 def build_program(plan, grid, dims=None) -> Program:
+    """The CUDA program of a plan whose elemental has no built-in kernel
+    (translated by _build_program, or from the translation cache)."""
+    key = _program_key(plan, grid, dims)
+    if key is not None:
+        hit = _tr_cache.get(key)
+        if hit is not None and _deps_valid(hit[0], plan):
+            return hit[1]
+    _dep_rec.deps = []
+    try:
+        prog = _build_program(plan, grid, dims)
+        deps = _dep_rec.deps
+    finally:
+        _dep_rec.deps = None
+    if key is not None and all(_stable(d[4]) for d in deps):
+        if len(_tr_cache) > 256:
+            _tr_cache.clear()
+        _tr_cache[key] = (deps, prog)
+    return prog
+
+
+def _build_program(plan, grid, dims=None) -> Program:
     """The CUDA program of a plan whose elemental has no built-in kernel.
     `dims`: the global grid dims when `grid` is one rank's row block."""
     fn = plan.fn
