@@ -1280,8 +1280,9 @@ __global__ void __launch_bounds__(BLOCK, 1) helm_resident_ll(const __grid_consta
     // the neighbours' rows of `it`: first loads issued before the interior
     // update (usually already tagged `it` when they land), polled after it
     const unsigned long long* xb = xbuf + (long long)((it & 1) * nb) * 2 * xp + col;
-    const unsigned long long* pu = xb + ((long long)(blockIdx.x - 1) * 2 + 1) * xp;
-    const unsigned long long* pd = xb + ((long long)(blockIdx.x + 1) * 2) * xp;
+    // (only formed for existing neighbours: no pointer past either end)
+    const unsigned long long* pu = has_up ? xb + ((long long)(blockIdx.x - 1) * 2 + 1) * xp : xb;
+    const unsigned long long* pd = has_dn ? xb + ((long long)(blockIdx.x + 1) * 2) * xp : xb;
     const bool lu = active && has_up, ld = active && has_dn;
     unsigned long long wu[VEC], wd[VEC];
 #pragma unroll
