@@ -139,3 +139,29 @@ def test_ll_resident_sum_matches_barrier_form(shape, delta):
     assert rep.iterations == it
     assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
     assert rep.final_reduce == pytest.approx(v, rel=1e-5)
+
+
+def test_ll_resident_seeded_sweep():
+    """40 seeded random geometries (rows 1..1184, cols 1..1024), MAX/SUM x
+    |d| / d^2, random caps and tolerances: the barrier-free loop equals the
+    barrier form bit for bit (grid, iterations, exhaustion, final value)."""
+    from paper_1609_04567_b200.apps import HelmholtzConfig
+
+    rng = np.random.default_rng(2024)
+    for case in range(40):
+        n = int(rng.integers(1, 1185))
+        m = int(rng.integers(1, 1025))
+        op = ("max", "sum")[case % 2]
+        delta = ("abs", "sq")[(case // 2) % 2]
+        u0 = rng.random((n, m)).astype(np.float32)
+        f = rng.random((n, m)).astype(np.float32)
+        cfg = HelmholtzConfig(rows=n, cols=m, alpha=float(rng.uniform(0.2, 2.0)), dx=0.5, dy=0.25,
+                              relax=float(rng.uniform(0.5, 1.0)))
+        tol = float(10 ** rng.uniform(-6, -2)) * (n * m if op == "sum" else 1)
+        cap = int(rng.integers(1, 50))
+        got, rep = _solve(u0, f, cfg, delta, tol, cap, op=op)
+        ref, rep0 = _solve(u0, f, cfg, delta, tol, cap, ll=False, op=op)
+        what = (case, n, m, op, delta, cap)
+        assert (rep.iterations, rep.exhausted) == (rep0.iterations, rep0.exhausted), what
+        assert np.float64(rep.final_reduce).tobytes() == np.float64(rep0.final_reduce).tobytes(), what
+        assert np.array_equal(got.view(np.uint32), ref.view(np.uint32)), what
